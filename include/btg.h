@@ -1,0 +1,141 @@
+/*
+ * btg.h — C ABI of the B200-native FFT block-Toeplitz matvec (libbtg.so).
+ *
+ * Drop-in boundary for the reference's operator API (paths are relative to
+ * /root/reference/proj). The reference is C++ with value semantics; this ABI
+ * is what its FFI for the hot path binds: plain pointers and sizes, an opaque
+ * handle that owns the device-resident frequency-domain operator, status codes
+ * instead of exceptions. include/btoep_gpu.hpp re-exposes the reference's C++
+ * signatures on top of it; INTEGRATION.md shows the bindings.
+ *
+ * Layouts (identical to the reference's, so no caller-side reordering):
+ *   blocks  TOSI first block column  blocks[(k*N_d + i)*N_m + j], k < N_t
+ *           (CompactP2O::entry, block_operator.cpp:147-153)
+ *   m, d    SOTI space-time vectors  v[s*N_t + t]   (space_time.hpp:10-11)
+ *           nrhs > 1 stacks right-hand sides: v[(r*dim + s)*N_t + t]
+ *   F-hat   device-resident, frequency-major [f][i][j] for f <= N_t
+ *           (the reference's freq_blocks, block_operator.cpp:164-167,199-202,
+ *           truncated to the N_t+1 non-redundant frequencies of a real signal).
+ *
+ * Pointer arguments are host pointers unless BTG_DEVICE_PTRS is set in
+ * `flags`, in which case they are device pointers on the handle's device and
+ * no host<->device copies happen. All calls on one handle are serialized
+ * (internal mutex); distinct handles may be used concurrently.
+ */
+#ifndef BTG_H_
+#define BTG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BTG_ABI_VERSION 1
+
+typedef enum {
+    BTG_OK = 0,
+    BTG_EDIM = 1,    /* shape/length mismatch  -> btoep::DimensionError (block_operator.cpp:123-133) */
+    BTG_EORDER = 2,  /* wrong ordering tag     -> btoep::OrderingError (space_time.cpp:39-44)      */
+    BTG_EARG = 3,    /* invalid argument / state -> btoep::Error                                   */
+    BTG_ECUDA = 4,   /* CUDA runtime failure                                                       */
+    BTG_ENOMEM = 5,  /* device allocation failed                                                   */
+    BTG_EGRID = 6    /* unserviceable processor grid -> btoep::GridError (distributed.cpp:147-152) */
+} btg_status;
+
+typedef enum { BTG_F64 = 64, BTG_F32 = 32 } btg_precision;
+
+/* flags */
+#define BTG_DEVICE_PTRS 0x1u  /* data pointers are device pointers */
+
+/* Hessian options (inverse.hpp:16; Gamma^-1 is the north star's noise weighting) */
+typedef enum { BTG_REG_IDENTITY = 0, BTG_REG_TEMPORAL_LAPLACIAN = 1 } btg_reg_kind;
+typedef enum {
+    BTG_GAMMA_NONE = 0,        /* Gamma^-1 = I                     */
+    BTG_GAMMA_PER_SENSOR = 1,  /* gamma_inv[i], length N_d         */
+    BTG_GAMMA_PER_SAMPLE = 2   /* gamma_inv[i*N_t + t], N_d x N_t  */
+} btg_gamma_kind;
+
+/* Mirrors btoep::StageCounters / PipelineCounters (counters.hpp:12-45). On the
+ * GPU pad+forward_fft+reorder_in run as ONE fused kernel (reported under
+ * forward_fft) and reorder_out+inverse_fft+unpad as one (inverse_fft). Bytes
+ * follow the algorithmic model with N_t+1 frequencies; seconds are CUDA-event
+ * times, filled only while btg_set_timing(op, 1) is active. */
+typedef struct { double ops, bytes, seconds; } btg_stage_counters;
+typedef struct {
+    btg_stage_counters pad, forward_fft, reorder_in, apply, reorder_out, inverse_fft, unpad;
+    uint64_t launches; /* kernels this handle launched */
+} btg_counters;
+
+typedef struct btg_op_s* btg_op;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* btg_last_error(void);
+int btg_abi_version(void);
+
+/* Allocate the device operator (F-hat uninitialised). Replaces the allocation
+ * half of btoep::setup (block_operator.hpp:64, block_operator.cpp:178-205). */
+btg_status btg_create(size_t num_sensors, size_t num_sources, size_t num_steps,
+                      int precision, int device, btg_op* out);
+
+/* Setup (Alg. 1) for the sensor rows [sensor_begin, sensor_end): `blocks` is
+ * the TOSI first block column RESTRICTED to those rows, shape
+ * (N_t, sensor_end-sensor_begin, N_m). Zero-pad to 2N_t, R2C along time,
+ * write F-hat frequency-major. Lets a caller stream an operator too large to
+ * hold twice in HBM. block_operator.cpp:178-205. */
+btg_status btg_setup_rows(btg_op op, const double* blocks, size_t sensor_begin,
+                          size_t sensor_end, unsigned flags);
+
+/* create + setup_rows(0, N_d): the drop-in for btoep::setup. */
+btg_status btg_setup(const double* blocks, size_t num_sensors, size_t num_sources,
+                     size_t num_steps, int precision, int device, unsigned flags,
+                     btg_op* out);
+
+/* d = F m (Alg. 2). m: nrhs x N_m x N_t SOTI (m_len elements), d: nrhs x N_d x N_t.
+ * btoep::apply_forward, block_operator.hpp:71 / block_operator.cpp:218-273. */
+btg_status btg_forward(btg_op op, const double* m, size_t m_len, double* d, size_t d_len,
+                       size_t nrhs, unsigned flags);
+
+/* m = F* d (Alg. 3), same operator, conjugate-transpose indexing.
+ * btoep::apply_adjoint, block_operator.hpp:76 / block_operator.cpp:275-331. */
+btg_status btg_adjoint(btg_op op, const double* d, size_t d_len, double* m, size_t m_len,
+                       size_t nrhs, unsigned flags);
+
+/* hv = F* Gamma^-1 F v + alpha R v. With gamma_kind = BTG_GAMMA_NONE this is
+ * btoep::HessianOperator::apply (inverse.hpp:32-39, inverse.cpp:78-91). */
+btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, size_t hv_len,
+                       size_t nrhs, const double* gamma_inv, int gamma_kind, double alpha,
+                       int reg_kind, unsigned flags);
+
+/* Run subsequent work on `stream` (a cudaStream_t; NULL = the handle's own). */
+btg_status btg_set_stream(btg_op op, void* stream);
+btg_status btg_synchronize(btg_op op);
+btg_status btg_set_timing(btg_op op, int enabled);
+btg_status btg_get_counters(btg_op op, btg_counters* out);
+btg_status btg_reset_counters(btg_op op);
+btg_status btg_get_dims(btg_op op, size_t* num_sensors, size_t* num_sources,
+                        size_t* num_steps, int* precision);
+
+/* Copy F-hat to host complex128 (interleaved re,im). full = 1: the reference's
+ * 2*N_t-frequency layout (freq_blocks, block_operator.hpp:40) with the upper
+ * half rebuilt by conjugate symmetry; full = 0: the N_t+1 stored frequencies. */
+btg_status btg_export_spectrum(btg_op op, double* out, int full);
+
+/* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */
+btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes);
+
+void btg_destroy(btg_op op);
+
+/* Synthetic-input generator (bench / large-config parity): out[k] =
+ * lo + (hi-lo) * ((splitmix64(seed ^ (offset + k)) >> 11) * 2^-53), the same
+ * 53-bit mapping as btoep::Rng::uniform (rng.hpp:16-18) but indexable so any
+ * slice is reproducible on the host. `out` is a device pointer. */
+btg_status btg_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo,
+                            double hi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BTG_H_ */

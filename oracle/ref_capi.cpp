@@ -1,0 +1,234 @@
+// TEST INFRASTRUCTURE ONLY — the checker, never the thing measured or shipped.
+//
+// A flat C ABI over the UNMODIFIED reference sources under
+// /root/reference/proj/src (compiled by oracle/Makefile into
+// oracle/_ref/libbtoep_ref.so together with oracle/ref_fft_shim.cpp). It lets
+// the pytest suite, the golden-fixture generator and bench.py's CPU arm call
+// the reference's own C++ operator API through ctypes:
+//
+//   setup            block_operator.hpp:64   (block_operator.cpp:178-205)
+//   apply_forward    block_operator.hpp:71   (block_operator.cpp:218-273)
+//   apply_adjoint    block_operator.hpp:76   (block_operator.cpp:275-331)
+//   naive_apply_*    block_operator.hpp:88   (block_operator.cpp:423-482)
+//   HessianOperator  inverse.hpp:32-39       (inverse.cpp:78-91)
+//   partition + distributed_forward/adjoint  distributed.hpp:57-121
+//   Rng              rng.hpp:12-32  (the seeded inputs of tests/oracles.cpp:87-98)
+//   run_verification verify.hpp:13
+//
+// Every entry point returns 0 on success, 1 on a btoep::Error (message in
+// ref_last_error()), 2 on any other exception.
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "btoep/block_operator.hpp"
+#include "btoep/distributed.hpp"
+#include "btoep/errors.hpp"
+#include "btoep/inverse.hpp"
+#include "btoep/rng.hpp"
+#include "btoep/verify.hpp"
+
+using namespace btoep;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+CompactP2O make_compact(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt) {
+    CompactP2O op = CompactP2O::zeros(nd, nm, nt);
+    std::memcpy(op.blocks.data(), blocks, sizeof(double) * op.blocks.size());
+    return op;
+}
+
+SpaceTimeVector make_soti(const double* v, std::size_t dim, std::size_t nt) {
+    SpaceTimeVector out = SpaceTimeVector::zeros(dim, nt, Ordering::SOTI);
+    std::memcpy(out.values.data(), v, sizeof(double) * out.values.size());
+    return out;
+}
+
+void copy_out(const SpaceTimeVector& v, double* out) {
+    const SpaceTimeVector soti = with_ordering(v, Ordering::SOTI);
+    std::memcpy(out, soti.values.data(), sizeof(double) * soti.values.size());
+}
+
+struct PartitionHandle {
+    Partition partition;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// ---- seeded inputs (tests/oracles.cpp:87-98 draws: blocks, then m, then d) ----
+int ref_rng_uniform(std::uint64_t seed, std::size_t n, double lo, double hi, double* out) {
+    return guarded([&] {
+        Rng rng(seed);
+        for (std::size_t i = 0; i < n; ++i) out[i] = rng.uniform(lo, hi);
+    });
+}
+
+int ref_rng_raw(std::uint64_t seed, std::size_t n, std::uint64_t* out) {
+    return guarded([&] {
+        std::mt19937_64 gen(seed);
+        for (std::size_t i = 0; i < n; ++i) out[i] = gen();
+    });
+}
+
+// ---- spectral operator handle ------------------------------------------------
+void* ref_setup(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt) {
+    SpectralP2O* op = nullptr;
+    const int rc = guarded([&] { op = new SpectralP2O(setup(make_compact(blocks, nd, nm, nt))); });
+    return rc == 0 ? op : nullptr;
+}
+
+void ref_destroy(void* h) { delete static_cast<SpectralP2O*>(h); }
+
+// Full reference spectrum, freq-major (2*nt, nd, nm) complex128 interleaved.
+int ref_spectrum(void* h, double* out_c128) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        std::memcpy(out_c128, op.freq_blocks.data(),
+                    sizeof(std::complex<double>) * op.freq_blocks.size());
+    });
+}
+
+// stage_seconds (7 doubles: pad, fwd_fft, reorder_in, apply, reorder_out,
+// inv_fft, unpad) is filled when non-null (PipelineCounters::time_stages).
+static void stages_out(const PipelineCounters& c, double* s) {
+    if (!s) return;
+    s[0] = c.pad.seconds;
+    s[1] = c.forward_fft.seconds;
+    s[2] = c.reorder_in.seconds;
+    s[3] = c.apply.seconds;
+    s[4] = c.reorder_out.seconds;
+    s[5] = c.inverse_fft.seconds;
+    s[6] = c.unpad.seconds;
+}
+
+int ref_forward(void* h, const double* m, double* d, double* stage_seconds) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        PipelineCounters c;
+        c.time_stages = stage_seconds != nullptr;
+        copy_out(apply_forward(op, make_soti(m, op.num_sources, op.num_steps), &c), d);
+        stages_out(c, stage_seconds);
+    });
+}
+
+int ref_adjoint(void* h, const double* d, double* m, double* stage_seconds) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        PipelineCounters c;
+        c.time_stages = stage_seconds != nullptr;
+        copy_out(apply_adjoint(op, make_soti(d, op.num_sensors, op.num_steps), &c), m);
+        stages_out(c, stage_seconds);
+    });
+}
+
+// reg_kind: 0 = ScaledIdentity, 1 = TemporalLaplacian (inverse.hpp:16).
+int ref_hessian(void* h, const double* v, double* hv, double alpha, int reg_kind) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        HessianOperator hess;
+        hess.op = &op;
+        hess.reg.kind = reg_kind ? RegKind::TemporalLaplacian : RegKind::ScaledIdentity;
+        hess.reg.alpha = alpha;
+        copy_out(hess.apply(make_soti(v, op.num_sources, op.num_steps)), hv);
+    });
+}
+
+// ---- naive (time-domain) backend: SOTI in, SOTI out ---------------------------
+int ref_naive_forward(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt,
+                      const double* m, double* d) {
+    return guarded([&] {
+        const CompactP2O op = make_compact(blocks, nd, nm, nt);
+        copy_out(naive_apply_forward(op, soti_to_tosi(make_soti(m, nm, nt))), d);
+    });
+}
+
+int ref_naive_adjoint(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt,
+                      const double* d, double* m) {
+    return guarded([&] {
+        const CompactP2O op = make_compact(blocks, nd, nm, nt);
+        copy_out(naive_apply_adjoint(op, soti_to_tosi(make_soti(d, nd, nt))), m);
+    });
+}
+
+// ---- distributed engine (distributed.hpp:57-121) ------------------------------
+void* ref_partition(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt,
+                    std::size_t rows, std::size_t cols) {
+    PartitionHandle* p = nullptr;
+    const int rc = guarded([&] {
+        p = new PartitionHandle{
+            partition_operator(make_compact(blocks, nd, nm, nt), GridShape{rows, cols})};
+    });
+    return rc == 0 ? p : nullptr;
+}
+
+void ref_partition_destroy(void* h) { delete static_cast<PartitionHandle*>(h); }
+
+// Shard bounds: out[4*w + {0,1,2,3}] = sensor_begin, sensor_end, source_begin, source_end.
+int ref_partition_bounds(void* h, std::size_t* out) {
+    return guarded([&] {
+        const Partition& part = static_cast<PartitionHandle*>(h)->partition;
+        for (std::size_t w = 0; w < part.shards.size(); ++w) {
+            out[4 * w + 0] = part.shards[w].sensor_begin;
+            out[4 * w + 1] = part.shards[w].sensor_end;
+            out[4 * w + 2] = part.shards[w].source_begin;
+            out[4 * w + 3] = part.shards[w].source_end;
+        }
+    });
+}
+
+int ref_distributed_forward(void* h, const double* m, double* d, int parallel) {
+    return guarded([&] {
+        const Partition& part = static_cast<PartitionHandle*>(h)->partition;
+        EngineOptions eo;
+        eo.policy = parallel ? ExecutionPolicy::Parallel : ExecutionPolicy::Serial;
+        copy_out(distributed_forward(part, make_soti(m, part.num_sources, part.num_steps), eo), d);
+    });
+}
+
+int ref_distributed_adjoint(void* h, const double* d, double* m, int parallel) {
+    return guarded([&] {
+        const Partition& part = static_cast<PartitionHandle*>(h)->partition;
+        EngineOptions eo;
+        eo.policy = parallel ? ExecutionPolicy::Parallel : ExecutionPolicy::Serial;
+        copy_out(distributed_adjoint(part, make_soti(d, part.num_sensors, part.num_steps), eo), m);
+    });
+}
+
+// ---- the reference's own invariant suite (verify.cpp:72-250) ------------------
+int ref_verify(std::uint64_t seed, char* report, std::size_t report_len, int* passed) {
+    return guarded([&] {
+        std::ostringstream os;
+        *passed = run_verification(os, seed) ? 1 : 0;
+        const std::string s = os.str();
+        if (report && report_len) {
+            std::strncpy(report, s.c_str(), report_len - 1);
+            report[report_len - 1] = '\0';
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+"""ctypes wrapper over ``oracle/_ref/libbtoep_ref.so`` — the reference's own
+CPU implementation (unmodified ``/root/reference/proj/src`` sources + the FFT
+shim, built by ``oracle/Makefile``).
+
+TEST INFRASTRUCTURE ONLY: used by ``tests/``, ``tests/golden/make_golden.py``,
+``__graft_entry__.smoke()`` and the CPU legs of ``bench.py``. Never imported by
+the product package.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_ref" / "libbtoep_ref.so"
+
+_lib = None
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_size_t = ctypes.c_size_t
+
+
+def available() -> bool:
+    return LIB_PATH.exists()
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FileNotFoundError(f"{LIB_PATH} not built (run `make -C oracle`)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.ref_last_error.restype = ctypes.c_char_p
+        L.ref_rng_uniform.argtypes = [ctypes.c_uint64, _size_t, ctypes.c_double, ctypes.c_double, _c_double_p]
+        L.ref_rng_raw.argtypes = [ctypes.c_uint64, _size_t, ctypes.POINTER(ctypes.c_uint64)]
+        L.ref_setup.argtypes = [_c_double_p, _size_t, _size_t, _size_t]
+        L.ref_setup.restype = ctypes.c_void_p
+        L.ref_destroy.argtypes = [ctypes.c_void_p]
+        L.ref_spectrum.argtypes = [ctypes.c_void_p, _c_double_p]
+        for name in ("ref_forward", "ref_adjoint"):
+            getattr(L, name).argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, _c_double_p]
+        L.ref_hessian.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int]
+        for name in ("ref_naive_forward", "ref_naive_adjoint"):
+            getattr(L, name).argtypes = [_c_double_p, _size_t, _size_t, _size_t, _c_double_p, _c_double_p]
+        L.ref_partition.argtypes = [_c_double_p, _size_t, _size_t, _size_t, _size_t, _size_t]
+        L.ref_partition.restype = ctypes.c_void_p
+        L.ref_partition_destroy.argtypes = [ctypes.c_void_p]
+        L.ref_partition_bounds.argtypes = [ctypes.c_void_p, ctypes.POINTER(_size_t)]
+        for name in ("ref_distributed_forward", "ref_distributed_adjoint"):
+            getattr(L, name).argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int]
+        L.ref_verify.argtypes = [ctypes.c_uint64, ctypes.c_char_p, _size_t, ctypes.POINTER(ctypes.c_int)]
+        _lib = L
+    return _lib
+
+
+class RefError(ValueError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        raise RefError(lib().ref_last_error().decode())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_c_double_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def rng_uniform(seed: int, n: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    out = np.empty(n, dtype=np.float64)
+    _check(lib().ref_rng_uniform(seed, n, lo, hi, _p(out)))
+    return out
+
+
+def rng_raw(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint64)
+    _check(lib().ref_rng_raw(seed, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
+
+
+class RefSpectralOperator:
+    """btoep::SpectralP2O built by the reference's setup (block_operator.cpp:178-205)."""
+
+    def __init__(self, blocks: np.ndarray):
+        self.blocks = _f64(blocks)
+        nt, nd, nm = self.blocks.shape
+        self.num_steps, self.num_sensors, self.num_sources = nt, nd, nm
+        h = lib().ref_setup(_p(self.blocks), nd, nm, nt)
+        if not h:
+            raise RefError(lib().ref_last_error().decode())
+        self._h = ctypes.c_void_p(h)
+
+    def close(self):
+        if self._h:
+            lib().ref_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def freq_blocks(self) -> np.ndarray:
+        out = np.empty((2 * self.num_steps, self.num_sensors, self.num_sources), dtype=np.complex128)
+        _check(lib().ref_spectrum(self._h, out.ctypes.data_as(_c_double_p)))
+        return out
+
+    def apply_forward(self, m, stage_seconds: np.ndarray | None = None) -> np.ndarray:
+        m = _f64(m)
+        d = np.empty((self.num_sensors, self.num_steps))
+        _check(lib().ref_forward(self._h, _p(m), _p(d), None if stage_seconds is None else _p(stage_seconds)))
+        return d
+
+    def apply_adjoint(self, d, stage_seconds: np.ndarray | None = None) -> np.ndarray:
+        d = _f64(d)
+        m = np.empty((self.num_sources, self.num_steps))
+        _check(lib().ref_adjoint(self._h, _p(d), _p(m), None if stage_seconds is None else _p(stage_seconds)))
+        return m
+
+    def hessian_apply(self, v, alpha: float = 0.0, reg_kind: int = 0) -> np.ndarray:
+        v = _f64(v)
+        hv = np.empty_like(v)
+        _check(lib().ref_hessian(self._h, _p(v), _p(hv), float(alpha), int(reg_kind)))
+        return hv
+
+
+def naive_forward(blocks, m) -> np.ndarray:
+    blocks, m = _f64(blocks), _f64(m)
+    nt, nd, nm = blocks.shape
+    d = np.empty((nd, nt))
+    _check(lib().ref_naive_forward(_p(blocks), nd, nm, nt, _p(m), _p(d)))
+    return d
+
+
+def naive_adjoint(blocks, d) -> np.ndarray:
+    blocks, d = _f64(blocks), _f64(d)
+    nt, nd, nm = blocks.shape
+    m = np.empty((nm, nt))
+    _check(lib().ref_naive_adjoint(_p(blocks), nd, nm, nt, _p(d), _p(m)))
+    return m
+
+
+class RefPartition:
+    """btoep::Partition (distributed.cpp:179-196) and its F / F* engine."""
+
+    def __init__(self, blocks, rows: int, cols: int):
+        self.blocks = _f64(blocks)
+        nt, nd, nm = self.blocks.shape
+        self.num_steps, self.num_sensors, self.num_sources = nt, nd, nm
+        self.rows, self.cols = rows, cols
+        h = lib().ref_partition(_p(self.blocks), nd, nm, nt, rows, cols)
+        if not h:
+            raise RefError(lib().ref_last_error().decode())
+        self._h = ctypes.c_void_p(h)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().ref_partition_destroy(self._h)
+        except Exception:
+            pass
+
+    def bounds(self):
+        out = (_size_t * (4 * self.rows * self.cols))()
+        _check(lib().ref_partition_bounds(self._h, out))
+        return [tuple(out[4 * w : 4 * w + 4]) for w in range(self.rows * self.cols)]
+
+    def forward(self, m, parallel: bool = False) -> np.ndarray:
+        m = _f64(m)
+        d = np.empty((self.num_sensors, self.num_steps))
+        _check(lib().ref_distributed_forward(self._h, _p(m), _p(d), int(parallel)))
+        return d
+
+    def adjoint(self, d, parallel: bool = False) -> np.ndarray:
+        d = _f64(d)
+        m = np.empty((self.num_sources, self.num_steps))
+        _check(lib().ref_distributed_adjoint(self._h, _p(d), _p(m), int(parallel)))
+        return m
+
+
+def verify(seed: int = 20240901):
+    buf = ctypes.create_string_buffer(1 << 16)
+    passed = ctypes.c_int(0)
+    _check(lib().ref_verify(seed, buf, len(buf), ctypes.byref(passed)))
+    return bool(passed.value), buf.value.decode()
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1

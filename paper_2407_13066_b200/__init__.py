@@ -1,0 +1,22 @@
+"""B200-native FFT block-Toeplitz matvec (arXiv 2407.13066) — the hot path of
+the reference ``btoep`` library, behind its own operator API.
+
+Compute runs only in ``libbtg.so`` (hand-written sm_100a CUDA, C ABI in
+``include/btg.h``); this package is the host-side mirror of the reference's
+Python surface plus the multi-GPU grid (``distributed``).
+"""
+
+from ._lib import DimensionError, Error, GridError, OrderingError  # noqa: F401
+from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
+
+__all__ = [
+    "DimensionError",
+    "Error",
+    "GridError",
+    "OrderingError",
+    "HessianOperator",
+    "SpectralOperator",
+    "create",
+    "fill_uniform",
+    "setup",
+]

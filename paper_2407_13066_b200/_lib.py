@@ -1,0 +1,142 @@
+"""ctypes binding of ``libbtg.so`` (the C ABI declared in ``include/btg.h``).
+
+There is deliberately no fallback: if the CUDA library is missing or no GPU is
+visible, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
+
+BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID = range(7)
+BTG_F64, BTG_F32 = 64, 32
+BTG_DEVICE_PTRS = 0x1
+BTG_REG_IDENTITY, BTG_REG_TEMPORAL_LAPLACIAN = 0, 1
+BTG_GAMMA_NONE, BTG_GAMMA_PER_SENSOR, BTG_GAMMA_PER_SAMPLE = 0, 1, 2
+
+# Every symbol include/btg.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "btg_last_error",
+    "btg_abi_version",
+    "btg_create",
+    "btg_setup_rows",
+    "btg_setup",
+    "btg_forward",
+    "btg_adjoint",
+    "btg_hessian",
+    "btg_set_stream",
+    "btg_synchronize",
+    "btg_set_timing",
+    "btg_get_counters",
+    "btg_reset_counters",
+    "btg_get_dims",
+    "btg_export_spectrum",
+    "btg_spectrum_device",
+    "btg_destroy",
+    "btg_fill_uniform",
+)
+
+
+class Error(RuntimeError):
+    """btoep::Error (errors.hpp:8-10) / CUDA failure."""
+
+
+class DimensionError(ValueError):
+    """btoep::DimensionError (errors.hpp:13-15)."""
+
+
+class OrderingError(ValueError):
+    """btoep::OrderingError (errors.hpp:18-20)."""
+
+
+class GridError(ValueError):
+    """btoep::GridError (errors.hpp:28-30)."""
+
+
+class _Stage(ctypes.Structure):
+    _fields_ = [("ops", ctypes.c_double), ("bytes", ctypes.c_double), ("seconds", ctypes.c_double)]
+
+
+class Counters(ctypes.Structure):
+    """btg_counters == btoep::PipelineCounters stages (counters.hpp:18-45)."""
+
+    _fields_ = [
+        ("pad", _Stage),
+        ("forward_fft", _Stage),
+        ("reorder_in", _Stage),
+        ("apply", _Stage),
+        ("reorder_out", _Stage),
+        ("inverse_fft", _Stage),
+        ("unpad", _Stage),
+        ("launches", ctypes.c_uint64),
+    ]
+
+    def as_dict(self):
+        out = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            out[name] = v if isinstance(v, int) else {"ops": v.ops, "bytes": v.bytes, "seconds": v.seconds}
+        return out
+
+
+_lib = None
+_sz = ctypes.c_size_t
+_vp = ctypes.c_void_p
+_dp = ctypes.c_void_p  # pointers passed as integers (host or device)
+
+
+def load():
+    """Load libbtg.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise Error(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    L.btg_last_error.restype = ctypes.c_char_p
+    L.btg_abi_version.restype = ctypes.c_int
+    L.btg_create.argtypes = [_sz, _sz, _sz, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.btg_setup_rows.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_uint]
+    L.btg_setup.argtypes = [_dp, _sz, _sz, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_uint, ctypes.POINTER(_vp)]
+    L.btg_forward.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_uint]
+    L.btg_adjoint.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_uint]
+    L.btg_hessian.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, _dp, ctypes.c_int, ctypes.c_double,
+                              ctypes.c_int, ctypes.c_uint]
+    L.btg_set_stream.argtypes = [_vp, _vp]
+    L.btg_synchronize.argtypes = [_vp]
+    L.btg_set_timing.argtypes = [_vp, ctypes.c_int]
+    L.btg_get_counters.argtypes = [_vp, ctypes.POINTER(Counters)]
+    L.btg_reset_counters.argtypes = [_vp]
+    L.btg_get_dims.argtypes = [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz), ctypes.POINTER(_sz),
+                               ctypes.POINTER(ctypes.c_int)]
+    L.btg_export_spectrum.argtypes = [_vp, _dp, ctypes.c_int]
+    L.btg_spectrum_device.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_sz)]
+    L.btg_destroy.argtypes = [_vp]
+    L.btg_destroy.restype = None
+    L.btg_fill_uniform.argtypes = [_dp, _sz, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
+                                   ctypes.c_double, _vp]
+    for name in EXPORTED:
+        if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    """Map a btg_status to the reference's exception taxonomy (errors.hpp)."""
+    if status == BTG_OK:
+        return
+    msg = load().btg_last_error().decode(errors="replace")
+    if status == BTG_EDIM:
+        raise DimensionError(msg)
+    if status == BTG_EORDER:
+        raise OrderingError(msg)
+    if status == BTG_EGRID:
+        raise GridError(msg)
+    if status == BTG_ENOMEM:
+        raise MemoryError(msg)
+    raise Error(msg)

@@ -1,0 +1,646 @@
+// C ABI (include/btg.h) over the sm_100a kernels: the device-resident
+// frequency-domain operator handle, its workspace, streams, counters and
+// host<->device staging. Host logic mirrors the reference's operator API:
+//   setup                block_operator.cpp:178-205
+//   apply_forward        block_operator.cpp:218-273  (check_apply_input :123-133)
+//   apply_adjoint        block_operator.cpp:275-331
+//   HessianOperator::apply  inverse.cpp:78-91 (+ Gamma^-1, north star)
+// There is no CPU compute path: every arithmetic step is a CUDA kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/btg.h"
+#include "btg_fft.cuh"
+#include "btg_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+btg_status fail(btg_status s, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define BTG_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? BTG_ENOMEM : BTG_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+    } while (0)
+
+#define BTG_TRY(call)                       \
+    do {                                    \
+        btg_status s_ = (call);             \
+        if (s_ != BTG_OK) return s_;        \
+    } while (0)
+
+// exp(-2*pi*i*num/den) with exact integer argument reduction.
+double2 root(long long num, long long den) {
+    num %= den;
+    if (num < 0) num += den;
+    const long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)num / (long double)den;
+    return make_double2((double)cosl(a), (double)(-sinl(a)));
+}
+
+std::vector<int> factorize(int n) {
+    std::vector<int> f;
+    while (n % 8 == 0) { f.push_back(8); n /= 8; }
+    while (n % 4 == 0) { f.push_back(4); n /= 4; }
+    while (n % 2 == 0) { f.push_back(2); n /= 2; }
+    while (n % 5 == 0) { f.push_back(5); n /= 5; }
+    while (n % 3 == 0) { f.push_back(3); n /= 3; }
+    for (int p = 7; (long long)p * p <= n; p += 2)
+        while (n % p == 0) { f.push_back(p); n /= p; }
+    if (n > 1) f.push_back(n);
+    return f;
+}
+
+constexpr size_t kFftSmemBudget = 200 * 1024;      // per CTA
+constexpr size_t kFftSmemTarget = 100 * 1024;      // aim for 2 CTAs / SM
+constexpr size_t kHostStageBytes = 512ull << 20;   // host->device setup staging
+
+}  // namespace
+
+struct btg_op_s {
+    int device = 0;
+    int precision = BTG_F64;
+    size_t nd = 0, nm = 0, nt = 0, nf = 0;
+    void* F = nullptr;  // [nf][nd][nm] double2 or float2
+    size_t F_elem = 16;
+
+    btg::FftPlanDev plan{};
+    double2* d_tw = nullptr;
+    double2* d_post = nullptr;
+    int fft_batch = 1;        // channels per CTA for vector transforms
+    int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
+
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+
+    // workspace (grown on demand)
+    double2* wa = nullptr;
+    double2* wb = nullptr;
+    size_t wcap = 0;  // complex elements each
+    double* wt = nullptr;
+    size_t wtcap = 0;  // doubles: time-domain Hessian intermediate
+    double* hin = nullptr;
+    double* hout = nullptr;
+    size_t hcap = 0;  // doubles each: staging for host-pointer calls
+    double* gam = nullptr;
+    size_t gcap = 0;
+    double* vcopy = nullptr;
+    size_t vcap = 0;
+
+    std::vector<char> rows_ready;
+    size_t rows_ready_count = 0;
+
+    bool timing = false;
+    btg_counters counters{};
+    std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+btg_status grow(T*& ptr, size_t& cap, size_t need) {
+    if (need <= cap) return BTG_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ptr), need * sizeof(T));
+    if (e != cudaSuccess) {
+        ptr = nullptr;
+        return fail(BTG_ENOMEM, "device allocation of %zu bytes failed: %s", need * sizeof(T),
+                    cudaGetErrorString(e));
+    }
+    cap = need;
+    return BTG_OK;
+}
+
+// Stage timing: one event pair per stage when timing is enabled.
+struct StageClock {
+    btg_op op;
+    btg_stage_counters* st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    StageClock(btg_op o, btg_stage_counters* s) : op(o), st(s) {
+        if (op->timing) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, op->stream);
+        }
+    }
+    void stop() {
+        if (op->timing && a) {
+            cudaEventRecord(b, op->stream);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            st->seconds += ms * 1e-3;
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+            a = b = nullptr;
+        }
+    }
+    ~StageClock() { stop(); }
+};
+
+double fft_ops(size_t channels, size_t nt) {
+    const double len = 2.0 * (double)nt;
+    return (double)channels * len * std::log2(len);
+}
+
+btg_status check_ready(btg_op op) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (op->rows_ready_count != op->nd)
+        return fail(BTG_EARG, "operator setup incomplete: %zu of %zu sensor rows transformed",
+                    op->rows_ready_count, op->nd);
+    return BTG_OK;
+}
+
+// The two spectral buffers share one capacity counter; grow both together.
+btg_status ensure_spectral(btg_op op, size_t nrhs) {
+    const size_t need = op->nf * nrhs * std::max(op->nm, op->nd);
+    if (need <= op->wcap && op->wa && op->wb) return BTG_OK;
+    if (op->wa) cudaFree(op->wa);
+    if (op->wb) cudaFree(op->wb);
+    op->wa = op->wb = nullptr;
+    op->wcap = 0;
+    cudaError_t e = cudaMalloc(&op->wa, need * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&op->wb, need * sizeof(double2));
+    if (e != cudaSuccess) {
+        if (op->wa) cudaFree(op->wa);
+        op->wa = nullptr;
+        return fail(BTG_ENOMEM, "workspace allocation (2 x %zu bytes) failed: %s",
+                    need * sizeof(double2), cudaGetErrorString(e));
+    }
+    op->wcap = need;
+    return BTG_OK;
+}
+
+btg_status host_buffers(btg_op op, size_t nin, size_t nout) {
+    const size_t need = std::max(nin, nout);
+    if (need <= op->hcap && op->hin && op->hout) return BTG_OK;
+    if (op->hin) cudaFree(op->hin);
+    if (op->hout) cudaFree(op->hout);
+    op->hin = op->hout = nullptr;
+    op->hcap = 0;
+    cudaError_t e = cudaMalloc(&op->hin, need * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&op->hout, need * sizeof(double));
+    if (e != cudaSuccess) return fail(BTG_ENOMEM, "staging allocation failed: %s", cudaGetErrorString(e));
+    op->hcap = need;
+    return BTG_OK;
+}
+
+// ---- pipeline pieces --------------------------------------------------------
+btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out) {
+    StageClock clk(op, &op->counters.forward_fft);
+    BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)channels, 1,
+                                      (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream));
+    op->counters.launches++;
+    op->counters.forward_fft.ops += fft_ops(channels, op->nt);
+    op->counters.forward_fft.bytes += 8.0 * channels * op->nt + 16.0 * op->nf * channels;
+    return BTG_OK;
+}
+
+btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* out,
+                       const btg::C2REpilogue& epi) {
+    StageClock clk(op, &op->counters.inverse_fft);
+    BTG_CUDA(btg::launch_c2r(in, (long long)channels, 1, out, (long long)op->nt, (int)channels,
+                             (int)op->nt, op->plan, op->fft_batch, epi, op->stream));
+    op->counters.launches++;
+    op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
+    op->counters.inverse_fft.bytes += 16.0 * op->nf * channels + 8.0 * channels * op->nt;
+    return BTG_OK;
+}
+
+btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, size_t nrhs) {
+    StageClock clk(op, &op->counters.apply);
+    const size_t nin = adjoint ? op->nd : op->nm;
+    const size_t nout = adjoint ? op->nm : op->nd;
+    if (nrhs != 1) return fail(BTG_EARG, "internal: run_apply expects nrhs == 1");
+    cudaError_t e;
+    if (op->precision == BTG_F64) {
+        const double2* F = static_cast<const double2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream)
+                    : btg::launch_gemv_fwd(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream);
+    } else {
+        const float2* F = static_cast<const float2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream)
+                    : btg::launch_gemv_fwd(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream);
+    }
+    BTG_CUDA(e);
+    op->counters.launches++;
+    op->counters.apply.ops += 8.0 * op->nd * op->nm * op->nf;
+    op->counters.apply.bytes += (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (nin + nout);
+    return BTG_OK;
+}
+
+// One direction (forward or adjoint) for nrhs right-hand sides, device pointers.
+btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size_t nrhs,
+                    const btg::C2REpilogue& epi) {
+    const size_t cin = adjoint ? op->nd : op->nm;
+    const size_t cout = adjoint ? op->nm : op->nd;
+    BTG_TRY(ensure_spectral(op, 1));
+    for (size_t r = 0; r < nrhs; ++r) {
+        BTG_TRY(run_r2c_vec(op, in + r * cin * op->nt, cin, op->wa));
+        BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, 1));
+        btg::C2REpilogue e = epi;
+        if (e.v) e.v = epi.v + r * cout * op->nt;
+        BTG_TRY(run_c2r_vec(op, op->wb, cout, out + r * cout * op->nt, e));
+    }
+    return BTG_OK;
+}
+
+btg_status check_len(const char* what, size_t got, size_t want_dim, size_t nt, size_t nrhs,
+                     size_t op_dim) {
+    if (got != want_dim * nt * nrhs)
+        return fail(BTG_EDIM, "%s: input has %zu values but operator expects %zu x %zu (x %zu rhs)",
+                    what, got, op_dim, nt, nrhs);
+    return BTG_OK;
+}
+
+btg_status finish_host(btg_op op, double* out_host, const double* out_dev, size_t n, unsigned flags) {
+    if (!(flags & BTG_DEVICE_PTRS)) {
+        BTG_CUDA(cudaMemcpyAsync(out_host, out_dev, n * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+        BTG_CUDA(cudaStreamSynchronize(op->stream));
+    } else {
+        BTG_CUDA(cudaGetLastError());
+    }
+    return BTG_OK;
+}
+
+btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, double* out,
+                     size_t out_len, size_t nrhs, unsigned flags) {
+    BTG_TRY(check_ready(op));
+    if (nrhs == 0) return fail(BTG_EARG, "nrhs must be >= 1");
+    if (!in || !out) return fail(BTG_EARG, "null vector pointer");
+    const char* what = adjoint ? "apply_adjoint" : "apply_forward";
+    const size_t din = adjoint ? op->nd : op->nm;
+    const size_t dout = adjoint ? op->nm : op->nd;
+    BTG_TRY(check_len(what, in_len, din, op->nt, nrhs, din));
+    BTG_TRY(check_len(what, out_len, dout, op->nt, nrhs, dout));
+    DeviceGuard g(op->device);
+    const double* din_p = in;
+    double* dout_p = out;
+    if (!(flags & BTG_DEVICE_PTRS)) {
+        BTG_TRY(host_buffers(op, in_len, out_len));
+        BTG_CUDA(cudaMemcpyAsync(op->hin, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        din_p = op->hin;
+        dout_p = op->hout;
+    }
+    BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, btg::C2REpilogue{}));
+    return finish_host(op, out, dout_p, out_len, flags);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* btg_last_error(void) { return g_err.c_str(); }
+int btg_abi_version(void) { return BTG_ABI_VERSION; }
+
+btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device, btg_op* out) {
+    if (!out) return fail(BTG_EARG, "null output handle");
+    *out = nullptr;
+    if (nd == 0 || nm == 0 || nt == 0)
+        return fail(BTG_EDIM, "compact operator: all dimensions must be positive");
+    if (precision != BTG_F64 && precision != BTG_F32)
+        return fail(BTG_EARG, "precision must be 64 or 32 (got %d)", precision);
+    if (nt > (1u << 30) || nd > (1u << 30) || nm > (1u << 30))
+        return fail(BTG_EDIM, "dimension exceeds 2^30");
+    int ndev = 0;
+    BTG_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(BTG_EARG, "device %d not present (%d devices)", device, ndev);
+
+    const std::vector<int> fac = factorize((int)nt);
+    if ((int)fac.size() > btg::kMaxFactors) return fail(BTG_EARG, "N_t=%zu has too many factors", nt);
+    const int batch_vec = btg::fft_batch((int)nt, kFftSmemTarget, 4);
+    const int batch_max = btg::fft_batch((int)nt, kFftSmemBudget, 1);
+    if (batch_max < 1)
+        return fail(BTG_EDIM, "N_t=%zu exceeds the shared-memory FFT limit (%zu bytes per channel)", nt,
+                    btg::fft_smem_bytes((int)nt, 1));
+
+    DeviceGuard g(device);
+    btg_op op = new (std::nothrow) btg_op_s();
+    if (!op) return fail(BTG_ENOMEM, "host allocation failed");
+    op->device = device;
+    op->precision = precision;
+    op->nd = nd;
+    op->nm = nm;
+    op->nt = nt;
+    op->nf = nt + 1;
+    op->F_elem = precision == BTG_F64 ? sizeof(double2) : sizeof(float2);
+    op->fft_batch = std::max(1, batch_vec);
+    op->fft_batch_setup = std::max(1, std::min(btg::fft_batch((int)nt, kFftSmemBudget, 8), 8));
+
+    auto cleanup_fail = [&](btg_status s) {
+        btg_destroy(op);
+        return s;
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&op->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cleanup_fail(fail(BTG_ECUDA, "stream: %s", cudaGetErrorString(e)));
+    op->stream = op->own_stream;
+
+    // twiddle tables
+    std::vector<double2> tw(nt), post(nt + 1);
+    for (size_t k = 0; k < nt; ++k) tw[k] = root((long long)k, (long long)nt);
+    for (size_t k = 0; k <= nt; ++k) post[k] = root((long long)k, 2 * (long long)nt);
+    e = cudaMalloc(&op->d_tw, nt * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&op->d_post, (nt + 1) * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMemcpy(op->d_tw, tw.data(), nt * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(op->d_post, post.data(), (nt + 1) * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cleanup_fail(fail(BTG_ECUDA, "twiddles: %s", cudaGetErrorString(e)));
+    op->plan.n = (int)nt;
+    op->plan.nfac = (int)fac.size();
+    for (size_t i = 0; i < fac.size(); ++i) op->plan.fac[i] = fac[i];
+    op->plan.tw = op->d_tw;
+    op->plan.post = op->d_post;
+
+    const size_t fbytes = op->nf * nd * nm * op->F_elem;
+    e = cudaMalloc(&op->F, fbytes);
+    if (e != cudaSuccess)
+        return cleanup_fail(fail(BTG_ENOMEM, "F-hat allocation of %zu bytes failed: %s", fbytes,
+                                 cudaGetErrorString(e)));
+    op->rows_ready.assign(nd, 0);
+    *out = op;
+    return BTG_OK;
+}
+
+btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (!blocks) return fail(BTG_EARG, "null blocks pointer");
+    if (i0 >= i1 || i1 > op->nd)
+        return fail(BTG_EDIM, "setup rows [%zu, %zu) outside [0, %zu)", i0, i1, op->nd);
+    std::lock_guard<std::mutex> lock(op->mu);
+    DeviceGuard g(op->device);
+    const size_t rows = i1 - i0;
+    const size_t slab_channels = rows * op->nm;
+    const long long out_fs = (long long)(op->nd * op->nm);
+    auto launch = [&](const double* src, long long in_ts, size_t c_begin, size_t count) -> btg_status {
+        StageClock clk(op, &op->counters.forward_fft);
+        cudaError_t e;
+        const size_t off = i0 * op->nm + c_begin;
+        if (op->precision == BTG_F64)
+            e = btg::launch_r2c<double2>(src, 1, in_ts, static_cast<double2*>(op->F) + off, out_fs, 1,
+                                         (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream);
+        else
+            e = btg::launch_r2c<float2>(src, 1, in_ts, static_cast<float2*>(op->F) + off, out_fs, 1,
+                                        (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream);
+        BTG_CUDA(e);
+        op->counters.launches++;
+        return BTG_OK;
+    };
+    if (flags & BTG_DEVICE_PTRS) {
+        // Channel counts must fit an int grid; split very large slabs.
+        const size_t max_chunk = (size_t)1 << 30;
+        for (size_t c = 0; c < slab_channels; c += max_chunk) {
+            const size_t cnt = std::min(max_chunk, slab_channels - c);
+            BTG_TRY(launch(blocks + c, (long long)slab_channels, c, cnt));
+        }
+    } else {
+        // Host input: stream channel ranges through a bounded device staging buffer.
+        size_t chunk = std::max<size_t>(1, kHostStageBytes / (op->nt * sizeof(double)));
+        chunk = std::min(chunk, slab_channels);
+        BTG_TRY(host_buffers(op, chunk * op->nt, 0));
+        for (size_t c = 0; c < slab_channels; c += chunk) {
+            const size_t cnt = std::min(chunk, slab_channels - c);
+            BTG_CUDA(cudaMemcpy2DAsync(op->hin, cnt * sizeof(double), blocks + c,
+                                       slab_channels * sizeof(double), cnt * sizeof(double), op->nt,
+                                       cudaMemcpyHostToDevice, op->stream));
+            BTG_TRY(launch(op->hin, (long long)cnt, c, cnt));
+        }
+        BTG_CUDA(cudaStreamSynchronize(op->stream));
+    }
+    for (size_t i = i0; i < i1; ++i)
+        if (!op->rows_ready[i]) {
+            op->rows_ready[i] = 1;
+            op->rows_ready_count++;
+        }
+    return BTG_OK;
+}
+
+btg_status btg_setup(const double* blocks, size_t nd, size_t nm, size_t nt, int precision,
+                     int device, unsigned flags, btg_op* out) {
+    BTG_TRY(btg_create(nd, nm, nt, precision, device, out));
+    btg_status s = btg_setup_rows(*out, blocks, 0, nd, flags);
+    if (s != BTG_OK) {
+        const std::string msg = g_err;
+        btg_destroy(*out);
+        *out = nullptr;
+        g_err = msg;
+    }
+    return s;
+}
+
+btg_status btg_forward(btg_op op, const double* m, size_t m_len, double* d, size_t d_len,
+                       size_t nrhs, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return apply_dir(op, false, m, m_len, d, d_len, nrhs, flags);
+}
+
+btg_status btg_adjoint(btg_op op, const double* d, size_t d_len, double* m, size_t m_len,
+                       size_t nrhs, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return apply_dir(op, true, d, d_len, m, m_len, nrhs, flags);
+}
+
+btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, size_t hv_len,
+                       size_t nrhs, const double* gamma_inv, int gamma_kind, double alpha,
+                       int reg_kind, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    BTG_TRY(check_ready(op));
+    if (nrhs == 0) return fail(BTG_EARG, "nrhs must be >= 1");
+    if (!v || !hv) return fail(BTG_EARG, "null vector pointer");
+    if (reg_kind != BTG_REG_IDENTITY && reg_kind != BTG_REG_TEMPORAL_LAPLACIAN)
+        return fail(BTG_EARG, "unknown regularization kind %d", reg_kind);
+    if (gamma_kind < BTG_GAMMA_NONE || gamma_kind > BTG_GAMMA_PER_SAMPLE)
+        return fail(BTG_EARG, "unknown gamma kind %d", gamma_kind);
+    if (gamma_kind != BTG_GAMMA_NONE && !gamma_inv) return fail(BTG_EARG, "gamma_inv is null");
+    BTG_TRY(check_len("hessian", v_len, op->nm, op->nt, nrhs, op->nm));
+    BTG_TRY(check_len("hessian", hv_len, op->nm, op->nt, nrhs, op->nm));
+    DeviceGuard g(op->device);
+
+    const double* vd = v;
+    double* hvd = hv;
+    if (!(flags & BTG_DEVICE_PTRS)) {
+        BTG_TRY(host_buffers(op, v_len, hv_len));
+        BTG_CUDA(cudaMemcpyAsync(op->hin, v, v_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        vd = op->hin;
+        hvd = op->hout;
+    } else if (vd == hvd && alpha != 0.0) {
+        // in-place call: the final epilogue reads v while writing hv
+        BTG_TRY(grow(op->vcopy, op->vcap, v_len));
+        BTG_CUDA(cudaMemcpyAsync(op->vcopy, v, v_len * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
+        vd = op->vcopy;
+    }
+    const double* gd = nullptr;
+    if (gamma_kind != BTG_GAMMA_NONE) {
+        const size_t glen = gamma_kind == BTG_GAMMA_PER_SENSOR ? op->nd : op->nd * op->nt;
+        if (flags & BTG_DEVICE_PTRS) {
+            gd = gamma_inv;
+        } else {
+            BTG_TRY(grow(op->gam, op->gcap, glen));
+            BTG_CUDA(cudaMemcpyAsync(op->gam, gamma_inv, glen * sizeof(double), cudaMemcpyHostToDevice,
+                                     op->stream));
+            gd = op->gam;
+        }
+    }
+    BTG_TRY(grow(op->wt, op->wtcap, op->nd * op->nt * nrhs));
+
+    btg::C2REpilogue e1{};
+    e1.gamma = gd;
+    e1.gamma_mode = gamma_kind;
+    e1.gamma_dim = (int)op->nd;
+    BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
+    btg::C2REpilogue e2{};
+    if (alpha != 0.0) {
+        e2.v = vd;
+        e2.alpha = alpha;
+        e2.reg_kind = reg_kind;
+    }
+    BTG_TRY(pipeline(op, true, op->wt, hvd, nrhs, e2));
+    return finish_host(op, hv, hvd, hv_len, flags);
+}
+
+btg_status btg_set_stream(btg_op op, void* stream) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    op->stream = stream ? static_cast<cudaStream_t>(stream) : op->own_stream;
+    return BTG_OK;
+}
+
+btg_status btg_synchronize(btg_op op) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    DeviceGuard g(op->device);
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    return BTG_OK;
+}
+
+btg_status btg_set_timing(btg_op op, int enabled) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    op->timing = enabled != 0;
+    return BTG_OK;
+}
+
+btg_status btg_get_counters(btg_op op, btg_counters* out) {
+    if (!op || !out) return fail(BTG_EARG, "null argument");
+    *out = op->counters;
+    return BTG_OK;
+}
+
+btg_status btg_reset_counters(btg_op op) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    op->counters = btg_counters{};
+    return BTG_OK;
+}
+
+btg_status btg_get_dims(btg_op op, size_t* nd, size_t* nm, size_t* nt, int* precision) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (nd) *nd = op->nd;
+    if (nm) *nm = op->nm;
+    if (nt) *nt = op->nt;
+    if (precision) *precision = op->precision;
+    return BTG_OK;
+}
+
+btg_status btg_export_spectrum(btg_op op, double* out, int full) {
+    if (!op || !out) return fail(BTG_EARG, "null argument");
+    std::lock_guard<std::mutex> lock(op->mu);
+    BTG_TRY(check_ready(op));
+    DeviceGuard g(op->device);
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    const size_t blk = op->nd * op->nm;
+    const size_t count = op->nf * blk;
+    std::vector<std::complex<double>> half(count);
+    if (op->precision == BTG_F64) {
+        BTG_CUDA(cudaMemcpy(half.data(), op->F, count * sizeof(double2), cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<std::complex<float>> tmp(count);
+        BTG_CUDA(cudaMemcpy(tmp.data(), op->F, count * sizeof(float2), cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < count; ++k) half[k] = std::complex<double>(tmp[k].real(), tmp[k].imag());
+    }
+    auto* dst = reinterpret_cast<std::complex<double>*>(out);
+    if (!full) {
+        std::memcpy(dst, half.data(), count * sizeof(std::complex<double>));
+        return BTG_OK;
+    }
+    const size_t len = 2 * op->nt;
+    for (size_t f = 0; f < len; ++f) {
+        if (f <= op->nt) {
+            std::memcpy(dst + f * blk, half.data() + f * blk, blk * sizeof(std::complex<double>));
+        } else {
+            const std::complex<double>* src = half.data() + (len - f) * blk;
+            for (size_t c = 0; c < blk; ++c) dst[f * blk + c] = std::conj(src[c]);
+        }
+    }
+    return BTG_OK;
+}
+
+btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (ptr) *ptr = op->F;
+    if (elem_bytes) *elem_bytes = op->F_elem;
+    return BTG_OK;
+}
+
+void btg_destroy(btg_op op) {
+    if (!op) return;
+    {
+        DeviceGuard g(op->device);
+        if (op->own_stream) cudaStreamSynchronize(op->own_stream);
+        if (op->stream && op->stream != op->own_stream) cudaStreamSynchronize(op->stream);
+        cudaFree(op->F);
+        cudaFree(op->d_tw);
+        cudaFree(op->d_post);
+        cudaFree(op->wa);
+        cudaFree(op->wb);
+        cudaFree(op->wt);
+        cudaFree(op->hin);
+        cudaFree(op->hout);
+        cudaFree(op->gam);
+        cudaFree(op->vcopy);
+        if (op->own_stream) cudaStreamDestroy(op->own_stream);
+    }
+    delete op;
+}
+
+btg_status btg_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo, double hi,
+                            void* stream) {
+    if (!out && n) return fail(BTG_EARG, "null output pointer");
+    BTG_CUDA(btg::launch_fill_uniform(out, n, seed, offset, lo, hi, static_cast<cudaStream_t>(stream)));
+    return BTG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,526 @@
+// sm_100a kernels of the FFT block-Toeplitz matvec.
+//
+//  k_r2c       K1/K5: pad + R2C along time + transpose to frequency-major,
+//              fused (reference: pad_and_transform + reorder_in,
+//              block_operator.cpp:54-80,231-236, and setup :178-205)
+//  k_c2r       K9: reorder_out + C2R + unpad (+ Gamma^-1, + alpha R v),
+//              fused (block_operator.cpp:83-121,261-268; inverse.cpp:78-91)
+//  k_gemv_fwd  K7 forward apply, d_f = F_f m_f (block_operator.cpp:239-259)
+//  k_gemv_adj  K7 adjoint apply, m_f = F_f^H d_f (block_operator.cpp:296-317)
+//
+// The Fourier-space step is a pure HBM stream over F-hat (arithmetic
+// intensity 0.5 flop/B in FP64): every F-hat element is read exactly once
+// with 16-byte non-coherent loads that bypass L1 and carry an L2 evict-first
+// policy, so the reused vector slices (m-hat_f, d-hat_f) stay L2-resident.
+// All reductions have a fixed order: results are bit-identical run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "btg_fft.cuh"
+#include "btg_kernels.cuh"
+
+namespace btg {
+namespace {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// streaming loads of F-hat
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+template <typename TF, int VEC>
+struct FLoad;
+
+template <>
+struct FLoad<double2, 1> {
+    __device__ __forceinline__ static void load(const double2* p, uint64_t pol, double2* out) {
+        double2 r;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+            : "=d"(r.x), "=d"(r.y)
+            : "l"(p), "l"(pol));
+        out[0] = r;
+    }
+    __device__ __forceinline__ static double2 scalar(const double2* p) { return __ldg(p); }
+};
+
+template <>
+struct FLoad<float2, 1> {
+    __device__ __forceinline__ static void load(const float2* p, uint64_t pol, double2* out) {
+        float x, y;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+            : "=f"(x), "=f"(y)
+            : "l"(p), "l"(pol));
+        out[0] = make_double2(x, y);
+    }
+    __device__ __forceinline__ static double2 scalar(const float2* p) {
+        const float2 v = __ldg(p);
+        return make_double2(v.x, v.y);
+    }
+};
+
+template <>
+struct FLoad<float2, 2> {
+    __device__ __forceinline__ static void load(const float2* p, uint64_t pol, double2* out) {
+        float a, b, c, d;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+            : "l"(p), "l"(pol));
+        out[0] = make_double2(a, b);
+        out[1] = make_double2(c, d);
+    }
+    __device__ __forceinline__ static double2 scalar(const float2* p) {
+        const float2 v = __ldg(p);
+        return make_double2(v.x, v.y);
+    }
+};
+
+// acc += a * b
+__device__ __forceinline__ void cmac(double& re, double& im, double2 a, double2 b) {
+    re = fma(a.x, b.x, re);
+    re = fma(-a.y, b.y, re);
+    im = fma(a.x, b.y, im);
+    im = fma(a.y, b.x, im);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cmac_conj(double& re, double& im, double2 a, double2 b) {
+    re = fma(a.x, b.x, re);
+    re = fma(a.y, b.y, re);
+    im = fma(a.x, b.y, im);
+    im = fma(-a.y, b.x, im);
+}
+
+template <typename T>
+__device__ __forceinline__ T to_out(double2 v);
+template <>
+__device__ __forceinline__ double2 to_out<double2>(double2 v) { return v; }
+template <>
+__device__ __forceinline__ float2 to_out<float2>(double2 v) {
+    return make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+}
+
+// ---------------------------------------------------------------------------
+// K1/K5: fused pad + R2C + frequency-major store
+// ---------------------------------------------------------------------------
+template <typename TOut>
+__global__ void __launch_bounds__(kThreads) k_r2c(const double* __restrict__ in, long long in_cs,
+                                                  long long in_ts, TOut* __restrict__ out,
+                                                  long long out_fs, long long out_cs, int channels,
+                                                  int nt, FftPlanDev plan, int batch) {
+    extern __shared__ double2 smem[];
+    const int n = plan.n;  // == nt
+    const int cs = fft_channel_stride(n);
+    double2* buf_a = smem;
+    double2* buf_b = smem + (size_t)batch * cs;
+    const int c0 = blockIdx.x * batch;
+    const int nb = min(batch, channels - c0);
+    const int len = 2 * n;  // padded real length
+    double* ad = reinterpret_cast<double*>(buf_a);
+
+    // Load: z[n] = x[2n] + i x[2n+1] is the real sequence itself viewed as
+    // interleaved complex, so sample t of channel b goes to double 2*cs*b + t.
+    if (in_ts == 1) {  // SOTI rows: time contiguous
+        for (int u = threadIdx.x; u < nb * len; u += blockDim.x) {
+            const int b = u / len;
+            const int t = u - b * len;
+            ad[2 * cs * b + t] = t < nt ? __ldg(in + (long long)(c0 + b) * in_cs + t) : 0.0;
+        }
+    } else {  // TOSI: channels contiguous
+        for (int u = threadIdx.x; u < nb * len; u += blockDim.x) {
+            const int t = u / nb;
+            const int b = u - t * nb;
+            ad[2 * cs * b + t] = t < nt ? __ldg(in + (long long)(c0 + b) * in_cs + t * in_ts) : 0.0;
+        }
+    }
+    __syncthreads();
+    const double2* z = fft_smem<-1>(buf_a, buf_b, nb, cs, plan);
+
+    // Split: X_k = 1/2 (Z_k + conj Z_{n-k}) - i/2 W_{2n}^k (Z_k - conj Z_{n-k}), k = 0..n.
+    for (int u = threadIdx.x; u < nb * (n + 1); u += blockDim.x) {
+        const int k = u / nb;
+        const int b = u - k * nb;
+        const double2 zk = z[b * cs + (k == n ? 0 : k)];
+        const double2 zn = cconj(z[b * cs + (k == 0 ? 0 : n - k)]);
+        const double2 a = cadd(zk, zn);
+        const double2 w = __ldg(plan.post + k);
+        const double2 wb = cmul(w, csub(zk, zn));
+        const double2 x = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
+        out[(long long)k * out_fs + (long long)(c0 + b) * out_cs] = to_out<TOut>(x);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K9: fused frequency-major load + C2R + unpad + epilogue
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_c2r(const double2* __restrict__ in, long long in_fs,
+                                                  long long in_cs, double* __restrict__ out,
+                                                  long long out_cs, int channels, int nt,
+                                                  FftPlanDev plan, int batch, C2REpilogue epi) {
+    extern __shared__ double2 smem[];
+    const int n = plan.n;
+    const int cs = fft_channel_stride(n);
+    double2* buf_a = smem;
+    double2* buf_b = smem + (size_t)batch * cs;
+    const int c0 = blockIdx.x * batch;
+    const int nb = min(batch, channels - c0);
+
+    for (int u = threadIdx.x; u < nb * (n + 1); u += blockDim.x) {
+        const int k = u / nb;
+        const int b = u - k * nb;
+        buf_a[b * cs + k] = __ldg(in + (long long)k * in_fs + (long long)(c0 + b) * in_cs);
+    }
+    __syncthreads();
+    // Z_k = (1/2n) [ (X_k + conj X_{n-k}) + i conj(W_{2n}^k) (X_k - conj X_{n-k}) ], k < n
+    const double inv_len = 0.5 / static_cast<double>(n);
+    for (int u = threadIdx.x; u < nb * n; u += blockDim.x) {
+        const int b = u / n;
+        const int k = u - b * n;
+        const double2 xk = buf_a[b * cs + k];
+        const double2 xn = cconj(buf_a[b * cs + n - k]);
+        const double2 e = cadd(xk, xn);
+        const double2 o = cmul(csub(xk, xn), cconj(__ldg(plan.post + k)));
+        buf_b[b * cs + k] = make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
+    }
+    __syncthreads();
+    const double2* z = fft_smem<+1>(buf_b, buf_a, nb, cs, plan);
+    const double* zd = reinterpret_cast<const double*>(z);
+
+    for (int u = threadIdx.x; u < nb * nt; u += blockDim.x) {
+        const int b = u / nt;
+        const int t = u - b * nt;
+        const int c = c0 + b;
+        double y = zd[2 * cs * b + t];
+        if (epi.gamma_mode == 1) {
+            y *= __ldg(epi.gamma + (c % epi.gamma_dim));
+        } else if (epi.gamma_mode == 2) {
+            y *= __ldg(epi.gamma + (long long)(c % epi.gamma_dim) * nt + t);
+        }
+        const long long o = (long long)c * out_cs + t;
+        if (epi.v) {
+            const double* vr = epi.v + (long long)c * out_cs;
+            double r = vr[t];
+            if (epi.reg_kind == 1) {
+                r = 2.0 * r;
+                if (t > 0) r -= vr[t - 1];
+                if (t + 1 < nt) r -= vr[t + 1];
+            }
+            y += epi.alpha * r;
+        }
+        out[o] = y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7 forward: one CTA = ROWS rows of one frequency, full sweep over j.
+// ---------------------------------------------------------------------------
+template <typename TF, int VEC, int ROWS, int UNR>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_gemv_fwd(const TF* __restrict__ F, const double2* __restrict__ x, double2* __restrict__ y,
+               int nd, int nm) {
+    const int f = blockIdx.y;
+    const int i0 = blockIdx.x * ROWS;
+    const int nr = min(ROWS, nd - i0);
+    const TF* fb = F + ((size_t)f * nd + i0) * nm;
+    const double2* xf = x + (size_t)f * nm;
+    const uint64_t pol = evict_first_policy();
+
+    double ar[ROWS], ai[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) ar[r] = ai[r] = 0.0;
+
+    constexpr int kStep = kThreads * VEC;
+    int j = threadIdx.x * VEC;
+    for (; j + (UNR - 1) * kStep + VEC <= nm; j += UNR * kStep) {
+        double2 xv[UNR][VEC];
+        double2 fv[UNR][ROWS][VEC];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) xv[u][v] = __ldg(xf + j + u * kStep + v);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                if (r < nr) {
+                    FLoad<TF, VEC>::load(fb + (size_t)r * nm + j + u * kStep, pol, fv[u][r]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) fv[u][r][v] = make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], fv[u][r][v], xv[u][v]);
+    }
+    for (; j < nm; j += kStep) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            if (j + v < nm) {
+                const double2 xv = __ldg(xf + j + v);
+#pragma unroll
+                for (int r = 0; r < ROWS; ++r)
+                    if (r < nr) cmac(ar[r], ai[r], FLoad<TF, VEC>::scalar(fb + (size_t)r * nm + j + v), xv);
+            }
+        }
+    }
+
+    // Fixed-order block reduction: xor-butterfly within warps, then warps in order.
+    __shared__ double red[kThreads / 32][ROWS][2];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
+            ai[r] += __shfl_xor_sync(0xffffffffu, ai[r], o);
+        }
+        if (lane == 0) {
+            red[warp][r][0] = ar[r];
+            red[warp][r][1] = ai[r];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+        double sr = 0.0, si = 0.0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+            sr += red[w][threadIdx.x][0];
+            si += red[w][threadIdx.x][1];
+        }
+        y[(size_t)f * nd + i0 + threadIdx.x] = make_double2(sr, si);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7 adjoint: one thread = JPT*VEC columns of one frequency, loop over rows
+// i ascending (the reference's accumulation order, block_operator.cpp:306-310).
+// ---------------------------------------------------------------------------
+template <typename TF, int VEC, int JPT, int UNR, bool kSmemD>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_gemv_adj(const TF* __restrict__ F, const double2* __restrict__ x, double2* __restrict__ y,
+               int nd, int nm) {
+    extern __shared__ double2 sd[];
+    const int f = blockIdx.y;
+    const double2* xf = x + (size_t)f * nd;
+    if constexpr (kSmemD) {
+        for (int i = threadIdx.x; i < nd; i += kThreads) sd[i] = xf[i];
+        __syncthreads();
+    }
+    const double2* dsrc = kSmemD ? sd : xf;
+    const TF* ff = F + (size_t)f * nd * nm;
+    const uint64_t pol = evict_first_policy();
+    constexpr int kStep = kThreads * VEC;
+    const int jb = blockIdx.x * (kStep * JPT) + threadIdx.x * VEC;
+
+    double ar[JPT][VEC], ai[JPT][VEC];
+#pragma unroll
+    for (int q = 0; q < JPT; ++q)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) ar[q][v] = ai[q][v] = 0.0;
+
+    if (jb + (JPT - 1) * kStep + VEC <= nm) {
+        int i = 0;
+        for (; i + UNR <= nd; i += UNR) {
+            double2 fv[UNR][JPT][VEC];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int q = 0; q < JPT; ++q)
+                    FLoad<TF, VEC>::load(ff + (size_t)(i + u) * nm + jb + q * kStep, pol, fv[u][q]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const double2 w = dsrc[i + u];
+#pragma unroll
+                for (int q = 0; q < JPT; ++q)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[u][q][v], w);
+            }
+        }
+        for (; i < nd; ++i) {
+            const double2 w = dsrc[i];
+#pragma unroll
+            for (int q = 0; q < JPT; ++q) {
+                double2 fv[VEC];
+                FLoad<TF, VEC>::load(ff + (size_t)i * nm + jb + q * kStep, pol, fv);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[v], w);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < JPT; ++q)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+                y[(size_t)f * nm + jb + q * kStep + v] = make_double2(ar[q][v], ai[q][v]);
+    } else {
+        for (int i = 0; i < nd; ++i) {
+            const double2 w = dsrc[i];
+#pragma unroll
+            for (int q = 0; q < JPT; ++q)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    const int j = jb + q * kStep + v;
+                    if (j < nm)
+                        cmac_conj(ar[q][v], ai[q][v], FLoad<TF, VEC>::scalar(ff + (size_t)i * nm + j), w);
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < JPT; ++q)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const int j = jb + q * kStep + v;
+                if (j < nm) y[(size_t)f * nm + j] = make_double2(ar[q][v], ai[q][v]);
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// indexable synthetic inputs
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_fill_uniform(double* __restrict__ out, size_t n, uint64_t seed, uint64_t offset,
+                               double lo, double span) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const uint64_t u = splitmix64(seed ^ (offset + k));
+        out[k] = lo + span * (static_cast<double>(u >> 11) * 0x1.0p-53);
+    }
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+int sm_count() {
+    static int count = [] {
+        int dev = 0, c = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        return c;
+    }();
+    return count;
+}
+
+}  // namespace
+
+size_t fft_smem_bytes(int n, int batch) {
+    return 2ull * (size_t)batch * (size_t)fft_channel_stride(n) * sizeof(double2);
+}
+
+int fft_batch(int n, size_t smem_budget, int want) {
+    const size_t per = fft_smem_bytes(n, 1);
+    int b = static_cast<int>(smem_budget / per);
+    if (b < 1) return 0;
+    return std::min(b, want);
+}
+
+template <typename TOut>
+cudaError_t launch_r2c(const double* in, long long in_cs, long long in_ts, TOut* out,
+                       long long out_fs, long long out_cs, int channels, int nt,
+                       const FftPlanDev& plan, int batch, cudaStream_t stream) {
+    if (channels <= 0) return cudaSuccess;
+    const size_t smem = fft_smem_bytes(plan.n, batch);
+    cudaError_t e = set_smem(k_r2c<TOut>, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (channels + batch - 1) / batch;
+    k_r2c<TOut><<<grid, kThreads, smem, stream>>>(in, in_cs, in_ts, out, out_fs, out_cs, channels,
+                                                  nt, plan, batch);
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_r2c<double2>(const double*, long long, long long, double2*, long long,
+                                         long long, int, int, const FftPlanDev&, int, cudaStream_t);
+template cudaError_t launch_r2c<float2>(const double*, long long, long long, float2*, long long,
+                                        long long, int, int, const FftPlanDev&, int, cudaStream_t);
+
+cudaError_t launch_c2r(const double2* in, long long in_fs, long long in_cs, double* out,
+                       long long out_cs, int channels, int nt, const FftPlanDev& plan, int batch,
+                       const C2REpilogue& epi, cudaStream_t stream) {
+    if (channels <= 0) return cudaSuccess;
+    const size_t smem = fft_smem_bytes(plan.n, batch);
+    cudaError_t e = set_smem(k_c2r, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (channels + batch - 1) / batch;
+    k_c2r<<<grid, kThreads, smem, stream>>>(in, in_fs, in_cs, out, out_cs, channels, nt, plan,
+                                            batch, epi);
+    return cudaGetLastError();
+}
+
+template <typename TF>
+cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream) {
+    constexpr int kRows = 8;
+    dim3 grid((nd + kRows - 1) / kRows, nf);
+    if constexpr (sizeof(TF) == 8) {
+        if ((nm & 1) == 0) {
+            k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+            return cudaGetLastError();
+        }
+    }
+    k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+    return cudaGetLastError();
+}
+
+template <typename TF, int VEC>
+cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                           cudaStream_t stream) {
+    constexpr int kJpt = 2;
+    constexpr int kUnr = 8;
+    dim3 grid((nm + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nf);
+    const size_t smem = (size_t)nd * sizeof(double2);
+    if (smem <= 96 * 1024) {
+        auto kern = k_gemv_adj<TF, VEC, kJpt, kUnr, true>;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kThreads, smem, stream>>>(F, x, y, nd, nm);
+    } else {
+        k_gemv_adj<TF, VEC, kJpt, kUnr, false><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+    }
+    return cudaGetLastError();
+}
+
+template <typename TF>
+cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream) {
+    if constexpr (sizeof(TF) == 8) {
+        if ((nm & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, stream);
+    }
+    return launch_adj_vec<TF, 1>(F, x, y, nf, nd, nm, stream);
+}
+
+template cudaError_t launch_gemv_fwd<double2>(const double2*, const double2*, double2*, int, int,
+                                              int, cudaStream_t);
+template cudaError_t launch_gemv_fwd<float2>(const float2*, const double2*, double2*, int, int,
+                                             int, cudaStream_t);
+template cudaError_t launch_gemv_adj<double2>(const double2*, const double2*, double2*, int, int,
+                                              int, cudaStream_t);
+template cudaError_t launch_gemv_adj<float2>(const float2*, const double2*, double2*, int, int,
+                                             int, cudaStream_t);
+
+cudaError_t launch_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo,
+                                double hi, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    const size_t want = (n + kThreads - 1) / kThreads;
+    const int grid = static_cast<int>(std::min<size_t>(want, (size_t)sm_count() * 16));
+    k_fill_uniform<<<grid, kThreads, 0, stream>>>(out, n, seed, offset, lo, hi - lo);
+    return cudaGetLastError();
+}
+
+}  // namespace btg

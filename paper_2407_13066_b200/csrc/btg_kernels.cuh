@@ -1,0 +1,58 @@
+// Launch interface of the sm_100a kernels behind the C ABI (btg_capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "btg_fft.cuh"
+
+namespace btg {
+
+// Epilogue of the C2R kernel: y = x * gamma (optional) + alpha * R(v) (optional).
+struct C2REpilogue {
+    const double* gamma = nullptr;  // per channel (mode 1) or per (channel, t) (mode 2)
+    int gamma_mode = 0;
+    int gamma_dim = 1;              // channels per right-hand side (gamma index = c % gamma_dim)
+    const double* v = nullptr;      // SOTI vector sharing the output layout
+    double alpha = 0.0;
+    int reg_kind = 0;               // 0 identity, 1 temporal Laplacian (inverse.cpp:32-49)
+};
+
+// Per-channel shared-memory footprint (complex elements) of an FFT of length n.
+__host__ __device__ inline int fft_channel_stride(int n) { return n + 1; }
+
+// Channels per CTA for the FFT kernels given the smem budget.
+int fft_batch(int n, size_t smem_budget, int want);
+size_t fft_smem_bytes(int n, int batch);
+
+// Real-to-complex along time of C channels: channel c sample t at
+// in[c*in_cs + t*in_ts] (t < nt, zero-padded to 2nt); frequency k <= nt lands
+// at out[k*out_fs + c*out_cs]. TOut = double2 (FP64) or float2 (FP32 F-hat).
+template <typename TOut>
+cudaError_t launch_r2c(const double* in, long long in_cs, long long in_ts, TOut* out,
+                       long long out_fs, long long out_cs, int channels, int nt,
+                       const FftPlanDev& plan, int batch, cudaStream_t stream);
+
+// Complex-to-real: frequency k <= nt of channel c at in[k*in_fs + c*in_cs];
+// output time t < nt (1/(2nt) normalised, real part) at out[c*out_cs + t],
+// through the epilogue.
+cudaError_t launch_c2r(const double2* in, long long in_fs, long long in_cs, double* out,
+                       long long out_cs, int channels, int nt, const FftPlanDev& plan,
+                       int batch, const C2REpilogue& epi, cudaStream_t stream);
+
+// Fourier-space step, one right-hand side: y[f][i] = sum_j F[f][i][j] x[f][j].
+template <typename TF>
+cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream);
+
+// Adjoint: y[f][j] = sum_i conj(F[f][i][j]) x[f][i].
+template <typename TF>
+cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream);
+
+cudaError_t launch_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo,
+                                double hi, cudaStream_t stream);
+
+}  // namespace btg
