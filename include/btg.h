@@ -108,7 +108,9 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
                        size_t nrhs, const double* gamma_inv, int gamma_kind, double alpha,
                        int reg_kind, unsigned flags);
 
-/* Run subsequent work on `stream` (a cudaStream_t; NULL = the handle's own). */
+/* Run subsequent work on `stream` (a cudaStream_t). NULL selects the handle's
+ * own non-blocking stream; pass cudaStreamLegacy ((void*)0x1) for the legacy
+ * default stream. Device-pointer calls are asynchronous on that stream. */
 btg_status btg_set_stream(btg_op op, void* stream);
 btg_status btg_synchronize(btg_op op);
 btg_status btg_set_timing(btg_op op, int enabled);

@@ -218,6 +218,23 @@ int ref_distributed_adjoint(void* h, const double* d, double* m, int parallel) {
     });
 }
 
+// HessianOperator::apply's partition branch (inverse.cpp:80-85) plus the
+// penalty add (:87-89); the operator pointer only has to be non-null there.
+int ref_distributed_hessian(void* h, const double* v, double* hv, double alpha, int reg_kind,
+                            int parallel) {
+    return guarded([&] {
+        const Partition& part = static_cast<PartitionHandle*>(h)->partition;
+        SpectralP2O placeholder;
+        HessianOperator hess;
+        hess.op = &placeholder;
+        hess.partition = &part;
+        hess.engine.policy = parallel ? ExecutionPolicy::Parallel : ExecutionPolicy::Serial;
+        hess.reg.kind = reg_kind ? RegKind::TemporalLaplacian : RegKind::ScaledIdentity;
+        hess.reg.alpha = alpha;
+        copy_out(hess.apply(make_soti(v, part.num_sources, part.num_steps)), hv);
+    });
+}
+
 // ---- the reference's own invariant suite (verify.cpp:72-250) ------------------
 int ref_verify(std::uint64_t seed, char* report, std::size_t report_len, int* passed) {
     return guarded([&] {

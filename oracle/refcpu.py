@@ -50,6 +50,8 @@ def lib():
         L.ref_partition_bounds.argtypes = [ctypes.c_void_p, ctypes.POINTER(_size_t)]
         for name in ("ref_distributed_forward", "ref_distributed_adjoint"):
             getattr(L, name).argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int]
+        L.ref_distributed_hessian.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double,
+                                              ctypes.c_int, ctypes.c_int]
         L.ref_verify.argtypes = [ctypes.c_uint64, ctypes.c_char_p, _size_t, ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
@@ -184,6 +186,12 @@ class RefPartition:
         m = np.empty((self.num_sources, self.num_steps))
         _check(lib().ref_distributed_adjoint(self._h, _p(d), _p(m), int(parallel)))
         return m
+
+    def hessian(self, v, alpha: float = 0.0, reg_kind: int = 0, parallel: bool = False) -> np.ndarray:
+        v = _f64(v)
+        hv = np.empty_like(v)
+        _check(lib().ref_distributed_hessian(self._h, _p(v), _p(hv), float(alpha), int(reg_kind), int(parallel)))
+        return hv
 
 
 def verify(seed: int = 20240901):

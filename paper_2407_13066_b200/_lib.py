@@ -14,6 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
 BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID = range(7)
 BTG_F64, BTG_F32 = 64, 32
 BTG_DEVICE_PTRS = 0x1
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's stream 0)
 BTG_REG_IDENTITY, BTG_REG_TEMPORAL_LAPLACIAN = 0, 1
 BTG_GAMMA_NONE, BTG_GAMMA_PER_SENSOR, BTG_GAMMA_PER_SAMPLE = 0, 1, 2
 

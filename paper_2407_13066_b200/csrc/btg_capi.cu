@@ -13,6 +13,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -88,6 +89,9 @@ struct btg_op_s {
     btg::FftPlanDev plan{};
     double2* d_tw = nullptr;
     double2* d_post = nullptr;
+    double2* d_fast = nullptr;  // split twiddle tables of the compile-time-N FFTs
+    btg::FastTables fast{};
+    bool fast_ok = false;
     int fft_batch = 1;        // channels per CTA for vector transforms
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
 
@@ -220,10 +224,16 @@ btg_status host_buffers(btg_op op, size_t nin, size_t nout) {
 }
 
 // ---- pipeline pieces --------------------------------------------------------
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out) {
     StageClock clk(op, &op->counters.forward_fft);
-    BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)channels, 1,
-                                      (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream));
+    if (op->fast_ok && aligned16(v) && aligned16(out))
+        BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, (long long)channels,
+                                          (int)channels, op->fast, op->stream));
+    else
+        BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)channels, 1,
+                                          (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream));
     op->counters.launches++;
     op->counters.forward_fft.ops += fft_ops(channels, op->nt);
     op->counters.forward_fft.bytes += 8.0 * channels * op->nt + 16.0 * op->nf * channels;
@@ -233,8 +243,12 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
 btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* out,
                        const btg::C2REpilogue& epi) {
     StageClock clk(op, &op->counters.inverse_fft);
-    BTG_CUDA(btg::launch_c2r(in, (long long)channels, 1, out, (long long)op->nt, (int)channels,
-                             (int)op->nt, op->plan, op->fft_batch, epi, op->stream));
+    if (op->fast_ok && aligned16(in) && aligned16(out))
+        BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)channels, out, (long long)op->nt,
+                                          (int)channels, op->fast, epi, op->stream));
+    else
+        BTG_CUDA(btg::launch_c2r(in, (long long)channels, 1, out, (long long)op->nt, (int)channels,
+                                 (int)op->nt, op->plan, op->fft_batch, epi, op->stream));
     op->counters.launches++;
     op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
     op->counters.inverse_fft.bytes += 16.0 * op->nf * channels + 8.0 * channels * op->nt;
@@ -379,6 +393,23 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
     if (e == cudaSuccess)
         e = cudaMemcpy(op->d_post, post.data(), (nt + 1) * sizeof(double2), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cleanup_fail(fail(BTG_ECUDA, "twiddles: %s", cudaGetErrorString(e)));
+    if (btg::fast_fft_supported((int)nt) && !std::getenv("BTG_DISABLE_FAST_FFT")) {
+        const int hi = btg::fast_fft_hi_count((int)nt);
+        std::vector<double2> t(32 + hi + 32 + hi + 1);
+        for (int i = 0; i < 32; ++i) t[i] = root(i, (long long)nt);
+        for (int h = 0; h < hi; ++h) t[32 + h] = root(32LL * h, (long long)nt);
+        for (int i = 0; i < 32; ++i) t[32 + hi + i] = root(i, 2 * (long long)nt);
+        for (int h = 0; h <= hi; ++h) t[64 + hi + h] = root(32LL * h, 2 * (long long)nt);
+        e = cudaMalloc(&op->d_fast, t.size() * sizeof(double2));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(op->d_fast, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cleanup_fail(fail(BTG_ECUDA, "fast twiddles: %s", cudaGetErrorString(e)));
+        op->fast.lo = op->d_fast;
+        op->fast.hi = op->d_fast + 32;
+        op->fast.post_lo = op->d_fast + 32 + hi;
+        op->fast.post_hi = op->d_fast + 64 + hi;
+        op->fast_ok = true;
+    }
     op->plan.n = (int)nt;
     op->plan.nfac = (int)fac.size();
     for (size_t i = 0; i < fac.size(); ++i) op->plan.fac[i] = fac[i];
@@ -624,6 +655,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->F);
         cudaFree(op->d_tw);
         cudaFree(op->d_post);
+        cudaFree(op->d_fast);
         cudaFree(op->wa);
         cudaFree(op->wb);
         cudaFree(op->wt);

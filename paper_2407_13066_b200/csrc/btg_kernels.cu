@@ -524,3 +524,74 @@ cudaError_t launch_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t o
 }
 
 }  // namespace btg
+
+// ---------------------------------------------------------------------------
+// compile-time-N vector FFTs (btg_fft_fast.cuh)
+// ---------------------------------------------------------------------------
+#include "btg_fft_fast.cuh"
+
+namespace btg {
+namespace {
+
+template <int N>
+cudaError_t r2c_fast_n(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
+                       const FastTables& tabs, cudaStream_t stream) {
+    using P = fast::FastPlan<N>;
+    constexpr size_t smem = fast::smem_bytes<N>();
+    auto kern = fast::k_r2c_fast<N>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (channels + P::CPB - 1) / P::CPB;
+    kern<<<grid, P::TPC * P::CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs);
+    return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
+                       const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
+    using P = fast::FastPlan<N>;
+    constexpr size_t smem = fast::smem_bytes<N>();
+    auto kern = fast::k_c2r_fast<N>;
+    cudaError_t e = set_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (channels + P::CPB - 1) / P::CPB;
+    kern<<<grid, P::TPC * P::CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
+    return cudaGetLastError();
+}
+
+#define BTG_FAST_SIZES(X) X(64) X(128) X(256) X(500) X(512) X(1000) X(1024) X(2000) X(2048) X(4096)
+
+}  // namespace
+
+bool fast_fft_supported(int n) {
+#define BTG_CASE(N) \
+    if (n == N) return true;
+    BTG_FAST_SIZES(BTG_CASE)
+#undef BTG_CASE
+    return false;
+}
+
+int fast_fft_hi_count(int n) { return (n + fast::kTwLo - 1) / fast::kTwLo + 1; }
+
+cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double2* out, long long out_fs,
+                                int channels, const FastTables& tabs, cudaStream_t stream) {
+    if (channels <= 0) return cudaSuccess;
+#define BTG_CASE(N) \
+    if (n == N) return r2c_fast_n<N>(in, in_cs, out, out_fs, channels, tabs, stream);
+    BTG_FAST_SIZES(BTG_CASE)
+#undef BTG_CASE
+    return cudaErrorNotSupported;
+}
+
+cudaError_t launch_c2r_vec_fast(int n, const double2* in, long long in_fs, double* out, long long out_cs,
+                                int channels, const FastTables& tabs, const C2REpilogue& epi,
+                                cudaStream_t stream) {
+    if (channels <= 0) return cudaSuccess;
+#define BTG_CASE(N) \
+    if (n == N) return c2r_fast_n<N>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+    BTG_FAST_SIZES(BTG_CASE)
+#undef BTG_CASE
+    return cudaErrorNotSupported;
+}
+
+}  // namespace btg

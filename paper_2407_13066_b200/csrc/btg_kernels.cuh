@@ -20,6 +20,27 @@ struct C2REpilogue {
     int reg_kind = 0;               // 0 identity, 1 temporal Laplacian (inverse.cpp:32-49)
 };
 
+// Split twiddle tables of the compile-time-N vector FFTs (btg_fft_fast.cuh):
+// lo[i] = W_N^i (i < 32), hi[h] = W_N^{32h}; post_* the same for W_{2N}.
+struct FastTables {
+    const double2* lo = nullptr;
+    const double2* hi = nullptr;
+    const double2* post_lo = nullptr;
+    const double2* post_hi = nullptr;
+};
+
+// Lengths N = N_t with a register-resident compile-time plan.
+bool fast_fft_supported(int n);
+int fast_fft_hi_count(int n);  // entries of hi (post_hi has one more)
+
+// SOTI rows (16-byte aligned) -> frequency-major; returns cudaErrorNotSupported
+// when N has no compile-time plan.
+cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double2* out, long long out_fs,
+                                int channels, const FastTables& tabs, cudaStream_t stream);
+cudaError_t launch_c2r_vec_fast(int n, const double2* in, long long in_fs, double* out, long long out_cs,
+                                int channels, const FastTables& tabs, const C2REpilogue& epi,
+                                cudaStream_t stream);
+
 // Per-channel shared-memory footprint (complex elements) of an FFT of length n.
 __host__ __device__ inline int fft_channel_stride(int n) { return n + 1; }
 

@@ -164,7 +164,11 @@ class SpectralOperator:
 
     # -- internals ------------------------------------------------------------
     def _bind_stream(self, t) -> None:
-        ptr = _torch_stream_ptr(t) if t is not None else None
+        """Run on torch's current stream for tensor inputs (its legacy default
+        stream 0 maps to cudaStreamLegacy), on the handle's own stream otherwise."""
+        ptr = None
+        if t is not None:
+            ptr = _torch_stream_ptr(t) or _lib.CUDA_STREAM_LEGACY
         check(_lib.load().btg_set_stream(self._h, ptr))
 
     def _prep_torch(self, t):

@@ -223,7 +223,7 @@ def test_multiple_right_hand_sides(btg):
         assert R.rel_l2(H[r], R.hessian_apply(spec, M[r], 0.2, 1)) <= TOL64
 
 
-@pytest.mark.parametrize("nt", [1, 2, 7, 97, 125, 1000, 1001])
+@pytest.mark.parametrize("nt", [1, 2, 7, 64, 97, 125, 128, 256, 500, 512, 1000, 1001, 1024, 2000, 2048, 4096])
 def test_fft_lengths(btg, nt):
     """Radix 2/4/8, 5 (N_t=1000 -> 2N_t=2000, configs[2]), 3, 7 and generic primes."""
     blocks, m, d = R.random_problem(100 + nt, 3, 9, nt)
@@ -262,3 +262,21 @@ def test_baseline_shape_slice_vs_reference_build(btg):
         assert R.rel_l2(op.apply_forward(m), ref.apply_forward(m)) <= TOL64
         assert R.rel_l2(op.apply_adjoint(d), ref.apply_adjoint(d)) <= TOL64
         assert R.rel_l2(op.hessian_apply(m), ref.hessian_apply(m, 0.0, 0)) <= TOL64
+
+
+def test_fast_and_generic_fft_paths_agree(btg, monkeypatch):
+    """The compile-time-N register FFT (default for N_t in its plan table) and the
+    generic shared-memory Stockham (BTG_DISABLE_FAST_FFT) give the same matvec."""
+    blocks, m, d = R.random_problem(77, 5, 130, 1024)
+    spec = R.setup_full(blocks)
+    with btg.setup(blocks) as fast_op:
+        f1, a1 = fast_op.apply_forward(m), fast_op.apply_adjoint(d)
+        h1 = fast_op.hessian_apply(m, alpha=0.2, reg="temporal-laplacian", gamma_inv=np.linspace(0.5, 2, 5))
+    monkeypatch.setenv("BTG_DISABLE_FAST_FFT", "1")
+    with btg.setup(blocks) as gen_op:
+        f2, a2 = gen_op.apply_forward(m), gen_op.apply_adjoint(d)
+        h2 = gen_op.hessian_apply(m, alpha=0.2, reg="temporal-laplacian", gamma_inv=np.linspace(0.5, 2, 5))
+    for got, other, want in ((f1, f2, R.apply_forward(spec, m)), (a1, a2, R.apply_adjoint(spec, d)),
+                             (h1, h2, R.gauss_newton_apply(spec, m, np.linspace(0.5, 2, 5), 0.2, 1))):
+        assert R.rel_l2(got, want) <= TOL64
+        assert R.rel_l2(other, want) <= TOL64
