@@ -207,23 +207,15 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def build_operator(btg, torch, cfg, device, seed, col_offset=0, nm_total=None):
-    """Synthetic F-hat: the TOSI first block column is generated on the device
-    slab by slab (indexable SplitMix64 uniform(-1,1)) and transformed with
-    btg_setup_rows, so blocks and F-hat never coexist in full."""
+def build_operator(cfg, device, seed):
+    """Synthetic F-hat on one GPU: the indexable first block column (entry
+    (k,i,j) = uniform(seed ^ ((k N_d + i) N_m + j))) is generated on the device
+    slab by slab and transformed with btg_setup_rows, so blocks and F-hat never
+    coexist in full."""
+    from paper_2407_13066_b200.distributed import Shard, synthetic_shard_operator
+
     nt, nd, nm = cfg["nt"], cfg["nd"], cfg["nm"]
-    op = btg.create(nd, nm, nt, 64, device)
-    slab_rows = max(1, min(nd, (2 << 30) // (8 * nt * nm)))
-    slab = torch.empty((nt, slab_rows, nm), dtype=torch.float64, device=f"cuda:{device}")
-    for i0 in range(0, nd, slab_rows):
-        i1 = min(nd, i0 + slab_rows)
-        buf = slab[:, : i1 - i0, :] if i1 - i0 == slab_rows else torch.empty(
-            (nt, i1 - i0, nm), dtype=torch.float64, device=f"cuda:{device}")
-        btg.fill_uniform(buf, seed=seed + i0, offset=col_offset)
-        op.setup_rows(buf, i0, i1)
-    torch.cuda.synchronize(device)
-    del slab
-    return op
+    return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), seed, device)
 
 
 def run_ours(args):
@@ -248,7 +240,7 @@ def run_ours(args):
 
     t0 = time.perf_counter()
     if world == 1:
-        op = build_operator(btg, torch, cfg, device, seed=1000)
+        op = build_operator(cfg, device, seed=1000)
         engine = None
         grid = "1x1"
     else:
@@ -420,7 +412,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: device SplitMix64 uniform(-1,1) first block column (seed 1000+row), m (seed 7), "
+            "data": "synthetic: device SplitMix64 uniform(-1,1) first block column (seed 1000, global index), m (seed 7), "
                     "Gamma^-1 uniform(0.5,2) per sensor (seed 8)",
             "config": {"workload": cfg["label"], "N_t": nt, "N_d": nd, "N_m": nm, "nrhs": 1, "grid": grid,
                        "step": "F m + F* d + F* Gamma^-1 F v (alpha=0), FP64, F-hat N_t+1 frequencies",

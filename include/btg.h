@@ -108,6 +108,23 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
                        size_t nrhs, const double* gamma_inv, int gamma_kind, double alpha,
                        int reg_kind, unsigned flags);
 
+/* Fused output epilogue of one direction (the C2R store, K9): y = Gamma^-1 x
+ * (gamma_kind != NONE; per output channel or per (channel, t)) + alpha R reg_v
+ * (alpha != 0; reg_v has the output's layout). Used to compose the
+ * Gauss-Newton action across a processor grid without extra passes. */
+typedef struct {
+    const double* gamma_inv;
+    int gamma_kind;
+    const double* reg_v;
+    double alpha;
+    int reg_kind;
+} btg_epilogue;
+
+btg_status btg_forward_ex(btg_op op, const double* m, size_t m_len, double* d, size_t d_len,
+                          size_t nrhs, const btg_epilogue* epi, unsigned flags);
+btg_status btg_adjoint_ex(btg_op op, const double* d, size_t d_len, double* m, size_t m_len,
+                          size_t nrhs, const btg_epilogue* epi, unsigned flags);
+
 /* Run subsequent work on `stream` (a cudaStream_t). NULL selects the handle's
  * own non-blocking stream; pass cudaStreamLegacy ((void*)0x1) for the legacy
  * default stream. Device-pointer calls are asynchronous on that stream. */
@@ -135,6 +152,12 @@ void btg_destroy(btg_op op);
  * slice is reproducible on the host. `out` is a device pointer. */
 btg_status btg_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo,
                             double hi, void* stream);
+
+/* 3-D strided variant: out[(a*nb + b)*nc + c] = the same stream at global
+ * index offset + a*stride_a + b*stride_b + c (a TOSI slab of a larger operator). */
+btg_status btg_fill_uniform_3d(double* out, size_t na, size_t nb, size_t nc, uint64_t seed,
+                               uint64_t offset, uint64_t stride_a, uint64_t stride_b, double lo,
+                               double hi, void* stream);
 
 #ifdef __cplusplus
 }

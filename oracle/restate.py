@@ -267,3 +267,27 @@ def tree_reduce(partials):
             parts[i] += parts[i + step]
         step *= 2
     return parts[0]
+
+
+# ---------------------------------------------------------------------------
+# Host twin of the product's indexable synthetic generator (btg_fill_uniform):
+# value at global index g = lo + (hi-lo) * ((splitmix64(seed ^ g) >> 11) * 2^-53).
+# Lets tests regenerate any slice of a device-generated full-size operator.
+# ---------------------------------------------------------------------------
+def splitmix_uniform(seed: int, idx, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        x = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) ^ np.asarray(idx, dtype=np.uint64)
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return lo + (hi - lo) * ((z >> np.uint64(11)).astype(np.float64) * 2.0**-53)
+
+
+def synthetic_blocks_slice(seed, nd, nm, nt, sensors, sources):
+    """Entries (k, i, j) of the synthetic first block column for the given
+    sensor / source index arrays: uniform(seed ^ ((k*N_d + i)*N_m + j))."""
+    k = np.arange(nt, dtype=np.uint64)[:, None, None]
+    i = np.asarray(sensors, dtype=np.uint64)[None, :, None]
+    j = np.asarray(sources, dtype=np.uint64)[None, None, :]
+    return splitmix_uniform(seed, (k * np.uint64(nd) + i) * np.uint64(nm) + j)

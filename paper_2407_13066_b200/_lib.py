@@ -38,6 +38,9 @@ EXPORTED = (
     "btg_spectrum_device",
     "btg_destroy",
     "btg_fill_uniform",
+    "btg_forward_ex",
+    "btg_adjoint_ex",
+    "btg_fill_uniform_3d",
 )
 
 
@@ -55,6 +58,18 @@ class OrderingError(ValueError):
 
 class GridError(ValueError):
     """btoep::GridError (errors.hpp:28-30)."""
+
+
+class Epilogue(ctypes.Structure):
+    """btg_epilogue: fused Gamma^-1 / alpha R v store epilogue."""
+
+    _fields_ = [
+        ("gamma_inv", ctypes.c_void_p),
+        ("gamma_kind", ctypes.c_int),
+        ("reg_v", ctypes.c_void_p),
+        ("alpha", ctypes.c_double),
+        ("reg_kind", ctypes.c_int),
+    ]
 
 
 class _Stage(ctypes.Structure):
@@ -120,6 +135,10 @@ def load():
     L.btg_destroy.restype = None
     L.btg_fill_uniform.argtypes = [_dp, _sz, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
                                    ctypes.c_double, _vp]
+    L.btg_forward_ex.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.POINTER(Epilogue), ctypes.c_uint]
+    L.btg_adjoint_ex.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.POINTER(Epilogue), ctypes.c_uint]
+    L.btg_fill_uniform_3d.argtypes = [_dp, _sz, _sz, _sz, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _vp]
     for name in EXPORTED:
         if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
             getattr(L, name).restype = ctypes.c_int

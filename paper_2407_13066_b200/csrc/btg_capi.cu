@@ -311,8 +311,16 @@ btg_status finish_host(btg_op op, double* out_host, const double* out_dev, size_
     return BTG_OK;
 }
 
+// Device-side copy of a host epilogue operand (gamma or reg_v).
+btg_status stage_small(btg_op op, const double* src, size_t n, double*& buf, size_t& cap, const double** dev) {
+    BTG_TRY(grow(buf, cap, n));
+    BTG_CUDA(cudaMemcpyAsync(buf, src, n * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+    *dev = buf;
+    return BTG_OK;
+}
+
 btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, double* out,
-                     size_t out_len, size_t nrhs, unsigned flags) {
+                     size_t out_len, size_t nrhs, const btg_epilogue* ex, unsigned flags) {
     BTG_TRY(check_ready(op));
     if (nrhs == 0) return fail(BTG_EARG, "nrhs must be >= 1");
     if (!in || !out) return fail(BTG_EARG, "null vector pointer");
@@ -321,6 +329,15 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
     const size_t dout = adjoint ? op->nm : op->nd;
     BTG_TRY(check_len(what, in_len, din, op->nt, nrhs, din));
     BTG_TRY(check_len(what, out_len, dout, op->nt, nrhs, dout));
+    btg::C2REpilogue epi{};
+    if (ex) {
+        if (ex->gamma_kind < BTG_GAMMA_NONE || ex->gamma_kind > BTG_GAMMA_PER_SAMPLE)
+            return fail(BTG_EARG, "unknown gamma kind %d", ex->gamma_kind);
+        if (ex->gamma_kind != BTG_GAMMA_NONE && !ex->gamma_inv) return fail(BTG_EARG, "gamma_inv is null");
+        if (ex->reg_kind != BTG_REG_IDENTITY && ex->reg_kind != BTG_REG_TEMPORAL_LAPLACIAN)
+            return fail(BTG_EARG, "unknown regularization kind %d", ex->reg_kind);
+        if (ex->alpha != 0.0 && !ex->reg_v) return fail(BTG_EARG, "reg_v is null with alpha != 0");
+    }
     DeviceGuard g(op->device);
     const double* din_p = in;
     double* dout_p = out;
@@ -330,7 +347,29 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
         din_p = op->hin;
         dout_p = op->hout;
     }
-    BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, btg::C2REpilogue{}));
+    if (ex && ex->gamma_kind != BTG_GAMMA_NONE) {
+        epi.gamma_mode = ex->gamma_kind;
+        epi.gamma_dim = (int)dout;
+        epi.gamma = ex->gamma_inv;
+        if (!(flags & BTG_DEVICE_PTRS)) {
+            const size_t glen = ex->gamma_kind == BTG_GAMMA_PER_SENSOR ? dout : dout * op->nt;
+            BTG_TRY(stage_small(op, ex->gamma_inv, glen, op->gam, op->gcap, &epi.gamma));
+        }
+    }
+    if (ex && ex->alpha != 0.0) {
+        epi.alpha = ex->alpha;
+        epi.reg_kind = ex->reg_kind;
+        epi.v = ex->reg_v;
+        if (!(flags & BTG_DEVICE_PTRS)) {
+            BTG_TRY(stage_small(op, ex->reg_v, out_len, op->vcopy, op->vcap, &epi.v));
+        } else if (epi.v == out) {
+            BTG_TRY(grow(op->vcopy, op->vcap, out_len));
+            BTG_CUDA(cudaMemcpyAsync(op->vcopy, epi.v, out_len * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     op->stream));
+            epi.v = op->vcopy;
+        }
+    }
+    BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, epi));
     return finish_host(op, out, dout_p, out_len, flags);
 }
 
@@ -496,14 +535,28 @@ btg_status btg_forward(btg_op op, const double* m, size_t m_len, double* d, size
                        size_t nrhs, unsigned flags) {
     if (!op) return fail(BTG_EARG, "null operator handle");
     std::lock_guard<std::mutex> lock(op->mu);
-    return apply_dir(op, false, m, m_len, d, d_len, nrhs, flags);
+    return apply_dir(op, false, m, m_len, d, d_len, nrhs, nullptr, flags);
+}
+
+btg_status btg_forward_ex(btg_op op, const double* m, size_t m_len, double* d, size_t d_len,
+                          size_t nrhs, const btg_epilogue* epi, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return apply_dir(op, false, m, m_len, d, d_len, nrhs, epi, flags);
+}
+
+btg_status btg_adjoint_ex(btg_op op, const double* d, size_t d_len, double* m, size_t m_len,
+                          size_t nrhs, const btg_epilogue* epi, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return apply_dir(op, true, d, d_len, m, m_len, nrhs, epi, flags);
 }
 
 btg_status btg_adjoint(btg_op op, const double* d, size_t d_len, double* m, size_t m_len,
                        size_t nrhs, unsigned flags) {
     if (!op) return fail(BTG_EARG, "null operator handle");
     std::lock_guard<std::mutex> lock(op->mu);
-    return apply_dir(op, true, d, d_len, m, m_len, nrhs, flags);
+    return apply_dir(op, true, d, d_len, m, m_len, nrhs, nullptr, flags);
 }
 
 btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, size_t hv_len,
@@ -670,8 +723,14 @@ void btg_destroy(btg_op op) {
 
 btg_status btg_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo, double hi,
                             void* stream) {
-    if (!out && n) return fail(BTG_EARG, "null output pointer");
-    BTG_CUDA(btg::launch_fill_uniform(out, n, seed, offset, lo, hi, static_cast<cudaStream_t>(stream)));
+    return btg_fill_uniform_3d(out, 1, 1, n, seed, offset, 0, 0, lo, hi, stream);
+}
+
+btg_status btg_fill_uniform_3d(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
+                               uint64_t stride_a, uint64_t stride_b, double lo, double hi, void* stream) {
+    if (!out && na * nb * nc) return fail(BTG_EARG, "null output pointer");
+    BTG_CUDA(btg::launch_fill_uniform(out, na, nb, nc, seed, offset, stride_a, stride_b, lo, hi,
+                                      static_cast<cudaStream_t>(stream)));
     return BTG_OK;
 }
 

@@ -393,11 +393,15 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return z ^ (z >> 31);
 }
 
-__global__ void k_fill_uniform(double* __restrict__ out, size_t n, uint64_t seed, uint64_t offset,
-                               double lo, double span) {
+__global__ void k_fill_uniform(double* __restrict__ out, size_t nb, size_t nc, size_t n, uint64_t seed,
+                               uint64_t offset, uint64_t sa, uint64_t sb, double lo, double span) {
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
          k += (size_t)gridDim.x * blockDim.x) {
-        const uint64_t u = splitmix64(seed ^ (offset + k));
+        const size_t c = k % nc;
+        const size_t ab = k / nc;
+        const size_t b = ab % nb;
+        const size_t a = ab / nb;
+        const uint64_t u = splitmix64(seed ^ (offset + a * sa + b * sb + c));
         out[k] = lo + span * (static_cast<double>(u >> 11) * 0x1.0p-53);
     }
 }
@@ -514,12 +518,13 @@ template cudaError_t launch_gemv_adj<double2>(const double2*, const double2*, do
 template cudaError_t launch_gemv_adj<float2>(const float2*, const double2*, double2*, int, int,
                                              int, cudaStream_t);
 
-cudaError_t launch_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offset, double lo,
-                                double hi, cudaStream_t stream) {
+cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
+                                uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream) {
+    const size_t n = na * nb * nc;
     if (n == 0) return cudaSuccess;
     const size_t want = (n + kThreads - 1) / kThreads;
     const int grid = static_cast<int>(std::min<size_t>(want, (size_t)sm_count() * 16));
-    k_fill_uniform<<<grid, kThreads, 0, stream>>>(out, n, seed, offset, lo, hi - lo);
+    k_fill_uniform<<<grid, kThreads, 0, stream>>>(out, nb, nc, n, seed, offset, sa, sb, lo, hi - lo);
     return cudaGetLastError();
 }
 

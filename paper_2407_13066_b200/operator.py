@@ -75,13 +75,15 @@ class SpectralOperator:
         check(_lib.load().btg_export_spectrum(self._h, out.ctypes.data, int(full)))
         return out
 
-    def apply_forward(self, m):
-        """d = F m (block_operator.cpp:218-273)."""
-        return self._apply(m, adjoint=False)
+    def apply_forward(self, m, gamma_inv=None):
+        """d = F m (block_operator.cpp:218-273); with ``gamma_inv`` the output is
+        weighted by Gamma^-1 in the fused C2R epilogue (d = Gamma^-1 F m)."""
+        return self._apply(m, adjoint=False, gamma_inv=gamma_inv)
 
-    def apply_adjoint(self, d):
-        """m = F* d (block_operator.cpp:275-331)."""
-        return self._apply(d, adjoint=True)
+    def apply_adjoint(self, d, reg_v=None, alpha: float = 0.0, reg="identity"):
+        """m = F* d (block_operator.cpp:275-331); with ``reg_v`` and ``alpha`` the
+        fused epilogue adds alpha R reg_v (inverse.cpp:87-89)."""
+        return self._apply(d, adjoint=True, reg_v=reg_v, alpha=alpha, reg=reg)
 
     def hessian_apply(self, v, alpha: float = 0.0, reg="identity", gamma_inv=None):
         """F* Gamma^-1 F v + alpha R v (inverse.cpp:78-91 with Gamma^-1 = I)."""
@@ -209,26 +211,53 @@ class SpectralOperator:
             return _lib.BTG_GAMMA_PER_SAMPLE, ptr, g
         raise DimensionError(f"gamma_inv must be ({self.num_sensors},) or ({self.num_sensors}, {self.num_steps})")
 
-    def _apply(self, x, adjoint: bool):
+    def _apply(self, x, adjoint: bool, gamma_inv=None, reg_v=None, alpha: float = 0.0, reg="identity"):
         din = self.num_sensors if adjoint else self.num_sources
         dout = self.num_sources if adjoint else self.num_sensors
         what = "apply_adjoint" if adjoint else "apply_forward"
         nrhs, shape = self._check_vec(x, din, what)
         out_shape = (dout, self.num_steps) if len(shape) == 2 else (nrhs, dout, self.num_steps)
+        on_dev = _is_torch(x)
+        epi, keep = None, []
+        if gamma_inv is not None or (reg_v is not None and alpha != 0.0):
+            epi = _lib.Epilogue()
+            if gamma_inv is not None:
+                g = self._prep_torch(gamma_inv) if on_dev else np.ascontiguousarray(gamma_inv, dtype=np.float64)
+                if tuple(g.shape) == (dout,):
+                    epi.gamma_kind = _lib.BTG_GAMMA_PER_SENSOR
+                elif tuple(g.shape) == (dout, self.num_steps):
+                    epi.gamma_kind = _lib.BTG_GAMMA_PER_SAMPLE
+                else:
+                    raise DimensionError(f"{what}: gamma_inv must be ({dout},) or ({dout}, {self.num_steps})")
+                epi.gamma_inv = g.data_ptr() if on_dev else g.ctypes.data
+                keep.append(g)
+            if reg_v is not None and alpha != 0.0:
+                reg_kind = _REG.get(reg)
+                if reg_kind is None:
+                    raise _lib.Error(f"unknown regularization '{reg}'")
+                if tuple(reg_v.shape) != out_shape:
+                    raise DimensionError(f"{what}: reg_v must be {out_shape}")
+                rv = self._prep_torch(reg_v) if on_dev else np.ascontiguousarray(reg_v, dtype=np.float64)
+                epi.reg_v = rv.data_ptr() if on_dev else rv.ctypes.data
+                epi.alpha = float(alpha)
+                epi.reg_kind = reg_kind
+                keep.append(rv)
         L = _lib.load()
-        fn = L.btg_adjoint if adjoint else L.btg_forward
-        if _is_torch(x):
+        fn = L.btg_adjoint_ex if adjoint else L.btg_forward_ex
+        epi_p = ctypes.byref(epi) if epi is not None else None
+        if on_dev:
             import torch
 
             x = self._prep_torch(x)
             out = torch.empty(out_shape, dtype=torch.float64, device=x.device)
             self._bind_stream(x)
-            check(fn(self._h, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), nrhs, BTG_DEVICE_PTRS))
+            check(fn(self._h, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), nrhs, epi_p, BTG_DEVICE_PTRS))
             return out
         x = np.ascontiguousarray(x, dtype=np.float64)
         out = np.empty(out_shape, dtype=np.float64)
         self._bind_stream(None)
-        check(fn(self._h, x.ctypes.data, x.size, out.ctypes.data, out.size, nrhs, 0))
+        check(fn(self._h, x.ctypes.data, x.size, out.ctypes.data, out.size, nrhs, epi_p, 0))
+        del keep
         return out
 
 
@@ -270,12 +299,20 @@ def setup(blocks, keep_channel_layout: bool = False, precision: int = BTG_F64,
     return op
 
 
-def fill_uniform(tensor, seed: int, offset: int = 0, lo: float = -1.0, hi: float = 1.0) -> None:
-    """Fill a float64 CUDA tensor with the indexable SplitMix64 uniform stream
-    (btg_fill_uniform); host reproduction: ``oracle.restate`` is NOT needed —
-    see tests for the closed form."""
+def fill_uniform(tensor, seed: int, offset: int = 0, lo: float = -1.0, hi: float = 1.0,
+                 strides=None) -> None:
+    """Fill a float64 CUDA tensor from the indexable SplitMix64 uniform stream
+    (btg_fill_uniform / btg_fill_uniform_3d). With ``strides=(sa, sb)`` a 3-D
+    tensor (A, B, C) takes global index ``offset + a*sa + b*sb + c`` — a TOSI
+    slab of a larger operator. Host twin: ``splitmix_uniform`` in the tests."""
     import torch
 
     assert tensor.dtype == torch.float64 and tensor.is_cuda and tensor.is_contiguous()
-    check(_lib.load().btg_fill_uniform(tensor.data_ptr(), tensor.numel(), seed & (2**64 - 1), offset, lo, hi,
-                                       _torch_stream_ptr(tensor)))
+    L = _lib.load()
+    stream = _torch_stream_ptr(tensor)
+    if strides is None:
+        check(L.btg_fill_uniform(tensor.data_ptr(), tensor.numel(), seed & (2**64 - 1), offset, lo, hi, stream))
+    else:
+        a, b, c = tensor.shape
+        check(L.btg_fill_uniform_3d(tensor.data_ptr(), a, b, c, seed & (2**64 - 1), offset, strides[0], strides[1],
+                                    lo, hi, stream))

@@ -18,7 +18,7 @@ HEADER = ROOT / "include" / "btg.h"
 def declared_symbols():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(btg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(btg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
