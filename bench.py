@@ -42,6 +42,10 @@ CONFIGS = {
                label="profiling slice of configs[1]: N_t=1024 N_d=100 N_m=4096 (F-hat 6.7 GB >> L2)"),
     "C": dict(nt=1000, nd=600, nm=8192, nrhs=1,
               label="configs[2]: weak scaling N_t=1000 N_d=600 N_m=8192 per GPU FP64, 1xN grid"),
+    "D": dict(nt=1024, nd=128, nm=16384, nrhs=32,
+              label="configs[3]: multi-RHS batched Hessian, 32 RHS, N_t=1024 N_d=128 N_m=16384 FP64, ZGEMM on DMMA"),
+    "Dp": dict(nt=1024, nd=128, nm=4096, nrhs=32,
+               label="profiling slice of configs[3]: 32 RHS, N_t=1024 N_d=128 N_m=4096"),
 }
 CPU_SAMPLE_NM = 2048  # N_m slice the CPU reference runs on (extrapolate linearly in N_m)
 
@@ -58,6 +62,22 @@ def alg_bytes(nt, nd, nm, nrhs=1, elem=16):
     one = fhat + 8 * nt * (nm + nd) * nrhs
     hess = 2 * fhat + 16 * nm * nt * nrhs + 8 * nd
     return {"F": one, "F*": one, "H": hess, "gemv": fhat + 16 * nf * (nm + nd) * nrhs}
+
+
+def alg_flops(nt, nd, nm, nrhs=1):
+    """Fourier-space step FLOPs: 8 per complex MAC (counters.hpp:7-9 model) x NF x N_d x N_m x nrhs."""
+    one = 8.0 * (nt + 1) * nd * nm * nrhs
+    return {"F": one, "F*": one, "H": 2 * one, "gemv": one}
+
+
+def run_probe():
+    """Measured FP64 tensor / FMA peaks and read-only HBM bandwidth (csrc/btg_probe.cu)."""
+    exe = ROOT / "paper_2407_13066_b200" / "btg_probe"
+    try:
+        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120).stdout.strip().splitlines()
+        return json.loads(out[-1])
+    except Exception as exc:
+        return {"error": str(exc)}
 
 
 def hbm_peak():
@@ -236,7 +256,11 @@ def run_ours(args):
     if args.config:
         cfg = dict(CONFIGS[args.config])
     nt, nd, nm = cfg["nt"], cfg["nd"], cfg["nm"]
+    nrhs = cfg.get("nrhs", 1)
     peak, peak_src = hbm_peak()
+    probe = run_probe() if rank == 0 and world == 1 else None
+    if probe:
+        log(f"[bench] probe: {probe}")
 
     t0 = time.perf_counter()
     if world == 1:
@@ -254,7 +278,8 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(device)
     dev = f"cuda:{device}"
-    m = torch.empty((nm * (1 if engine is None else 1), nt), dtype=torch.float64, device=dev)
+    vshape = (nm, nt) if nrhs == 1 else (nrhs, nm, nt)
+    m = torch.empty(vshape, dtype=torch.float64, device=dev)
     btg.fill_uniform(m, seed=7)
     gamma = torch.empty((nd,), dtype=torch.float64, device=dev)
     btg.fill_uniform(gamma, seed=8, lo=0.5, hi=2.0)
@@ -324,11 +349,13 @@ def run_ours(args):
     else:
         per_mean = {k: statistics.mean(v) for k, v in per.items()}
     ms_step = total_ms / args.steps
-    b = alg_bytes(nt, nd, nm)
+    b = alg_bytes(nt, nd, nm, nrhs)
+    fl = alg_flops(nt, nd, nm, nrhs)
     step_bytes = (b["F"] + b["F*"] + b["H"]) * world
     value = step_bytes / (ms_step * 1e-3) / 1e12
     ops = {k: {"ms": per_mean[k], "TB/s": b[k] / (per_mean[k] * 1e-3) / 1e12,
-               "frac_of_peak": b[k] / (per_mean[k] * 1e-3) / 1e9 / peak} for k in ("F", "F*", "H")}
+               "frac_of_peak": b[k] / (per_mean[k] * 1e-3) / 1e9 / peak,
+               "TFLOP/s": fl[k] / (per_mean[k] * 1e-3) / 1e12} for k in ("F", "F*", "H")}
 
     # Per-kernel durations: CUDA-event stage timers inside the library (same
     # stream), F then F* separately so forward / adjoint GEMV are distinct.
@@ -344,44 +371,56 @@ def run_ours(args):
             kernels[name] = {st: c[st]["seconds"] / reps * 1e3 for st in ("forward_fft", "apply", "inverse_fft")}
         op.set_timing(False)
     gemv_bytes = b["gemv"]
+    roof = None
     if kernels:
         dom = max(("fwd", "adj"), key=lambda k: kernels[k]["apply"])
         dur = kernels[dom]["apply"]
-        roof = {"bound": "hbm", "kernel": f"k_gemv_{dom}", "achieved": gemv_bytes / (dur * 1e-3) / 1e9,
-                "peak": peak, "unit": "GB/s", "frac": gemv_bytes / (dur * 1e-3) / 1e9 / peak,
-                "traffic": None, "peak_source": peak_src,
-                "bytes_per_launch": gemv_bytes, "ms_per_launch": dur,
-                "per_unit": "16 B per F-hat complex + 16 B per vector complex, x (N_t+1) x (N_d N_m + N_d + N_m)",
-                "stage_ms": kernels}
+        if nrhs == 1:
+            kname = f"k_gemv_{dom}"
+            roof = {"bound": "hbm", "kernel": kname, "achieved": gemv_bytes / (dur * 1e-3) / 1e9,
+                    "peak": peak, "unit": "GB/s", "frac": gemv_bytes / (dur * 1e-3) / 1e9 / peak,
+                    "traffic": None, "peak_source": peak_src,
+                    "per_unit": "16 B per F-hat complex + 16 B per vector complex, "
+                                "x (N_t+1) x (N_d N_m + N_d + N_m)"}
+        else:
+            kname = f"k_zgemm_{dom}"
+            tpeak = (probe or {}).get("dmma_f64_tflops") or None
+            ach = fl["gemv"] / (dur * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": kname, "achieved": ach, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": (ach / tpeak) if tpeak else None, "traffic": None,
+                    "peak_source": "measured mma.sync.m16n8k4.f64 peak (csrc/btg_probe.cu, this run)",
+                    "hbm_achieved_gbs": gemv_bytes / (dur * 1e-3) / 1e9,
+                    "per_unit": "8 FLOP per complex MAC x (N_t+1) x N_d x N_m x nrhs"}
+        roof.update({"bytes_per_launch": gemv_bytes, "flops_per_launch": fl["gemv"], "ms_per_launch": dur,
+                     "stage_ms": kernels, "probe": probe})
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
             try:
-                roof["traffic"] = json.loads(tf.read_text()).get(f"k_gemv_{dom}")
+                roof["traffic"] = json.loads(tf.read_text()).get(f"{args.config or 'B'}:{kname}")
             except Exception:
                 pass
-    else:
-        roof = None
 
     # End to end through the public API with host buffers (pinned), N=1 only.
     e2e = None
     if engine is None:
-        hm = torch.empty((nm, nt), dtype=torch.float64, pin_memory=True)
+        dshape = tuple(d.shape)
+        hm = torch.empty(vshape, dtype=torch.float64, pin_memory=True)
         hm.copy_(m.cpu())
-        hd = torch.empty((nd, nt), dtype=torch.float64, pin_memory=True)
+        hd = torch.empty(dshape, dtype=torch.float64, pin_memory=True)
         hd.copy_(d.cpu())
         hg = gamma.cpu().numpy()
         hm_np, hd_np = hm.numpy(), hd.numpy()
-        out_d = torch.empty((nd, nt), dtype=torch.float64, pin_memory=True).numpy()
-        out_m = torch.empty((nm, nt), dtype=torch.float64, pin_memory=True).numpy()
-        out_h = torch.empty((nm, nt), dtype=torch.float64, pin_memory=True).numpy()
+        out_d = torch.empty(dshape, dtype=torch.float64, pin_memory=True).numpy()
+        out_m = torch.empty(vshape, dtype=torch.float64, pin_memory=True).numpy()
+        out_h = torch.empty(vshape, dtype=torch.float64, pin_memory=True).numpy()
         from paper_2407_13066_b200 import _lib
 
         L = _lib.load()
 
         def e2e_step():
-            _lib.check(L.btg_forward(op._h, hm_np.ctypes.data, hm_np.size, out_d.ctypes.data, out_d.size, 1, 0))
-            _lib.check(L.btg_adjoint(op._h, hd_np.ctypes.data, hd_np.size, out_m.ctypes.data, out_m.size, 1, 0))
-            _lib.check(L.btg_hessian(op._h, hm_np.ctypes.data, hm_np.size, out_h.ctypes.data, out_h.size, 1,
+            _lib.check(L.btg_forward(op._h, hm_np.ctypes.data, hm_np.size, out_d.ctypes.data, out_d.size, nrhs, 0))
+            _lib.check(L.btg_adjoint(op._h, hd_np.ctypes.data, hd_np.size, out_m.ctypes.data, out_m.size, nrhs, 0))
+            _lib.check(L.btg_hessian(op._h, hm_np.ctypes.data, hm_np.size, out_h.ctypes.data, out_h.size, nrhs,
                                      hg.ctypes.data, 1, 0.0, 0, 0))
 
         op._bind_stream(None)
@@ -394,15 +433,15 @@ def run_ours(args):
         torch.cuda.synchronize(device)
         e_s = (time.perf_counter() - t) / e_steps
         e2e = {"value": (b["F"] + b["F*"] + b["H"]) / e_s / 1e12, "unit": "TB/s",
-               "h2d_bytes_per_step": 8 * (2 * nm * nt + nd * nt + nd),
-               "d2h_bytes_per_step": 8 * (nd * nt + 2 * nm * nt),
+               "h2d_bytes_per_step": 8 * nrhs * (2 * nm * nt + nd * nt) + 8 * nd,
+               "d2h_bytes_per_step": 8 * nrhs * (nd * nt + 2 * nm * nt),
                "ms_per_step": e_s * 1e3, "steps": e_steps,
                "path": "btg_forward/btg_adjoint/btg_hessian with pinned host buffers (H2D + compute + D2H per call)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and nrhs == 1:
         try:
-            c = cpu_line(nt, nd, nm, steps=2, warmup=1)
+            c = cpu_line(nt, nd, nm, steps=2, warmup=1) if nrhs == 1 else None
             cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as exc:  # the CPU leg must not kill the GPU line
             cpu = {"value": None, "unit": "TB/s", "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
@@ -414,7 +453,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: device SplitMix64 uniform(-1,1) first block column (seed 1000, global index), m (seed 7), "
                     "Gamma^-1 uniform(0.5,2) per sensor (seed 8)",
-            "config": {"workload": cfg["label"], "N_t": nt, "N_d": nd, "N_m": nm, "nrhs": 1, "grid": grid,
+            "config": {"workload": cfg["label"], "N_t": nt, "N_d": nd, "N_m": nm, "nrhs": nrhs, "grid": grid,
                        "step": "F m + F* d + F* Gamma^-1 F v (alpha=0), FP64, F-hat N_t+1 frequencies",
                        "fhat_gb_per_gpu": 16 * (nt + 1) * nd * nm / 1e9,
                        "l2": "inputs larger than L2: every matvec streams the full F-hat (>> 126 MB L2)",

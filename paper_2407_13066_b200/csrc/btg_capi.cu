@@ -92,6 +92,7 @@ struct btg_op_s {
     double2* d_fast = nullptr;  // split twiddle tables of the compile-time-N FFTs
     btg::FastTables fast{};
     bool fast_ok = false;
+    bool no_dmma = false;  // BTG_DISABLE_DMMA: per-RHS GEMV streams instead of the ZGEMM
     int fft_batch = 1;        // channels per CTA for vector transforms
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
 
@@ -259,29 +260,45 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
     StageClock clk(op, &op->counters.apply);
     const size_t nin = adjoint ? op->nd : op->nm;
     const size_t nout = adjoint ? op->nm : op->nd;
-    if (nrhs != 1) return fail(BTG_EARG, "internal: run_apply expects nrhs == 1");
+    const int nf = (int)op->nf, nd = (int)op->nd, nm = (int)op->nm;
     cudaError_t e;
-    if (op->precision == BTG_F64) {
+    if (nrhs > 1) {
+        // ZGEMM on the FP64 tensor cores (btg_zgemm.cu); FP64 F-hat only.
+        if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
         const double2* F = static_cast<const double2*>(op->F);
-        e = adjoint ? btg::launch_gemv_adj(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream)
-                    : btg::launch_gemv_fwd(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream);
+        e = adjoint ? btg::launch_zgemm_adj(F, in, out, nf, nd, nm, (int)nrhs, op->stream)
+                    : btg::launch_zgemm_fwd(F, in, out, nf, nd, nm, (int)nrhs, op->stream);
+    } else if (op->precision == BTG_F64) {
+        const double2* F = static_cast<const double2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj(F, in, out, nf, nd, nm, op->stream)
+                    : btg::launch_gemv_fwd(F, in, out, nf, nd, nm, op->stream);
     } else {
         const float2* F = static_cast<const float2*>(op->F);
-        e = adjoint ? btg::launch_gemv_adj(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream)
-                    : btg::launch_gemv_fwd(F, in, out, (int)op->nf, (int)op->nd, (int)op->nm, op->stream);
+        e = adjoint ? btg::launch_gemv_adj(F, in, out, nf, nd, nm, op->stream)
+                    : btg::launch_gemv_fwd(F, in, out, nf, nd, nm, op->stream);
     }
     BTG_CUDA(e);
     op->counters.launches++;
-    op->counters.apply.ops += 8.0 * op->nd * op->nm * op->nf;
-    op->counters.apply.bytes += (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (nin + nout);
+    op->counters.apply.ops += 8.0 * op->nd * op->nm * op->nf * nrhs;
+    op->counters.apply.bytes +=
+        (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (nin + nout) * nrhs;
     return BTG_OK;
 }
 
 // One direction (forward or adjoint) for nrhs right-hand sides, device pointers.
+// FP64: all right-hand sides go through one R2C, one ZGEMM (DMMA) and one C2R;
+// FP32 F-hat: one GEMV stream per right-hand side.
 btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size_t nrhs,
                     const btg::C2REpilogue& epi) {
     const size_t cin = adjoint ? op->nd : op->nm;
     const size_t cout = adjoint ? op->nm : op->nd;
+    if (nrhs > 1 && op->precision == BTG_F64 && !op->no_dmma) {
+        BTG_TRY(ensure_spectral(op, nrhs));
+        BTG_TRY(run_r2c_vec(op, in, nrhs * cin, op->wa));
+        BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, nrhs));
+        BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi));
+        return BTG_OK;
+    }
     BTG_TRY(ensure_spectral(op, 1));
     for (size_t r = 0; r < nrhs; ++r) {
         BTG_TRY(run_r2c_vec(op, in + r * cin * op->nt, cin, op->wa));
@@ -449,6 +466,7 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
         op->fast.post_hi = op->d_fast + 64 + hi;
         op->fast_ok = true;
     }
+    op->no_dmma = std::getenv("BTG_DISABLE_DMMA") != nullptr;
     op->plan.n = (int)nt;
     op->plan.nfac = (int)fac.size();
     for (size_t i = 0; i < fac.size(); ++i) op->plan.fac[i] = fac[i];

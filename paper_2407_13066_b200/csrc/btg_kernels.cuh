@@ -73,6 +73,13 @@ template <typename TF>
 cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
                             cudaStream_t stream);
 
+// Multi-RHS Fourier-space step on FP64 tensor cores (btg_zgemm.cu). X/Y are
+// [f][r][dim] (dim = N_m or N_d), FP64 F-hat only.
+cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
+                             cudaStream_t stream);
+cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
+                             cudaStream_t stream);
+
 // out[(a*nb + b)*nc + c] = uniform(seed ^ (offset + a*sa + b*sb + c))
 cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                 uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream);

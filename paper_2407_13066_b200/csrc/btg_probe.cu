@@ -1,0 +1,105 @@
+// btg_probe — measured denominators for the rooflines bench.py reports:
+//   dmma   FP64 tensor-core peak: mma.sync.m16n8k4.f64 (the instruction the
+//          multi-RHS ZGEMM issues), 8 independent accumulators per warp
+//   dfma   FP64 FMA-pipe peak
+//   read   HBM read-only stream (16-byte non-coherent loads, 8 GiB buffer)
+// Prints one JSON object. Timed with CUDA events after a warm-up launch.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+__global__ void k_dmma_peak(double* out, int iters) {
+    double c[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j] = 0.0;
+    double a0 = threadIdx.x * 1e-9, a1 = 1.0 + a0, b0 = 0.5 - a0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile(
+                "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                : "d"(a0), "d"(a1), "d"(b0));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+    if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_dfma_peak(double* out, int iters) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-9 + i;
+    const double a = 0.999999, b = 1e-7;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_read(const double2* __restrict__ in, size_t n, double* out) {
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double2 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(in + i));
+        acc += v.x + v.y;
+    }
+    if (acc == 12345.678) out[0] = acc;
+}
+
+template <typename F>
+static float time_ms(F launch) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch();
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        launch();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return best;
+}
+
+int main() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out;
+    cudaMalloc(&out, 64);
+    const int iters = 4096;
+    const int blocks = sms * 4, threads = 256;
+    const float ms_mma = time_ms([&] { k_dmma_peak<<<blocks, threads>>>(out, iters); });
+    const double mma_flops = 2.0 * 16 * 8 * 4 * 8.0 * iters * (blocks * threads / 32.0);
+    const float ms_fma = time_ms([&] { k_dfma_peak<<<blocks, threads>>>(out, iters * 8); });
+    const double fma_flops = 2.0 * 8.0 * iters * 8.0 * blocks * threads;
+    const size_t bytes = 8ull << 30;
+    double2* buf = nullptr;
+    float ms_rd = 0.f;
+    if (cudaMalloc(&buf, bytes) == cudaSuccess) {
+        cudaMemset(buf, 0, bytes);
+        ms_rd = time_ms([&] { k_read<<<sms * 8, 512>>>(buf, bytes / 16, out); });
+        cudaFree(buf);
+    }
+    const cudaError_t e = cudaDeviceSynchronize();
+    std::printf("{\"dmma_f64_tflops\": %.3f, \"dfma_f64_tflops\": %.3f, \"hbm_read_gbs\": %.1f, \"sms\": %d, "
+                "\"status\": \"%s\"}\n",
+                mma_flops / (ms_mma * 1e-3) / 1e12, fma_flops / (ms_fma * 1e-3) / 1e12,
+                ms_rd > 0 ? bytes / (ms_rd * 1e-3) / 1e9 : 0.0, sms, cudaGetErrorString(e));
+    return e == cudaSuccess ? 0 : 1;
+}

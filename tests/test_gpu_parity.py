@@ -223,6 +223,32 @@ def test_multiple_right_hand_sides(btg):
         assert R.rel_l2(H[r], R.hessian_apply(spec, M[r], 0.2, 1)) <= TOL64
 
 
+@pytest.mark.parametrize("dims", [(130, 300, 40, 33), (5, 77, 16, 2), (128, 256, 64, 32)])
+def test_multi_rhs_dmma_zgemm(btg, dims, monkeypatch):
+    """configs[3] shape class (ZGEMM on FP64 tensor cores): ragged N_d > 128
+    (two row tiles), N_m not a multiple of the K chunk, nrhs > 32 (two RHS
+    tiles); against the oracle and against the per-RHS GEMV path."""
+    nd, nm, nt, nrhs = dims
+    blocks, _, _ = R.random_problem(500 + nd, nd, nm, nt)
+    spec = R.setup_full(blocks)
+    rng = R.Mt19937_64(600 + nd)
+    M = rng.uniform(nrhs * nm * nt, -1, 1).reshape(nrhs, nm, nt)
+    Dv = rng.uniform(nrhs * nd * nt, -1, 1).reshape(nrhs, nd, nt)
+    gam = np.linspace(0.5, 2.0, nd)
+    with btg.setup(blocks) as op:
+        F = op.apply_forward(M)
+        A = op.apply_adjoint(Dv)
+        H = op.hessian_apply(M, alpha=0.3, reg="temporal-laplacian", gamma_inv=gam)
+    for r in range(nrhs):
+        assert R.rel_l2(F[r], R.apply_forward(spec, M[r])) <= TOL64
+        assert R.rel_l2(A[r], R.apply_adjoint(spec, Dv[r])) <= TOL64
+        assert R.rel_l2(H[r], R.gauss_newton_apply(spec, M[r], gam, 0.3, 1)) <= TOL64
+    monkeypatch.setenv("BTG_DISABLE_DMMA", "1")
+    with btg.setup(blocks) as op:
+        F2 = op.apply_forward(M)
+    assert R.rel_l2(F, F2) <= 1e-14
+
+
 @pytest.mark.parametrize("nt", [1, 2, 7, 64, 97, 125, 128, 256, 500, 512, 1000, 1001, 1024, 2000, 2048, 4096])
 def test_fft_lengths(btg, nt):
     """Radix 2/4/8, 5 (N_t=1000 -> 2N_t=2000, configs[2]), 3, 7 and generic primes."""
