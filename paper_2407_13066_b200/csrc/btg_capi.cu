@@ -92,7 +92,8 @@ struct btg_op_s {
     double2* d_fast = nullptr;  // split twiddle tables of the compile-time-N FFTs
     btg::FastTables fast{};
     bool fast_ok = false;
-    bool no_dmma = false;  // BTG_DISABLE_DMMA: per-RHS GEMV streams instead of the ZGEMM
+    bool no_dmma = false;      // BTG_DISABLE_DMMA: per-RHS GEMV streams instead of the ZGEMM
+    bool legacy_gemv = true;   // register-load GEMV; BTG_GEMV_TMA=1 selects the TMA ring
     int fft_batch = 1;        // channels per CTA for vector transforms
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
 
@@ -268,6 +269,11 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
         const double2* F = static_cast<const double2*>(op->F);
         e = adjoint ? btg::launch_zgemm_adj(F, in, out, nf, nd, nm, (int)nrhs, op->stream)
                     : btg::launch_zgemm_fwd(F, in, out, nf, nd, nm, (int)nrhs, op->stream);
+    } else if (op->precision == BTG_F64 && !op->legacy_gemv) {
+        // persistent TMA-staged stream (btg_gemv_tma.cu)
+        const double2* F = static_cast<const double2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj_tma(F, in, out, nf, nd, nm, op->stream)
+                    : btg::launch_gemv_fwd_tma(F, in, out, nf, nd, nm, op->stream);
     } else if (op->precision == BTG_F64) {
         const double2* F = static_cast<const double2*>(op->F);
         e = adjoint ? btg::launch_gemv_adj(F, in, out, nf, nd, nm, op->stream)
@@ -467,6 +473,9 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
         op->fast_ok = true;
     }
     op->no_dmma = std::getenv("BTG_DISABLE_DMMA") != nullptr;
+    // Default: the register-load GEMV (7.4 TB/s at configs[1]); the TMA ring is
+    // opt-in (BTG_GEMV_TMA=1): faster on a 6.7 GB operator, slower at 54 GB.
+    op->legacy_gemv = std::getenv("BTG_GEMV_TMA") == nullptr;
     op->plan.n = (int)nt;
     op->plan.nfac = (int)fac.size();
     for (size_t i = 0; i < fac.size(); ++i) op->plan.fac[i] = fac[i];

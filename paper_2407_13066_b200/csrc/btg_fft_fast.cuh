@@ -47,6 +47,10 @@ template <> struct FastPlan<2000> { static constexpr int TPC = 128, CPB = 2;  us
 template <> struct FastPlan<2048> { static constexpr int TPC = 128, CPB = 2;  using R = Radices<16, 16, 8>; };
 template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  using R = Radices<16, 16, 16>; };
 
+// Register budget: aim for 768 resident threads per SM (<= 85 registers).
+template <int N, int CPB>
+constexpr int kMinBlocks = (768 / (FastPlan<N>::TPC * CPB)) > 0 ? (768 / (FastPlan<N>::TPC * CPB)) : 1;
+
 __host__ __device__ constexpr int pad_idx(int p) { return p + (p >> 4); }
 __host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }  // room for X_N in c2r
 constexpr int kTwLo = 32;
@@ -54,9 +58,9 @@ constexpr int kTwLo = 32;
 template <int N>
 __host__ __device__ constexpr int tw_hi_count() { return (N + kTwLo - 1) / kTwLo + 1; }
 
-template <int N>
+template <int N, int CPB>
 __host__ __device__ constexpr size_t smem_bytes() {
-    return sizeof(double2) * ((size_t)FastPlan<N>::CPB * chan_stride(N) + 2 * kTwLo + 2 * tw_hi_count<N>() + 2);
+    return sizeof(double2) * ((size_t)CPB * chan_stride(N) + 2 * kTwLo + 2 * tw_hi_count<N>() + 2);
 }
 
 // W^e for W = exp(SIGN * 2 pi i / n_tw) from the split table (lo[e % 32] * hi[e / 32]).
@@ -117,10 +121,17 @@ __device__ __forceinline__ void dft(double2* v) {
 template <int N, int R, int NS, int SIGN>
 __device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2* lo, const double2* hi) {
     if constexpr (NS > 1) {
+        // One table lookup per butterfly; the powers W^{k q step}, q = 2..R-1, are
+        // products of lower powers (depth log2 R, error a few ulp) instead of
+        // 2 (R-1) shared-memory loads.
         const int k = j % NS;
         constexpr int step = N / (NS * R);
+        double2 w[R];
+        w[1] = tw_lookup<SIGN>(lo, hi, k * step);
 #pragma unroll
-        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], tw_lookup<SIGN>(lo, hi, k * q * step));
+        for (int q = 2; q < R; ++q) w[q] = cmul(w[q / 2], w[q - q / 2]);
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
     }
 }
 
@@ -208,12 +219,12 @@ __device__ __forceinline__ void load_tables(double2* lo, double2* hi, int hi_cou
 // ---------------------------------------------------------------------------
 // r2c: SOTI rows (time contiguous) -> frequency-major out[k*out_fs + c]
 // ---------------------------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
+template <int N, int CPB>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
     k_r2c_fast(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
                int channels, FastTables tabs) {
     using P = FastPlan<N>;
-    constexpr int TPC = P::TPC, CPB = P::CPB, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
@@ -240,10 +251,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
         for (int bf = 0; bf < BF; ++bf) {
             const int j = tc + bf * TPC;
             if (NB % TPC == 0 || j < NB) {
+                // n = j + q NB < N/2 iff q < R/2: the zero-padded half is never loaded
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     const int n = j + q * NB;
-                    v[bf][q] = (live && n < N / 2) ? __ldg(row + n) : make_double2(0.0, 0.0);
+                    v[bf][q] = (q < R / 2 && live) ? __ldg(row + n) : make_double2(0.0, 0.0);
                 }
                 dft<R, -1>(v[bf]);
             }
@@ -270,10 +282,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
         const double2* z = sm + bb * CS;
         const double2 zk = z[pad_idx(k == 0 ? 0 : k)];
         const double2 zn = z[pad_idx(k == 0 ? 0 : N - k)];
-        // X_k
+        // X_k  (one table lookup per pair: W_{2N}^{N-k} = -conj(W_{2N}^k))
+        const double2 w = tw_lookup<-1>(plo, phi, k);
         {
             const double2 a = cadd(zk, cconj(zn));
-            const double2 w = tw_lookup<-1>(plo, phi, k);
             const double2 wb = cmul(w, csub(zk, cconj(zn)));
             out[(long long)k * out_fs + cc] = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
         }
@@ -281,8 +293,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
         if (k < N / 2) {
             const int kk = N - k;
             const double2 a = cadd(zn, cconj(zk));
-            const double2 w = tw_lookup<-1>(plo, phi, kk);
-            const double2 wb = cmul(w, csub(zn, cconj(zk)));
+            const double2 wn = make_double2(-w.x, w.y);
+            const double2 wb = cmul(wn, csub(zn, cconj(zk)));
             out[(long long)kk * out_fs + cc] = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
         }
     }
@@ -291,12 +303,12 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
 // ---------------------------------------------------------------------------
 // c2r: frequency-major in[k*in_fs + c] -> SOTI rows out[c*out_cs + t], t < N
 // ---------------------------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
+template <int N, int CPB>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
     k_c2r_fast(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
     using P = FastPlan<N>;
-    constexpr int TPC = P::TPC, CPB = P::CPB, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
@@ -320,15 +332,16 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * FastPlan<N>::CPB)
             xk = __ldg(in + (long long)k * in_fs + cc);
             xn = __ldg(in + (long long)(N - k) * in_fs + cc);
         }
+        const double2 w = tw_lookup<-1>(plo, phi, k);  // W_{2N}^{N-k} = -conj(W_{2N}^k)
         {
             const double2 e = cadd(xk, cconj(xn));
-            const double2 o = cmul(csub(xk, cconj(xn)), cconj(tw_lookup<-1>(plo, phi, k)));
+            const double2 o = cmul(csub(xk, cconj(xn)), cconj(w));
             z[pad_idx(k == 0 ? 0 : k)] = make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
         }
         if (k > 0 && k < N / 2) {
             const int kk = N - k;
             const double2 e = cadd(xn, cconj(xk));
-            const double2 o = cmul(csub(xn, cconj(xk)), cconj(tw_lookup<-1>(plo, phi, kk)));
+            const double2 o = cmul(csub(xn, cconj(xk)), make_double2(-w.x, -w.y));
             z[pad_idx(kk)] = make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
         }
     }

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "btg_fft.cuh"
 #include "btg_kernels.cuh"
@@ -489,7 +490,10 @@ cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, in
     constexpr int kUnr = 8;
     dim3 grid((nm + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nf);
     const size_t smem = (size_t)nd * sizeof(double2);
-    if (smem <= 96 * 1024) {
+    // Default: read d-hat_f through the read-only path (a warp-uniform broadcast
+    // that hits L1), so a CTA starts streaming F-hat without a fill + barrier.
+    static const bool use_smem = std::getenv("BTG_ADJ_SMEM") != nullptr;
+    if (use_smem && smem <= 96 * 1024) {
         auto kern = k_gemv_adj<TF, VEC, kJpt, kUnr, true>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
@@ -538,30 +542,71 @@ cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, ui
 namespace btg {
 namespace {
 
+// Channels per CTA: the plan's default, overridable with BTG_FFT_CPB (tuning).
+int fft_cpb(int dflt) {
+    static const int env = [] {
+        const char* v = std::getenv("BTG_FFT_CPB");
+        return v ? std::atoi(v) : 0;
+    }();
+    return env > 0 ? env : dflt;
+}
+
+template <int N, int CPB>
+cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
+                        const FastTables& tabs, cudaStream_t stream) {
+    using P = fast::FastPlan<N>;
+    if constexpr (P::TPC * CPB > 1024 || fast::smem_bytes<N, CPB>() > 227 * 1024) {
+        return cudaErrorNotSupported;
+    } else {
+        constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        auto kern = fast::k_r2c_fast<N, CPB>;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        const int grid = (channels + CPB - 1) / CPB;
+        kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs);
+        return cudaGetLastError();
+    }
+}
+
+template <int N, int CPB>
+cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
+                        const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
+    using P = fast::FastPlan<N>;
+    if constexpr (P::TPC * CPB > 1024 || fast::smem_bytes<N, CPB>() > 227 * 1024) {
+        return cudaErrorNotSupported;
+    } else {
+        constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        auto kern = fast::k_c2r_fast<N, CPB>;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        const int grid = (channels + CPB - 1) / CPB;
+        kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
+        return cudaGetLastError();
+    }
+}
+
 template <int N>
 cudaError_t r2c_fast_n(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
                        const FastTables& tabs, cudaStream_t stream) {
-    using P = fast::FastPlan<N>;
-    constexpr size_t smem = fast::smem_bytes<N>();
-    auto kern = fast::k_r2c_fast<N>;
-    cudaError_t e = set_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-    const int grid = (channels + P::CPB - 1) / P::CPB;
-    kern<<<grid, P::TPC * P::CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs);
-    return cudaGetLastError();
+    switch (fft_cpb(fast::FastPlan<N>::CPB)) {
+        case 1: return r2c_fast_nc<N, 1>(in, in_cs, out, out_fs, channels, tabs, stream);
+        case 2: return r2c_fast_nc<N, 2>(in, in_cs, out, out_fs, channels, tabs, stream);
+        case 4: return r2c_fast_nc<N, 4>(in, in_cs, out, out_fs, channels, tabs, stream);
+        case 8: return r2c_fast_nc<N, 8>(in, in_cs, out, out_fs, channels, tabs, stream);
+        default: return r2c_fast_nc<N, fast::FastPlan<N>::CPB>(in, in_cs, out, out_fs, channels, tabs, stream);
+    }
 }
 
 template <int N>
 cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
                        const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
-    using P = fast::FastPlan<N>;
-    constexpr size_t smem = fast::smem_bytes<N>();
-    auto kern = fast::k_c2r_fast<N>;
-    cudaError_t e = set_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-    const int grid = (channels + P::CPB - 1) / P::CPB;
-    kern<<<grid, P::TPC * P::CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
-    return cudaGetLastError();
+    switch (fft_cpb(fast::FastPlan<N>::CPB)) {
+        case 1: return c2r_fast_nc<N, 1>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        case 2: return c2r_fast_nc<N, 2>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        case 4: return c2r_fast_nc<N, 4>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        case 8: return c2r_fast_nc<N, 8>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        default: return c2r_fast_nc<N, fast::FastPlan<N>::CPB>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+    }
 }
 
 #define BTG_FAST_SIZES(X) X(64) X(128) X(256) X(500) X(512) X(1000) X(1024) X(2000) X(2048) X(4096)

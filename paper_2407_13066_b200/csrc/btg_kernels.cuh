@@ -73,6 +73,12 @@ template <typename TF>
 cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
                             cudaStream_t stream);
 
+// TMA-staged persistent single-RHS Fourier-space step, FP64 F-hat (btg_gemv_tma.cu).
+cudaError_t launch_gemv_fwd_tma(const double2* F, const double2* x, double2* y, int nf, int nd, int nm,
+                                cudaStream_t stream);
+cudaError_t launch_gemv_adj_tma(const double2* F, const double2* x, double2* y, int nf, int nd, int nm,
+                                cudaStream_t stream);
+
 // Multi-RHS Fourier-space step on FP64 tensor cores (btg_zgemm.cu). X/Y are
 // [f][r][dim] (dim = N_m or N_d), FP64 F-hat only.
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,

@@ -44,13 +44,59 @@ __global__ void k_dfma_peak(double* out, int iters) {
     if (s == 12345.678) out[0] = s;
 }
 
+// Even warps issue DMMA, odd warps DFMA: do the two FP64 pipes add up?
+__global__ void k_mixed_peak(double* out, int iters) {
+    if ((threadIdx.x >> 5) & 1) {
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-9 + i;
+        const double a = 0.999999, b = 1e-7;
+        for (int it = 0; it < iters * 8; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += x[i];
+        if (s == 12345.678) out[0] = s;
+    } else {
+        double c[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[i][j] = 0.0;
+        double a0 = threadIdx.x * 1e-9, a1 = 1.0 + a0, b0 = 0.5 - a0;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile(
+                    "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                    : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                    : "d"(a0), "d"(a1), "d"(b0));
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+        if (s == 12345.678) out[0] = s;
+    }
+}
+
+// Read-only stream, UNR independent 16-byte loads in flight per thread.
+template <int UNR>
 __global__ void k_read(const double2* __restrict__ in, size_t n, double* out) {
     double acc = 0.0;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        double2 v;
-        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(in + i));
-        acc += v.x + v.y;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    for (; i + (UNR - 1) * stride < n; i += UNR * stride) {
+        double2 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                         : "=d"(v[u].x), "=d"(v[u].y)
+                         : "l"(in + i + u * stride));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc += v[u].x + v[u].y;
     }
+    for (; i < n; i += stride) acc += in[i].x;
     if (acc == 12345.678) out[0] = acc;
 }
 
@@ -88,12 +134,24 @@ int main() {
     const double mma_flops = 2.0 * 16 * 8 * 4 * 8.0 * iters * (blocks * threads / 32.0);
     const float ms_fma = time_ms([&] { k_dfma_peak<<<blocks, threads>>>(out, iters * 8); });
     const double fma_flops = 2.0 * 8.0 * iters * 8.0 * blocks * threads;
+    // mixed: half the warps at the DMMA rate per iteration (8 MMAs = 8*1024 flops
+    // per warp-iteration), half at the DFMA rate (64 DFMA = 2*64*32 flops per warp-iteration)
+    const float ms_mix = time_ms([&] { k_mixed_peak<<<blocks, threads>>>(out, iters); });
+    const double mix_flops = 0.5 * mma_flops + 0.5 * fma_flops;
+    std::fprintf(stderr, "mixed DMMA+DFMA: %.3f TFLOP/s (%.3f ms)\n", mix_flops / (ms_mix * 1e-3) / 1e12, ms_mix);
     const size_t bytes = 8ull << 30;
     double2* buf = nullptr;
     float ms_rd = 0.f;
     if (cudaMalloc(&buf, bytes) == cudaSuccess) {
         cudaMemset(buf, 0, bytes);
-        ms_rd = time_ms([&] { k_read<<<sms * 8, 512>>>(buf, bytes / 16, out); });
+        // best over a few (grid, in-flight) shapes: the practical read ceiling
+        const float a = time_ms([&] { k_read<4><<<sms * 4, 512>>>(buf, bytes / 16, out); });
+        const float b = time_ms([&] { k_read<8><<<sms * 2, 512>>>(buf, bytes / 16, out); });
+        const float c = time_ms([&] { k_read<8><<<sms * 4, 256>>>(buf, bytes / 16, out); });
+        const float d = time_ms([&] { k_read<16><<<sms * 2, 256>>>(buf, bytes / 16, out); });
+        ms_rd = a < b ? a : b;
+        ms_rd = ms_rd < c ? ms_rd : c;
+        ms_rd = ms_rd < d ? ms_rd : d;
         cudaFree(buf);
     }
     const cudaError_t e = cudaDeviceSynchronize();
