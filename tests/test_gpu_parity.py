@@ -306,3 +306,16 @@ def test_fast_and_generic_fft_paths_agree(btg, monkeypatch):
                              (h1, h2, R.gauss_newton_apply(spec, m, np.linspace(0.5, 2, 5), 0.2, 1))):
         assert R.rel_l2(got, want) <= TOL64
         assert R.rel_l2(other, want) <= TOL64
+
+
+def test_tma_gemv_path_matches(btg, monkeypatch):
+    """The opt-in TMA-ring GEMV (BTG_GEMV_TMA=1) against the oracle, ragged shapes."""
+    monkeypatch.setenv("BTG_GEMV_TMA", "1")
+    for nd, nm, nt in ((13, 1500, 64), (100, 4096, 96), (3, 17, 20)):
+        blocks, m, d = R.random_problem(900 + nm, nd, nm, nt)
+        spec = R.setup_full(blocks)
+        with btg.setup(blocks) as op:
+            assert R.rel_l2(op.apply_forward(m), R.apply_forward(spec, m)) <= TOL64
+            assert R.rel_l2(op.apply_adjoint(d), R.apply_adjoint(spec, d)) <= TOL64
+            a = op.apply_forward(m)
+            assert np.array_equal(a, op.apply_forward(m))
