@@ -41,7 +41,8 @@ typedef enum {
     BTG_EARG = 3,    /* invalid argument / state -> btoep::Error                                   */
     BTG_ECUDA = 4,   /* CUDA runtime failure                                                       */
     BTG_ENOMEM = 5,  /* device allocation failed                                                   */
-    BTG_EGRID = 6    /* unserviceable processor grid -> btoep::GridError (distributed.cpp:147-152) */
+    BTG_EGRID = 6,   /* unserviceable processor grid -> btoep::GridError (distributed.cpp:147-152) */
+    BTG_ESOLVER = 7  /* CG lost positive definiteness -> btoep::SolverError (inverse.cpp:124-136) */
 } btg_status;
 
 typedef enum { BTG_F64 = 64, BTG_F32 = 32 } btg_precision;
@@ -107,6 +108,29 @@ btg_status btg_adjoint(btg_op op, const double* d, size_t d_len, double* m, size
 btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, size_t hv_len,
                        size_t nrhs, const double* gamma_inv, int gamma_kind, double alpha,
                        int reg_kind, unsigned flags);
+
+/* Device-resident conjugate gradients on (F* Gamma^-1 F + alpha R) x = rhs,
+ * optionally preconditioned with R^-1 (Thomas solve per source): the caller
+ * of the Hessian action, btoep::cg_solve (inverse.hpp:51-53, inverse.cpp:105-156),
+ * same stopping rule (relative residual <= tol; max_iterations = 0 selects
+ * 10 ceil(sqrt(N_m N_t)) + 1) and the same SolverError conditions
+ * (BTG_ESOLVER). x starts at zero. Vectors stay in HBM; only the scalars of
+ * each iteration cross to the host. */
+typedef struct {
+    size_t iterations;
+    double relative_residual;
+    int converged;
+    double seconds;  /* device time of the solve */
+} btg_cg_result;
+
+btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x, size_t x_len,
+                        const double* gamma_inv, int gamma_kind, double alpha, int reg_kind,
+                        double tol, size_t max_iterations, int use_reg_preconditioner,
+                        unsigned flags, btg_cg_result* result);
+
+/* 1/2 |F m - d_obs|^2 + alpha/2 m^T R m  (btoep::objective_eval, inverse.cpp:93-103). */
+btg_status btg_objective(btg_op op, const double* m, size_t m_len, const double* d_obs, size_t d_len,
+                         double alpha, int reg_kind, unsigned flags, double* value);
 
 /* Fused output epilogue of one direction (the C2R store, K9): y = Gamma^-1 x
  * (gamma_kind != NONE; per output channel or per (channel, t)) + alpha R reg_v

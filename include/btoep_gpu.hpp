@@ -38,6 +38,9 @@ struct OrderingError : Error {
 struct GridError : Error {
     using Error::Error;
 };
+struct SolverError : Error {
+    using Error::Error;
+};
 
 namespace detail {
 inline void check(btg_status s) {
@@ -47,6 +50,7 @@ inline void check(btg_status s) {
         case BTG_EDIM: throw DimensionError(msg);
         case BTG_EORDER: throw OrderingError(msg);
         case BTG_EGRID: throw GridError(msg);
+        case BTG_ESOLVER: throw SolverError(msg);
         default: throw Error(msg);
     }
 }
@@ -294,5 +298,52 @@ struct HessianOperator {
         return out;
     }
 };
+
+// btoep::CGResult / cg_solve (inverse.hpp:44-53): the whole iteration runs in HBM.
+struct CGResult {
+    SpaceTimeVector solution;
+    std::size_t iterations = 0;
+    double relative_residual = 0.0;
+    bool converged = false;
+};
+
+inline CGResult cg_solve(const HessianOperator& hessian, const SpaceTimeVector& rhs, double tol = 1e-8,
+                         std::size_t max_iterations = 0, bool use_reg_preconditioner = false) {
+    if (!hessian.op) throw Error("hessian: no operator attached");
+    const SpectralP2O& op = *hessian.op;
+    detail::check_apply_input(op, rhs, op.num_sources, "cg_solve");
+    int gk = BTG_GAMMA_NONE;
+    if (hessian.gamma_inv.size() == op.num_sensors) gk = BTG_GAMMA_PER_SENSOR;
+    else if (hessian.gamma_inv.size() == op.num_sensors * op.num_steps) gk = BTG_GAMMA_PER_SAMPLE;
+    CGResult out;
+    out.solution = SpaceTimeVector::zeros(rhs.spatial_dim, rhs.num_steps, Ordering::SOTI);
+    btg_cg_result r{};
+    detail::check(btg_cg_solve(op.handle(), rhs.values.data(), rhs.values.size(), out.solution.values.data(),
+                               out.solution.values.size(),
+                               hessian.gamma_inv.empty() ? nullptr : hessian.gamma_inv.data(), gk,
+                               hessian.reg.alpha,
+                               hessian.reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN
+                                                                              : BTG_REG_IDENTITY,
+                               tol, max_iterations, use_reg_preconditioner ? 1 : 0, 0u, &r));
+    out.iterations = r.iterations;
+    out.relative_residual = r.relative_residual;
+    out.converged = r.converged != 0;
+    return out;
+}
+
+// btoep::objective_eval (inverse.hpp:41-42)
+inline double objective_eval(const SpectralP2O& op, const SpaceTimeVector& m, const SpaceTimeVector& d_obs,
+                             const Regularization& reg) {
+    detail::check_apply_input(op, m, op.num_sources, "objective");
+    d_obs.validate();
+    d_obs.require_ordering(Ordering::SOTI);
+    double v = 0.0;
+    detail::check(btg_objective(op.handle(), m.values.data(), m.values.size(), d_obs.values.data(),
+                                d_obs.values.size(), reg.alpha,
+                                reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN
+                                                                       : BTG_REG_IDENTITY,
+                                0u, &v));
+    return v;
+}
 
 }  // namespace btoep

@@ -157,6 +157,36 @@ int ref_hessian(void* h, const double* v, double* hv, double alpha, int reg_kind
     });
 }
 
+// cg_solve (inverse.cpp:105-156) on HessianOperator{op, reg}; out[0..2] =
+// iterations, relative_residual, converged.
+int ref_cg_solve(void* h, const double* rhs, double* x, double alpha, int reg_kind, double tol,
+                 std::size_t max_iterations, int precondition, double* out) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        HessianOperator hess;
+        hess.op = &op;
+        hess.reg.kind = reg_kind ? RegKind::TemporalLaplacian : RegKind::ScaledIdentity;
+        hess.reg.alpha = alpha;
+        const CGResult r = cg_solve(hess, make_soti(rhs, op.num_sources, op.num_steps), tol, max_iterations,
+                                    precondition != 0);
+        copy_out(r.solution, x);
+        out[0] = static_cast<double>(r.iterations);
+        out[1] = r.relative_residual;
+        out[2] = r.converged ? 1.0 : 0.0;
+    });
+}
+
+int ref_objective(void* h, const double* m, const double* d_obs, double alpha, int reg_kind, double* value) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        Regularization reg;
+        reg.kind = reg_kind ? RegKind::TemporalLaplacian : RegKind::ScaledIdentity;
+        reg.alpha = alpha;
+        *value = objective_eval(op, make_soti(m, op.num_sources, op.num_steps),
+                                make_soti(d_obs, op.num_sensors, op.num_steps), reg);
+    });
+}
+
 // ---- naive (time-domain) backend: SOTI in, SOTI out ---------------------------
 int ref_naive_forward(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt,
                       const double* m, double* d) {

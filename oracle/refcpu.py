@@ -53,6 +53,10 @@ def lib():
         L.ref_distributed_hessian.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double,
                                               ctypes.c_int, ctypes.c_int]
         L.ref_verify.argtypes = [ctypes.c_uint64, ctypes.c_char_p, _size_t, ctypes.POINTER(ctypes.c_int)]
+        L.ref_cg_solve.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_double, _size_t, ctypes.c_int, _c_double_p]
+        L.ref_objective.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int,
+                                    _c_double_p]
         _lib = L
     return _lib
 
@@ -132,6 +136,21 @@ class RefSpectralOperator:
         hv = np.empty_like(v)
         _check(lib().ref_hessian(self._h, _p(v), _p(hv), float(alpha), int(reg_kind)))
         return hv
+
+    def cg_solve(self, rhs, alpha: float, reg_kind: int = 0, tol: float = 1e-8, maxiter: int = 0,
+                 precondition: bool = False):
+        """btoep::cg_solve (inverse.cpp:105-156): (x, iterations, relative_residual, converged)."""
+        rhs = _f64(rhs)
+        x = np.empty_like(rhs)
+        out = np.zeros(3)
+        _check(lib().ref_cg_solve(self._h, _p(rhs), _p(x), float(alpha), int(reg_kind), float(tol), int(maxiter),
+                                  int(precondition), _p(out)))
+        return x, int(out[0]), float(out[1]), bool(out[2])
+
+    def objective(self, m, d_obs, alpha: float, reg_kind: int = 0) -> float:
+        v = np.zeros(1)
+        _check(lib().ref_objective(self._h, _p(_f64(m)), _p(_f64(d_obs)), float(alpha), int(reg_kind), _p(v)))
+        return float(v[0])
 
 
 def naive_forward(blocks, m) -> np.ndarray:

@@ -6,14 +6,19 @@ Compute runs only in ``libbtg.so`` (hand-written sm_100a CUDA, C ABI in
 Python surface plus the multi-GPU grid (``distributed``).
 """
 
-from ._lib import DimensionError, Error, GridError, OrderingError  # noqa: F401
+from ._lib import DimensionError, Error, GridError, OrderingError, SolverError  # noqa: F401
 from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
+from .solver import cg_solve, cg_solve_op, objective_eval  # noqa: F401
 
 __all__ = [
     "DimensionError",
     "Error",
     "GridError",
     "OrderingError",
+    "SolverError",
+    "cg_solve",
+    "cg_solve_op",
+    "objective_eval",
     "HessianOperator",
     "SpectralOperator",
     "create",

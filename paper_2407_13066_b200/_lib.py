@@ -11,7 +11,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
 
-BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID = range(7)
+BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER = range(8)
 BTG_F64, BTG_F32 = 64, 32
 BTG_DEVICE_PTRS = 0x1
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's stream 0)
@@ -41,6 +41,8 @@ EXPORTED = (
     "btg_forward_ex",
     "btg_adjoint_ex",
     "btg_fill_uniform_3d",
+    "btg_cg_solve",
+    "btg_objective",
 )
 
 
@@ -58,6 +60,21 @@ class OrderingError(ValueError):
 
 class GridError(ValueError):
     """btoep::GridError (errors.hpp:28-30)."""
+
+
+class SolverError(RuntimeError):
+    """btoep::SolverError (errors.hpp:33-35); the reference binds it to RuntimeError."""
+
+
+class CgResult(ctypes.Structure):
+    """btg_cg_result == btoep::CGResult minus the solution (inverse.hpp:44-49)."""
+
+    _fields_ = [
+        ("iterations", ctypes.c_size_t),
+        ("relative_residual", ctypes.c_double),
+        ("converged", ctypes.c_int),
+        ("seconds", ctypes.c_double),
+    ]
 
 
 class Epilogue(ctypes.Structure):
@@ -139,6 +156,10 @@ def load():
     L.btg_adjoint_ex.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.POINTER(Epilogue), ctypes.c_uint]
     L.btg_fill_uniform_3d.argtypes = [_dp, _sz, _sz, _sz, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _vp]
+    L.btg_cg_solve.argtypes = [_vp, _dp, _sz, _dp, _sz, _dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                               ctypes.c_double, _sz, ctypes.c_int, ctypes.c_uint, ctypes.POINTER(CgResult)]
+    L.btg_objective.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_double, ctypes.c_int, ctypes.c_uint,
+                                ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTED:
         if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
             getattr(L, name).restype = ctypes.c_int
@@ -159,4 +180,6 @@ def check(status: int) -> None:
         raise GridError(msg)
     if status == BTG_ENOMEM:
         raise MemoryError(msg)
+    if status == BTG_ESOLVER:
+        raise SolverError(msg)
     raise Error(msg)

@@ -645,6 +645,241 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
     return finish_host(op, hv, hvd, hv_len, flags);
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident CG (inverse.cpp:105-156) and objective (inverse.cpp:93-103)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct CgBuffers {
+    double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *hp = nullptr, *partial = nullptr,
+           *scal = nullptr, *pivot = nullptr, *scratch = nullptr, *rhs = nullptr, *gam = nullptr;
+    ~CgBuffers() {
+        for (double* q : {x, r, z, p, hp, partial, scal, pivot, scratch, rhs, gam}) cudaFree(q);
+    }
+};
+
+btg_status alloc(double** p, size_t n) {
+    BTG_CUDA(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(double)));
+    return BTG_OK;
+}
+
+btg_status read_scalar(btg_op op, const double* dev, double* host) {
+    BTG_CUDA(cudaMemcpyAsync(host, dev, sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    return BTG_OK;
+}
+
+// H v on device pointers (the body of btg_hessian without staging).
+btg_status hessian_dev(btg_op op, const double* vd, double* hvd, const double* gd, int gamma_kind, double alpha,
+                       int reg_kind) {
+    BTG_TRY(grow(op->wt, op->wtcap, op->nd * op->nt));
+    btg::C2REpilogue e1{};
+    e1.gamma = gd;
+    e1.gamma_mode = gamma_kind;
+    e1.gamma_dim = (int)op->nd;
+    BTG_TRY(pipeline(op, false, vd, op->wt, 1, e1));
+    btg::C2REpilogue e2{};
+    if (alpha != 0.0) {
+        e2.v = vd;
+        e2.alpha = alpha;
+        e2.reg_kind = reg_kind;
+    }
+    return pipeline(op, true, op->wt, hvd, 1, e2);
+}
+
+}  // namespace
+
+btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_out, size_t x_len,
+                        const double* gamma_inv, int gamma_kind, double alpha, int reg_kind, double tol,
+                        size_t max_iterations, int use_reg_preconditioner, unsigned flags, btg_cg_result* result) {
+    if (!op || !result) return fail(BTG_EARG, "null argument");
+    std::lock_guard<std::mutex> lock(op->mu);
+    BTG_TRY(check_ready(op));
+    if (!rhs || !x_out) return fail(BTG_EARG, "null vector pointer");
+    if (reg_kind != BTG_REG_IDENTITY && reg_kind != BTG_REG_TEMPORAL_LAPLACIAN)
+        return fail(BTG_EARG, "unknown regularization kind %d", reg_kind);
+    if (gamma_kind < BTG_GAMMA_NONE || gamma_kind > BTG_GAMMA_PER_SAMPLE)
+        return fail(BTG_EARG, "unknown gamma kind %d", gamma_kind);
+    if (gamma_kind != BTG_GAMMA_NONE && !gamma_inv) return fail(BTG_EARG, "gamma_inv is null");
+    BTG_TRY(check_len("cg_solve", rhs_len, op->nm, op->nt, 1, op->nm));
+    BTG_TRY(check_len("cg_solve", x_len, op->nm, op->nt, 1, op->nm));
+    DeviceGuard g(op->device);
+    const size_t n = rhs_len;
+    if (max_iterations == 0)
+        max_iterations = 10 * static_cast<size_t>(std::ceil(std::sqrt(static_cast<double>(n)))) + 1;
+    *result = btg_cg_result{};
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, op->stream);
+
+    CgBuffers b;
+    const bool dev = flags & BTG_DEVICE_PTRS;
+    BTG_TRY(alloc(&b.r, n));
+    BTG_TRY(alloc(&b.p, n));
+    BTG_TRY(alloc(&b.hp, n));
+    BTG_TRY(alloc(&b.partial, btg::kRedBlocks));
+    BTG_TRY(alloc(&b.scal, 4));
+    const bool precond = use_reg_preconditioner != 0;
+    if (precond) BTG_TRY(alloc(&b.z, n));
+    double* x = dev ? x_out : nullptr;
+    if (!dev) {
+        BTG_TRY(alloc(&b.x, n));
+        x = b.x;
+    }
+    const double* rhs_d = rhs;
+    if (!dev) {
+        BTG_TRY(alloc(&b.rhs, n));
+        BTG_CUDA(cudaMemcpyAsync(b.rhs, rhs, n * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        rhs_d = b.rhs;
+    }
+    const double* gd = nullptr;
+    if (gamma_kind != BTG_GAMMA_NONE) {
+        const size_t glen = gamma_kind == BTG_GAMMA_PER_SENSOR ? op->nd : op->nd * op->nt;
+        gd = gamma_inv;
+        if (!dev) {
+            BTG_TRY(alloc(&b.gam, glen));
+            BTG_CUDA(cudaMemcpyAsync(b.gam, gamma_inv, glen * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+            gd = b.gam;
+        }
+    }
+    const bool lap = reg_kind == BTG_REG_TEMPORAL_LAPLACIAN;
+    if (precond && lap) {
+        // Thomas pivots of the (-1, 2, -1) system, in the reference's order (inverse.cpp:57-63)
+        std::vector<double> piv(op->nt), scr(op->nt, 0.0);
+        double pivot = 2.0;
+        piv[0] = pivot;
+        for (size_t t = 1; t < op->nt; ++t) {
+            scr[t] = -1.0 / pivot;
+            pivot = 2.0 + scr[t];
+            piv[t] = pivot;
+        }
+        BTG_TRY(alloc(&b.pivot, op->nt));
+        BTG_TRY(alloc(&b.scratch, op->nt));
+        BTG_CUDA(cudaMemcpyAsync(b.pivot, piv.data(), op->nt * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        BTG_CUDA(cudaMemcpyAsync(b.scratch, scr.data(), op->nt * sizeof(double), cudaMemcpyHostToDevice,
+                                 op->stream));
+    }
+    auto precondition = [&](double* zout, const double* rin) -> btg_status {
+        if (lap) {
+            BTG_CUDA(btg::launch_reg_apply_inverse(zout, rin, b.pivot, b.scratch, op->nm, (int)op->nt, op->stream));
+        } else {
+            BTG_CUDA(cudaMemcpyAsync(zout, rin, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
+        }
+        op->counters.launches++;
+        return BTG_OK;
+    };
+    auto dot = [&](const double* a, const double* c, double* host) -> btg_status {
+        BTG_CUDA(btg::launch_dot(a, c, n, b.partial, b.scal, op->stream));
+        op->counters.launches += 2;
+        return read_scalar(op, b.scal, host);
+    };
+
+    BTG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), op->stream));
+    double rhs_n2 = 0.0;
+    BTG_TRY(dot(rhs_d, rhs_d, &rhs_n2));
+    const double rhs_norm = std::sqrt(rhs_n2);
+    btg_status status = BTG_OK;
+    if (rhs_norm == 0.0) {
+        result->converged = 1;
+    } else {
+        BTG_CUDA(cudaMemcpyAsync(b.r, rhs_d, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
+        const double* zp = b.r;
+        if (precond) {
+            BTG_TRY(precondition(b.z, b.r));
+            zp = b.z;
+        }
+        BTG_CUDA(cudaMemcpyAsync(b.p, zp, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
+        double rho = 0.0;
+        BTG_TRY(dot(b.r, zp, &rho));
+        if (rho <= 0.0 && precond)
+            return fail(BTG_ESOLVER, "cg: preconditioned residual product r^T z = %g <= 0; regularization is not "
+                                     "positive definite", rho);
+        result->relative_residual = 1.0;
+        for (size_t it = 1; it <= max_iterations; ++it) {
+            BTG_TRY(hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind));
+            double curvature = 0.0;
+            BTG_TRY(dot(b.p, b.hp, &curvature));
+            if (!(curvature > 0.0)) {
+                status = fail(BTG_ESOLVER, "cg: direction of non-positive curvature, p^T H p = %g; the Hessian is "
+                                           "not positive definite", curvature);
+                break;
+            }
+            const double step = rho / curvature;
+            double rn2 = 0.0;
+            BTG_CUDA(btg::launch_cg_update(x, b.r, b.p, b.hp, step, n, b.partial, b.scal, op->stream));
+            op->counters.launches += 2;
+            BTG_TRY(read_scalar(op, b.scal, &rn2));
+            result->iterations = it;
+            result->relative_residual = std::sqrt(rn2) / rhs_norm;
+            if (result->relative_residual <= tol) {
+                result->converged = 1;
+                break;
+            }
+            double rho_next = rn2;
+            if (precond) {
+                BTG_TRY(precondition(b.z, b.r));
+                BTG_TRY(dot(b.r, b.z, &rho_next));
+            }
+            const double beta = rho_next / rho;
+            rho = rho_next;
+            BTG_CUDA(btg::launch_xpby(b.p, precond ? b.z : b.r, beta, n, op->stream));
+            op->counters.launches++;
+        }
+    }
+    if (status != BTG_OK) return status;
+    if (!dev) BTG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+    cudaEventRecord(t1, op->stream);
+    BTG_CUDA(cudaEventSynchronize(t1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    result->seconds = ms * 1e-3;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    return BTG_OK;
+}
+
+btg_status btg_objective(btg_op op, const double* m, size_t m_len, const double* d_obs, size_t d_len, double alpha,
+                         int reg_kind, unsigned flags, double* value) {
+    if (!op || !value) return fail(BTG_EARG, "null argument");
+    std::lock_guard<std::mutex> lock(op->mu);
+    BTG_TRY(check_ready(op));
+    if (!m || !d_obs) return fail(BTG_EARG, "null vector pointer");
+    if (reg_kind != BTG_REG_IDENTITY && reg_kind != BTG_REG_TEMPORAL_LAPLACIAN)
+        return fail(BTG_EARG, "unknown regularization kind %d", reg_kind);
+    if (d_len != op->nd * op->nt)
+        return fail(BTG_EDIM, "objective: observations do not match the operator");
+    BTG_TRY(check_len("objective", m_len, op->nm, op->nt, 1, op->nm));
+    DeviceGuard g(op->device);
+    CgBuffers b;
+    const bool dev = flags & BTG_DEVICE_PTRS;
+    const double* md = m;
+    const double* dd = d_obs;
+    if (!dev) {
+        BTG_TRY(alloc(&b.x, m_len));
+        BTG_TRY(alloc(&b.rhs, d_len));
+        BTG_CUDA(cudaMemcpyAsync(b.x, m, m_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        BTG_CUDA(cudaMemcpyAsync(b.rhs, d_obs, d_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        md = b.x;
+        dd = b.rhs;
+    }
+    BTG_TRY(alloc(&b.r, d_len));
+    BTG_TRY(alloc(&b.p, m_len));
+    BTG_TRY(alloc(&b.partial, btg::kRedBlocks));
+    BTG_TRY(alloc(&b.scal, 1));
+    BTG_TRY(pipeline(op, false, md, b.r, 1, btg::C2REpilogue{}));
+    BTG_CUDA(btg::launch_sub(b.r, b.r, dd, d_len, op->stream));
+    double misfit = 0.0, reg = 0.0;
+    BTG_CUDA(btg::launch_dot(b.r, b.r, d_len, b.partial, b.scal, op->stream));
+    BTG_TRY(read_scalar(op, b.scal, &misfit));
+    BTG_CUDA(btg::launch_reg_apply(b.p, md, op->nm, (int)op->nt, reg_kind, op->stream));
+    BTG_CUDA(btg::launch_dot(md, b.p, m_len, b.partial, b.scal, op->stream));
+    BTG_TRY(read_scalar(op, b.scal, &reg));
+    op->counters.launches += 6;
+    *value = 0.5 * misfit + 0.5 * alpha * reg;
+    return BTG_OK;
+}
+
 btg_status btg_set_stream(btg_op op, void* stream) {
     if (!op) return fail(BTG_EARG, "null operator handle");
     std::lock_guard<std::mutex> lock(op->mu);

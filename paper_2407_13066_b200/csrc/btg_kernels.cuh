@@ -86,6 +86,19 @@ cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int
 cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream);
 
+// CG vector kernels (btg_blas.cu). Reductions use a fixed grid of kRedBlocks
+// blocks; `partial` holds kRedBlocks doubles; scalar results land in device memory.
+constexpr int kRedBlocks = 592;
+cudaError_t launch_dot(const double* a, const double* b, size_t n, double* partial, double* out,
+                       cudaStream_t stream);
+cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* hp, double s, size_t n,
+                             double* partial, double* rnorm2, cudaStream_t stream);
+cudaError_t launch_xpby(double* p, const double* z, double beta, size_t n, cudaStream_t stream);
+cudaError_t launch_sub(double* y, const double* a, const double* b, size_t n, cudaStream_t stream);
+cudaError_t launch_reg_apply(double* y, const double* v, size_t rows, int nt, int kind, cudaStream_t stream);
+cudaError_t launch_reg_apply_inverse(double* x, const double* b, const double* pivot, const double* scratch,
+                                     size_t rows, int nt, cudaStream_t stream);
+
 // out[(a*nb + b)*nc + c] = uniform(seed ^ (offset + a*sa + b*sb + c))
 cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                 uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream);
