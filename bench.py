@@ -46,6 +46,10 @@ CONFIGS = {
               label="configs[3]: multi-RHS batched Hessian, 32 RHS, N_t=1024 N_d=128 N_m=16384 FP64, ZGEMM on DMMA"),
     "Dp": dict(nt=1024, nd=128, nm=4096, nrhs=32,
                label="profiling slice of configs[3]: 32 RHS, N_t=1024 N_d=128 N_m=4096"),
+    "E8": dict(nt=4096, nd=256, nm=8192, nrhs=1,
+               label="configs[4] per-GPU shard of the 1x8 grid: N_t=4096 N_d=256 N_m=65536/8 FP64 (F-hat 137 GB)"),
+    "E4f32": dict(nt=4096, nd=256, nm=16384, nrhs=1, precision=32,
+                  label="configs[4] per-GPU shard of the 1x4 grid, FP32 F-hat: N_t=4096 N_d=256 N_m=65536/4"),
 }
 CPU_SAMPLE_NM = 2048  # N_m slice the CPU reference runs on (extrapolate linearly in N_m)
 
@@ -235,7 +239,8 @@ def build_operator(cfg, device, seed):
     from paper_2407_13066_b200.distributed import Shard, synthetic_shard_operator
 
     nt, nd, nm = cfg["nt"], cfg["nd"], cfg["nm"]
-    return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), seed, device)
+    return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), seed, device,
+                                    precision=cfg.get("precision", 64))
 
 
 def run_ours(args):
@@ -255,6 +260,8 @@ def run_ours(args):
     cfg = dict(CONFIGS["B" if world == 1 else "C"])
     if args.config:
         cfg = dict(CONFIGS[args.config])
+    if args.precision:
+        cfg["precision"] = args.precision
     nt, nd, nm = cfg["nt"], cfg["nd"], cfg["nm"]
     nrhs = cfg.get("nrhs", 1)
     peak, peak_src = hbm_peak()
@@ -349,7 +356,8 @@ def run_ours(args):
     else:
         per_mean = {k: statistics.mean(v) for k, v in per.items()}
     ms_step = total_ms / args.steps
-    b = alg_bytes(nt, nd, nm, nrhs)
+    prec = cfg.get("precision", 64)
+    b = alg_bytes(nt, nd, nm, nrhs, elem=16 if prec == 64 else 8)
     fl = alg_flops(nt, nd, nm, nrhs)
     step_bytes = (b["F"] + b["F*"] + b["H"]) * world
     value = step_bytes / (ms_step * 1e-3) / 1e12
@@ -450,7 +458,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64",
+            "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32 F-hat, f64 vectors/accumulation",
             "data": "synthetic: device SplitMix64 uniform(-1,1) first block column (seed 1000, global index), m (seed 7), "
                     "Gamma^-1 uniform(0.5,2) per sensor (seed 8)",
             "config": {"workload": cfg["label"], "N_t": nt, "N_d": nd, "N_m": nm, "nrhs": nrhs, "grid": grid,
@@ -481,6 +489,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--precision", type=int, choices=[64, 32], default=None, help="F-hat precision override")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rules)")

@@ -1,0 +1,83 @@
+// A reference-style C++ caller compiled against include/btoep_gpu.hpp and
+// linked with libbtg.so (instead of the reference's btoep_core + FFTW). The
+// statements mirror the reference's own tests (test_block_operator.cpp:88-115,
+// test_inverse.cpp:81-98): identity and shift operators, typed errors, the
+// Hessian of the zero operator, and CG.
+#include <cmath>
+#include <cstdio>
+
+#include "btoep_gpu.hpp"
+
+using namespace btoep;
+
+static int failures = 0;
+#define CHECK(cond)                                              \
+    do {                                                         \
+        if (!(cond)) {                                           \
+            std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                          \
+        }                                                        \
+    } while (0)
+
+int main() {
+    // identity-block operator acts as the identity
+    CompactP2O eye = CompactP2O::zeros(3, 3, 8);
+    for (std::size_t i = 0; i < 3; ++i) eye.entry(0, i, i) = 1.0;
+    SpectralP2O op = setup(eye);
+    SpaceTimeVector m = SpaceTimeVector::zeros(3, 8, Ordering::SOTI);
+    for (std::size_t k = 0; k < m.values.size(); ++k) m.values[k] = std::sin(0.3 * k);
+    PipelineCounters counters;
+    counters.time_stages = true;
+    SpaceTimeVector d = apply_forward(op, m, &counters);
+    for (std::size_t k = 0; k < m.values.size(); ++k) CHECK(std::abs(d.values[k] - m.values[k]) < 1e-12);
+    CHECK(counters.apply.ops > 0.0 && counters.apply.seconds > 0.0);
+    SpaceTimeVector a = apply_adjoint(op, m);
+    for (std::size_t k = 0; k < m.values.size(); ++k) CHECK(std::abs(a.values[k] - m.values[k]) < 1e-12);
+    CHECK(op.num_freq() == 16);
+    CHECK(op.freq_blocks().size() == 16 * 9);
+
+    // shift delays the input
+    CompactP2O sh = CompactP2O::zeros(2, 2, 6);
+    for (std::size_t i = 0; i < 2; ++i) sh.entry(1, i, i) = 1.0;
+    SpectralP2O sop = setup(sh);
+    SpaceTimeVector v = SpaceTimeVector::zeros(2, 6, Ordering::SOTI);
+    for (std::size_t k = 0; k < v.values.size(); ++k) v.values[k] = 1.0 + k;
+    SpaceTimeVector dv = apply_forward(sop, v);
+    for (std::size_t s = 0; s < 2; ++s) {
+        CHECK(std::abs(dv.at(s, 0)) < 1e-12);
+        for (std::size_t t = 1; t < 6; ++t) CHECK(std::abs(dv.at(s, t) - v.at(s, t - 1)) < 1e-12);
+    }
+
+    // typed errors
+    bool threw = false;
+    try {
+        apply_forward(op, SpaceTimeVector::zeros(4, 8, Ordering::SOTI));
+    } catch (const DimensionError&) {
+        threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+        apply_forward(op, SpaceTimeVector::zeros(3, 8, Ordering::TOSI));
+    } catch (const OrderingError&) {
+        threw = true;
+    }
+    CHECK(threw);
+
+    // zero operator with identity regularization scales by alpha (test_inverse.cpp:88-97)
+    SpectralP2O zop = setup(CompactP2O::zeros(2, 3, 4));
+    HessianOperator h{&zop, {RegKind::ScaledIdentity, 0.25}};
+    SpaceTimeVector w = SpaceTimeVector::zeros(3, 4, Ordering::SOTI);
+    for (std::size_t k = 0; k < w.values.size(); ++k) w.values[k] = 0.1 * k - 0.3;
+    SpaceTimeVector hw = h.apply(w);
+    for (std::size_t k = 0; k < w.values.size(); ++k) CHECK(std::abs(hw.values[k] - 0.25 * w.values[k]) < 1e-14);
+
+    // CG on the identity operator: (I + alpha I) x = b
+    HessianOperator hi{&op, {RegKind::ScaledIdentity, 1.0}};
+    CGResult r = cg_solve(hi, m, 1e-12, 50, false);
+    CHECK(r.converged);
+    for (std::size_t k = 0; k < m.values.size(); ++k) CHECK(std::abs(r.solution.values[k] - 0.5 * m.values[k]) < 1e-12);
+
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}
