@@ -98,6 +98,8 @@ struct btg_op_s {
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
 
     cudaStream_t own_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
+    cudaEvent_t ev[9] = {};              // kHostChunks + 1 chunk / ordering events
     cudaStream_t stream = nullptr;
 
     // workspace (grown on demand)
@@ -228,13 +230,16 @@ btg_status host_buffers(btg_op op, size_t nin, size_t nout) {
 // ---- pipeline pieces --------------------------------------------------------
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out) {
+// R2C of `channels` SOTI rows into a frequency-major array whose frequency
+// stride is `fs` (default: channels; a column chunk of a wider array otherwise).
+btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out, size_t fs = 0) {
     StageClock clk(op, &op->counters.forward_fft);
+    if (!fs) fs = channels;
     if (op->fast_ok && aligned16(v) && aligned16(out))
-        BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, (long long)channels,
+        BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, (long long)fs,
                                           (int)channels, op->fast, op->stream));
     else
-        BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)channels, 1,
+        BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)fs, 1,
                                           (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream));
     op->counters.launches++;
     op->counters.forward_fft.ops += fft_ops(channels, op->nt);
@@ -243,13 +248,14 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
 }
 
 btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* out,
-                       const btg::C2REpilogue& epi) {
+                       const btg::C2REpilogue& epi, size_t fs = 0) {
     StageClock clk(op, &op->counters.inverse_fft);
+    if (!fs) fs = channels;
     if (op->fast_ok && aligned16(in) && aligned16(out))
-        BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)channels, out, (long long)op->nt,
+        BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)fs, out, (long long)op->nt,
                                           (int)channels, op->fast, epi, op->stream));
     else
-        BTG_CUDA(btg::launch_c2r(in, (long long)channels, 1, out, (long long)op->nt, (int)channels,
+        BTG_CUDA(btg::launch_c2r(in, (long long)fs, 1, out, (long long)op->nt, (int)channels,
                                  (int)op->nt, op->plan, op->fft_batch, epi, op->stream));
     op->counters.launches++;
     op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
@@ -342,6 +348,105 @@ btg_status stage_small(btg_op op, const double* src, size_t n, double*& buf, siz
     return BTG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Host-pointer calls: overlap the PCIe transfers of the long (N_m x N_t)
+// vector with the HBM-bound Fourier-space step. The N_m channels are cut into
+// column chunks; chunk c's H2D copy (copy stream) overlaps chunk c-1's R2C +
+// forward GEMV partial (compute stream), and on the way out chunk c's D2H
+// overlaps chunk c+1's adjoint GEMV + C2R. Forward partial products are added
+// chunk by chunk in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr size_t kHostChunks = 8;
+
+bool host_pipelined(btg_op op, size_t nrhs) {
+    static const bool off = std::getenv("BTG_NO_HOST_PIPELINE") != nullptr;
+    return !off && nrhs == 1 && op->legacy_gemv && op->nm >= 4096;
+}
+
+size_t chunk_cols(btg_op op) {
+    const size_t per = (op->nm + kHostChunks - 1) / kHostChunks;
+    return (per + 511) / 512 * 512;
+}
+
+btg_status ensure_copy_stream(btg_op op) {
+    if (!op->copy_stream) BTG_CUDA(cudaStreamCreateWithFlags(&op->copy_stream, cudaStreamNonBlocking));
+    for (size_t c = 0; c <= kHostChunks; ++c)
+        if (!op->ev[c]) BTG_CUDA(cudaEventCreateWithFlags(&op->ev[c], cudaEventDisableTiming));
+    return BTG_OK;
+}
+
+btg_status gemv_range(btg_op op, bool adjoint, const double2* in, double2* out, size_t j0, size_t nc, bool acc) {
+    const int nf = (int)op->nf, nd = (int)op->nd, nm = (int)op->nm;
+    cudaError_t e;
+    if (op->precision == BTG_F64) {
+        const double2* F = static_cast<const double2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj_range(F, in, out, nf, nd, nm, (int)j0, (int)nc, op->stream)
+                    : btg::launch_gemv_fwd_range(F, in, out, nf, nd, nm, (int)j0, (int)nc, acc, op->stream);
+    } else {
+        const float2* F = static_cast<const float2*>(op->F);
+        e = adjoint ? btg::launch_gemv_adj_range(F, in, out, nf, nd, nm, (int)j0, (int)nc, op->stream)
+                    : btg::launch_gemv_fwd_range(F, in, out, nf, nd, nm, (int)j0, (int)nc, acc, op->stream);
+    }
+    BTG_CUDA(e);
+    op->counters.launches++;
+    return BTG_OK;
+}
+
+void count_apply(btg_op op) {
+    op->counters.apply.ops += 8.0 * op->nd * op->nm * op->nf;
+    op->counters.apply.bytes += (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (op->nm + op->nd);
+}
+
+// m (host, N_m x N_t) -> d-hat in op->wb; the device copy of m stays in op->hin.
+btg_status host_forward_stage(btg_op op, const double* m_host) {
+    BTG_TRY(ensure_spectral(op, 1));
+    BTG_TRY(ensure_copy_stream(op));
+    const size_t nt = op->nt, cols = chunk_cols(op);
+    BTG_CUDA(cudaEventRecord(op->ev[kHostChunks], op->stream));  // hin free of earlier readers
+    BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[kHostChunks], 0));
+    StageClock clk(op, &op->counters.apply);
+    for (size_t c = 0, j0 = 0; j0 < op->nm; ++c, j0 += cols) {
+        const size_t nc = std::min(cols, op->nm - j0);
+        BTG_CUDA(cudaMemcpyAsync(op->hin + j0 * nt, m_host + j0 * nt, nc * nt * sizeof(double),
+                                 cudaMemcpyHostToDevice, op->copy_stream));
+        BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
+        BTG_CUDA(cudaStreamWaitEvent(op->stream, op->ev[c], 0));
+        BTG_TRY(run_r2c_vec(op, op->hin + j0 * nt, nc, op->wa + j0, op->nm));
+        BTG_TRY(gemv_range(op, false, op->wa, op->wb, j0, nc, c > 0));
+    }
+    count_apply(op);
+    return BTG_OK;
+}
+
+// d-hat spectrum in op->wa -> m (host) through chunked adjoint GEMV + C2R + D2H.
+btg_status host_adjoint_stage(btg_op op, double* m_host, const btg::C2REpilogue& epi) {
+    BTG_TRY(ensure_copy_stream(op));
+    const size_t nt = op->nt, cols = chunk_cols(op);
+    size_t nchunks = 0;
+    {
+        StageClock clk(op, &op->counters.apply);
+        for (size_t c = 0, j0 = 0; j0 < op->nm; ++c, j0 += cols) {
+            const size_t nc = std::min(cols, op->nm - j0);
+            BTG_TRY(gemv_range(op, true, op->wa, op->wb, j0, nc, false));
+            btg::C2REpilogue e = epi;
+            if (e.v) e.v = epi.v + j0 * nt;
+            BTG_TRY(run_c2r_vec(op, op->wb + j0, nc, op->hout + j0 * nt, e, op->nm));
+            BTG_CUDA(cudaEventRecord(op->ev[c], op->stream));
+            nchunks = c + 1;
+        }
+    }
+    count_apply(op);
+    for (size_t c = 0, j0 = 0; c < nchunks; ++c, j0 += cols) {
+        const size_t nc = std::min(cols, op->nm - j0);
+        BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[c], 0));
+        BTG_CUDA(cudaMemcpyAsync(m_host + j0 * nt, op->hout + j0 * nt, nc * nt * sizeof(double),
+                                 cudaMemcpyDeviceToHost, op->copy_stream));
+    }
+    BTG_CUDA(cudaStreamSynchronize(op->copy_stream));
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    return BTG_OK;
+}
+
 btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, double* out,
                      size_t out_len, size_t nrhs, const btg_epilogue* ex, unsigned flags) {
     BTG_TRY(check_ready(op));
@@ -364,9 +469,12 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
     DeviceGuard g(op->device);
     const double* din_p = in;
     double* dout_p = out;
-    if (!(flags & BTG_DEVICE_PTRS)) {
+    const bool host = !(flags & BTG_DEVICE_PTRS);
+    const bool chunked = host && host_pipelined(op, nrhs);
+    if (host) {
         BTG_TRY(host_buffers(op, in_len, out_len));
-        BTG_CUDA(cudaMemcpyAsync(op->hin, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        if (!(chunked && !adjoint))  // the chunked forward streams its input itself
+            BTG_CUDA(cudaMemcpyAsync(op->hin, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         din_p = op->hin;
         dout_p = op->hout;
     }
@@ -391,6 +499,16 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
                                      op->stream));
             epi.v = op->vcopy;
         }
+    }
+    if (chunked && !adjoint) {
+        BTG_TRY(host_forward_stage(op, in));
+        BTG_TRY(run_c2r_vec(op, op->wb, op->nd, dout_p, epi));
+        return finish_host(op, out, dout_p, out_len, flags);
+    }
+    if (chunked && adjoint) {
+        BTG_TRY(ensure_spectral(op, 1));
+        BTG_TRY(run_r2c_vec(op, din_p, op->nd, op->wa));
+        return host_adjoint_stage(op, out, epi);
     }
     BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, epi));
     return finish_host(op, out, dout_p, out_len, flags);
@@ -605,9 +723,11 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
 
     const double* vd = v;
     double* hvd = hv;
+    const bool chunked = !(flags & BTG_DEVICE_PTRS) && host_pipelined(op, nrhs);
     if (!(flags & BTG_DEVICE_PTRS)) {
         BTG_TRY(host_buffers(op, v_len, hv_len));
-        BTG_CUDA(cudaMemcpyAsync(op->hin, v, v_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        if (!chunked)
+            BTG_CUDA(cudaMemcpyAsync(op->hin, v, v_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         vd = op->hin;
         hvd = op->hout;
     } else if (vd == hvd && alpha != 0.0) {
@@ -634,13 +754,20 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
     e1.gamma = gd;
     e1.gamma_mode = gamma_kind;
     e1.gamma_dim = (int)op->nd;
-    BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
     btg::C2REpilogue e2{};
     if (alpha != 0.0) {
         e2.v = vd;
         e2.alpha = alpha;
         e2.reg_kind = reg_kind;
     }
+    if (chunked) {
+        // H2D of v overlapped with the forward GEMV, D2H of Hv with the adjoint GEMV
+        BTG_TRY(host_forward_stage(op, v));
+        BTG_TRY(run_c2r_vec(op, op->wb, op->nd, op->wt, e1));
+        BTG_TRY(run_r2c_vec(op, op->wt, op->nd, op->wa));
+        return host_adjoint_stage(op, hv, e2);
+    }
+    BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
     BTG_TRY(pipeline(op, true, op->wt, hvd, nrhs, e2));
     return finish_host(op, hv, hvd, hv_len, flags);
 }
@@ -979,6 +1106,12 @@ void btg_destroy(btg_op op) {
         cudaFree(op->gam);
         cudaFree(op->vcopy);
         if (op->own_stream) cudaStreamDestroy(op->own_stream);
+        if (op->copy_stream) {
+            cudaStreamSynchronize(op->copy_stream);
+            cudaStreamDestroy(op->copy_stream);
+        }
+        for (cudaEvent_t e : op->ev)
+            if (e) cudaEventDestroy(e);
     }
     delete op;
 }

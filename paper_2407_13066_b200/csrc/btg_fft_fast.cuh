@@ -1,25 +1,34 @@
 // Register-resident Stockham FFT for the vector transforms (K5 / K9), with the
 // transform length N = N_t fixed at compile time.
 //
-// Per channel, TPC threads hold the data in registers; each radix-R pass loads
-// its R inputs, applies the inter-pass twiddles, runs the R-point DFT in
-// registers and scatters the R outputs autosorted. Passes exchange data through
-// ONE in-place shared-memory buffer per channel (loads of a pass complete at a
-// barrier before any thread overwrites), so a length-1024 transform costs two
-// shared-memory round trips (16 x 16 x 4) instead of a read+write per pass.
+// A real length-2N series is transformed as the complex length-N series
+// z[n] = x[2n] + i x[2n+1] plus an O(N) split; only the N+1 non-redundant
+// frequencies exist. Per channel, TPC threads hold the data in registers: each
+// radix-R pass loads its R inputs, applies the inter-pass twiddles, runs the
+// R-point DFT in registers and scatters the outputs autosorted through ONE
+// in-place shared-memory buffer per channel (all loads of a pass complete at a
+// barrier before any thread overwrites).
 //
-//  r2c: pass 1 reads z[n] = (x[2n], x[2n+1]) straight from the SOTI row with
-//       16-byte loads (only n < N/2 is non-zero: the zero padding prunes half
-//       the first-pass inputs), the split X_k = f(Z_k, Z_{N-k}) runs on pairs
-//       (k, N-k) and stores frequency-major with CPB consecutive channels per
-//       frequency.
-//  c2r: the pre-split builds Z from pairs (X_k, X_{N-k}) loaded
-//       frequency-major; the last pass stores x[2p], x[2p+1] straight into the
-//       SOTI row (only p < N/2 survives the unpad) through the epilogue.
-//
-// Shared-memory index p is padded to p + p/16 so the stride-R scatter of the
-// first pass is bank-conflict free. Twiddles W_N^e = lo[e % 32] * hi[e / 32]
-// come from two small shared tables.
+// The split between the complex transform and the real spectrum pairs
+// frequency k with N-k. Both live in the SAME thread when butterflies j and
+// NB-j of the last (R2C) / first (C2R) pass are processed together (butterfly
+// j holds positions j + q NB, whose partners N - j - q NB are positions of
+// butterfly NB - j). So:
+//  r2c: pass 1 reads z straight from the SOTI row with 16-byte loads (the
+//       zero-padded half, q >= R/2, is never loaded); the last pass runs on
+//       butterfly pairs and computes X_k, X_{N-k} in registers, storing
+//       frequency-major — no shared-memory split pass.
+//  c2r: the first pass loads X_k, X_{N-k} pairs frequency-major, forms
+//       Z_k, Z_{N-k} in registers and runs the pair of butterflies; the last
+//       pass stores x[2p], x[2p+1] straight into the SOTI row (only p < N/2
+//       survives the unpad) through the Gamma^-1 / alpha R v epilogue.
+// A length-1024 transform is three passes (16,16,4 / 4,16,16) and two
+// shared-memory round trips. Threads are interleaved over channels
+// (channel = tid % CPB) so every global access is CPB contiguous complex
+// values per frequency / 8 consecutive 16-byte words per row. Shared index p
+// is padded to p + p/16 (conflict-free stride-R scatter); twiddles
+// W^e = lo[e % 32] * hi[e / 32] come from two small shared tables, higher
+// powers by multiplication.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,26 +42,27 @@ namespace fast {
 template <int... Rs>
 struct Radices {};
 
-// Plans: (TPC threads per channel, CPB channels per CTA, radices in pass order).
+// Plans: TPC threads per channel, default CPB channels per CTA, pass radices
+// for R2C (small radix last: it runs on butterfly pairs) and C2R (small first).
 template <int N>
 struct FastPlan;
-template <> struct FastPlan<64>   { static constexpr int TPC = 8,   CPB = 32; using R = Radices<8, 8>; };
-template <> struct FastPlan<128>  { static constexpr int TPC = 16,  CPB = 16; using R = Radices<8, 16>; };
-template <> struct FastPlan<256>  { static constexpr int TPC = 16,  CPB = 16; using R = Radices<16, 16>; };
-template <> struct FastPlan<500>  { static constexpr int TPC = 64,  CPB = 4;  using R = Radices<4, 5, 5, 5>; };
-template <> struct FastPlan<512>  { static constexpr int TPC = 64,  CPB = 4;  using R = Radices<8, 8, 8>; };
-template <> struct FastPlan<1000> { static constexpr int TPC = 128, CPB = 2;  using R = Radices<8, 5, 5, 5>; };
-template <> struct FastPlan<1024> { static constexpr int TPC = 64,  CPB = 4;  using R = Radices<16, 16, 4>; };
-template <> struct FastPlan<2000> { static constexpr int TPC = 128, CPB = 2;  using R = Radices<16, 5, 5, 5>; };
-template <> struct FastPlan<2048> { static constexpr int TPC = 128, CPB = 2;  using R = Radices<16, 16, 8>; };
-template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  using R = Radices<16, 16, 16>; };
+template <> struct FastPlan<64>   { static constexpr int TPC = 8,   CPB = 32; using R2C = Radices<16, 4>;        using C2R = Radices<4, 16>; };
+template <> struct FastPlan<128>  { static constexpr int TPC = 16,  CPB = 16; using R2C = Radices<8, 4, 4>;      using C2R = Radices<4, 4, 8>; };
+template <> struct FastPlan<256>  { static constexpr int TPC = 16,  CPB = 16; using R2C = Radices<16, 4, 4>;     using C2R = Radices<4, 4, 16>; };
+template <> struct FastPlan<500>  { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<4, 5, 5, 5>;   using C2R = Radices<5, 5, 5, 4>; };
+template <> struct FastPlan<512>  { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<16, 8, 4>;     using C2R = Radices<4, 8, 16>; };
+template <> struct FastPlan<1000> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<8, 5, 5, 5>;   using C2R = Radices<5, 5, 5, 8>; };
+template <> struct FastPlan<1024> { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<16, 16, 4>;    using C2R = Radices<4, 16, 16>; };
+template <> struct FastPlan<2000> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 5, 5, 5>;  using C2R = Radices<5, 5, 5, 16>; };
+template <> struct FastPlan<2048> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 8, 4, 4>;  using C2R = Radices<4, 4, 8, 16>; };
+template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  using R2C = Radices<16, 16, 4, 4>; using C2R = Radices<4, 4, 16, 16>; };
 
 // Register budget: aim for 768 resident threads per SM (<= 85 registers).
 template <int N, int CPB>
 constexpr int kMinBlocks = (768 / (FastPlan<N>::TPC * CPB)) > 0 ? (768 / (FastPlan<N>::TPC * CPB)) : 1;
 
 __host__ __device__ constexpr int pad_idx(int p) { return p + (p >> 4); }
-__host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }  // room for X_N in c2r
+__host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }
 constexpr int kTwLo = 32;
 
 template <int N>
@@ -79,7 +89,7 @@ __device__ __forceinline__ void dft(double2* v) {
     else if constexpr (R == 5) dft5<SIGN>(v);
     else if constexpr (R == 8) dft8<SIGN>(v);
     else if constexpr (R == 16) {
-        // 16 = 4 x 4: columns, twiddle W_16^{q r}, rows, transpose.
+        // 16 = 4 x 4: columns, twiddle W_16^{r k}, rows, transpose.
         double2 a[4][4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -89,7 +99,6 @@ __device__ __forceinline__ void dft(double2* v) {
         }
         constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
         constexpr double c2 = 0.70710678118654752440;
-        // a[r][k] *= W_16^{r k}, W_16 = exp(SIGN 2 pi i / 16)
 #pragma unroll
         for (int r = 1; r < 4; ++r)
 #pragma unroll
@@ -117,13 +126,11 @@ __device__ __forceinline__ void dft(double2* v) {
     }
 }
 
-// Inputs of butterfly j of a radix-R pass, already twiddled: v[q] = s[j + q N/R] * W^{k q N/(NS R)}.
+// Butterfly j of a radix-R pass: v[q] = s[j + q N/R] * W^{k q N/(NS R)}, k = j % NS.
+// One table lookup; the powers q = 2..R-1 are products of lower powers.
 template <int N, int R, int NS, int SIGN>
 __device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2* lo, const double2* hi) {
     if constexpr (NS > 1) {
-        // One table lookup per butterfly; the powers W^{k q step}, q = 2..R-1, are
-        // products of lower powers (depth log2 R, error a few ulp) instead of
-        // 2 (R-1) shared-memory loads.
         const int k = j % NS;
         constexpr int step = N / (NS * R);
         double2 w[R];
@@ -138,8 +145,8 @@ __device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2*
 // One in-place radix-R pass over the channel buffer `s` (smem, padded).
 template <int N, int TPC, int R, int NS, int SIGN>
 __device__ __forceinline__ void pass_smem(double2* s, int tc, const double2* lo, const double2* hi) {
-    constexpr int NB = N / R;                 // butterflies
-    constexpr int BF = (NB + TPC - 1) / TPC;  // per thread
+    constexpr int NB = N / R;
+    constexpr int BF = (NB + TPC - 1) / TPC;
     double2 v[BF][R];
 #pragma unroll
     for (int b = 0; b < BF; ++b) {
@@ -165,32 +172,24 @@ __device__ __forceinline__ void pass_smem(double2* s, int tc, const double2* lo,
     __syncthreads();
 }
 
-// Remaining passes after the first (forward direction: all in smem).
-template <int N, int TPC, int NS, int SIGN>
-__device__ __forceinline__ void passes_rest(double2*, int, const double2*, const double2*, Radices<>) {}
-
-template <int N, int TPC, int NS, int SIGN, int R, int... Rest>
-__device__ __forceinline__ void passes_rest(double2* s, int tc, const double2* lo, const double2* hi,
-                                            Radices<R, Rest...>) {
-    pass_smem<N, TPC, R, NS, SIGN>(s, tc, lo, hi);
-    passes_rest<N, TPC, NS * R, SIGN>(s, tc, lo, hi, Radices<Rest...>{});
-}
-
+// ---- compile-time radix-list helpers -----------------------------------------
 template <int R, int... Rest>
-__device__ constexpr int first_radix(Radices<R, Rest...>) { return R; }
+__host__ __device__ constexpr int first_radix(Radices<R, Rest...>) { return R; }
 template <int R, int... Rest>
-__device__ constexpr Radices<Rest...> tail(Radices<R, Rest...>) { return {}; }
+__host__ __device__ constexpr Radices<Rest...> tail(Radices<R, Rest...>) { return {}; }
+template <int R>
+__host__ __device__ constexpr int last_radix(Radices<R>) { return R; }
+template <int R, int R2, int... Rest>
+__host__ __device__ constexpr int last_radix(Radices<R, R2, Rest...>) { return last_radix(Radices<R2, Rest...>{}); }
+// product of all radices but the last (the NS of the last pass)
+template <int R>
+__host__ __device__ constexpr int ns_of_last(Radices<R>) { return 1; }
+template <int R, int R2, int... Rest>
+__host__ __device__ constexpr int ns_of_last(Radices<R, R2, Rest...>) { return R * ns_of_last(Radices<R2, Rest...>{}); }
 
-// All passes but the last (inverse direction; the last pass stores to global).
-template <int N, int TPC, int NS, int SIGN, int R>
-__device__ constexpr int last_ns(Radices<R>) { return NS; }
-
-template <int... Rs>
-struct Count { static constexpr int value = sizeof...(Rs); };
-
+// Apply every pass of the list but the last, starting at NS.
 template <int N, int TPC, int NS, int SIGN, int R>
 __device__ __forceinline__ void passes_but_last(double2*, int, const double2*, const double2*, Radices<R>) {}
-
 template <int N, int TPC, int NS, int SIGN, int R, int R2, int... Rest>
 __device__ __forceinline__ void passes_but_last(double2* s, int tc, const double2* lo, const double2* hi,
                                                 Radices<R, R2, Rest...>) {
@@ -198,23 +197,28 @@ __device__ __forceinline__ void passes_but_last(double2* s, int tc, const double
     passes_but_last<N, TPC, NS * R, SIGN>(s, tc, lo, hi, Radices<R2, Rest...>{});
 }
 
-template <int NS, int R>
-__device__ constexpr int ns_before_last(Radices<R>) { return NS; }
-template <int NS, int R, int R2, int... Rest>
-__device__ constexpr int ns_before_last(Radices<R, R2, Rest...>) {
-    return ns_before_last<NS * R>(Radices<R2, Rest...>{});
-}
-template <int R>
-__device__ constexpr int last_radix(Radices<R>) { return R; }
-template <int R, int R2, int... Rest>
-__device__ constexpr int last_radix(Radices<R, R2, Rest...>) { return last_radix(Radices<R2, Rest...>{}); }
-
-// Shared twiddle tables for W_n (lo: W^0..31, hi: W^{32 h}) loaded once per CTA.
 __device__ __forceinline__ void load_tables(double2* lo, double2* hi, int hi_count, const double2* g_lo,
                                             const double2* g_hi) {
     for (int i = threadIdx.x; i < kTwLo; i += blockDim.x) lo[i] = g_lo[i];
     for (int i = threadIdx.x; i < hi_count; i += blockDim.x) hi[i] = g_hi[i];
 }
+
+// X_k from Z_k and Z_{N-k}, w = W_{2N}^k:
+//   X_k = 1/2 (Z_k + conj Z_{N-k}) - i/2 w (Z_k - conj Z_{N-k})
+__device__ __forceinline__ double2 split_x(double2 zk, double2 zn, double2 w) {
+    const double2 a = cadd(zk, cconj(zn));
+    const double2 wb = cmul(w, csub(zk, cconj(zn)));
+    return make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
+}
+// Z_k from X_k and X_{N-k}, w = W_{2N}^k:
+//   Z_k = (1/2N) [ (X_k + conj X_{N-k}) + i conj(w) (X_k - conj X_{N-k}) ]
+__device__ __forceinline__ double2 presplit_z(double2 xk, double2 xn, double2 w, double inv_len) {
+    const double2 e = cadd(xk, cconj(xn));
+    const double2 o = cmul(csub(xk, cconj(xn)), cconj(w));
+    return make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
+}
+// W_{2N}^{N-k} = -conj(W_{2N}^k)
+__device__ __forceinline__ double2 partner_w(double2 w) { return make_double2(-w.x, w.y); }
 
 // ---------------------------------------------------------------------------
 // r2c: SOTI rows (time contiguous) -> frequency-major out[k*out_fs + c]
@@ -224,25 +228,26 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
     k_r2c_fast(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
                int channels, FastTables tabs) {
     using P = FastPlan<N>;
+    using RL = typename P::R2C;
     constexpr int TPC = P::TPC, CS = chan_stride(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
     double2* hi = lo + kTwLo;
-    double2* plo = hi + HI;   // post twiddles W_{2N}
+    double2* plo = hi + HI;  // W_{2N} tables
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
-    const int b = threadIdx.x / TPC;
-    const int tc = threadIdx.x - b * TPC;
+    const int b = threadIdx.x % CPB;
+    const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
     const bool live = c < channels;
     double2* s = sm + b * CS;
     __syncthreads();
 
-    // ---- first pass straight from global: z[n] = (x[2n], x[2n+1]); z[n] = 0 for n >= N/2
+    // ---- pass 1 from global: z[n] = (x[2n], x[2n+1]); n = j + q NB < N/2 iff q < R/2
     {
-        constexpr int R = first_radix(typename P::R{});
+        constexpr int R = first_radix(RL{});
         constexpr int NB = N / R;
         constexpr int BF = (NB + TPC - 1) / TPC;
         const double2* row = reinterpret_cast<const double2*>(in + (long long)c * in_cs);
@@ -251,12 +256,9 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
         for (int bf = 0; bf < BF; ++bf) {
             const int j = tc + bf * TPC;
             if (NB % TPC == 0 || j < NB) {
-                // n = j + q NB < N/2 iff q < R/2: the zero-padded half is never loaded
 #pragma unroll
-                for (int q = 0; q < R; ++q) {
-                    const int n = j + q * NB;
-                    v[bf][q] = (q < R / 2 && live) ? __ldg(row + n) : make_double2(0.0, 0.0);
-                }
+                for (int q = 0; q < R; ++q)
+                    v[bf][q] = (q < R / 2 && live) ? __ldg(row + j + q * NB) : make_double2(0.0, 0.0);
                 dft<R, -1>(v[bf]);
             }
         }
@@ -269,33 +271,67 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
             }
         }
         __syncthreads();
-        passes_rest<N, TPC, R, -1>(s, tc, lo, hi, tail(typename P::R{}));
     }
+    // ---- middle passes
+    passes_but_last<N, TPC, first_radix(RL{}), -1>(s, tc, lo, hi, tail(RL{}));
 
-    // ---- split: X_k = 1/2 (Z_k + conj Z_{N-k}) - i/2 W_{2N}^k (Z_k - conj Z_{N-k}), pairs (k, N-k)
-    constexpr int NPAIR = N / 2 + 1;  // k = 0..N/2
-    for (int u = threadIdx.x; u < NPAIR * CPB; u += blockDim.x) {
-        const int k = u / CPB;
-        const int bb = u - k * CPB;
-        const int cc = blockIdx.x * CPB + bb;
-        if (cc >= channels) continue;
-        const double2* z = sm + bb * CS;
-        const double2 zk = z[pad_idx(k == 0 ? 0 : k)];
-        const double2 zn = z[pad_idx(k == 0 ? 0 : N - k)];
-        // X_k  (one table lookup per pair: W_{2N}^{N-k} = -conj(W_{2N}^k))
-        const double2 w = tw_lookup<-1>(plo, phi, k);
-        {
-            const double2 a = cadd(zk, cconj(zn));
-            const double2 wb = cmul(w, csub(zk, cconj(zn)));
-            out[(long long)k * out_fs + cc] = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
+    // ---- last pass on butterfly pairs (j, NB-j) + split in registers
+    constexpr int R = last_radix(RL{});
+    constexpr int NS = ns_of_last(RL{});
+    constexpr int NB = N / R;  // == NS
+    constexpr int NU = NB / 2;
+    constexpr int UF = (NU + TPC - 1) / TPC;
+    if (!live) return;  // no barrier follows
+    double2* orow = out + c;
+#pragma unroll
+    for (int uf = 0; uf < UF; ++uf) {
+        const int u = tc + uf * TPC;
+        if (NU % TPC != 0 && u >= NU) break;
+        const int ja = u == 0 ? 0 : u;
+        const int jb = u == 0 ? NB / 2 : NB - u;
+        double2 va[R], vb[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            va[q] = s[pad_idx(ja + q * NB)];
+            vb[q] = s[pad_idx(jb + q * NB)];
         }
-        // X_{N-k} (k=0 gives X_N; k = N/2 is its own partner)
-        if (k < N / 2) {
-            const int kk = N - k;
-            const double2 a = cadd(zn, cconj(zk));
-            const double2 wn = make_double2(-w.x, w.y);
-            const double2 wb = cmul(wn, csub(zn, cconj(zk)));
-            out[(long long)kk * out_fs + cc] = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
+        twiddle_inputs<N, R, NS, -1>(va, ja, lo, hi);
+        twiddle_inputs<N, R, NS, -1>(vb, jb, lo, hi);
+        dft<R, -1>(va);
+        dft<R, -1>(vb);
+        if (u != 0) {
+            // position ja + q NB pairs with jb + (R-1-q) NB
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int k = ja + q * NB;
+                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 zk = va[q], zn = vb[R - 1 - q];
+                orow[(long long)k * out_fs] = split_x(zk, zn, w);
+                orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+            }
+        } else {
+            // butterfly 0: positions q NB pair with ((R - q) % R) NB; q = 0 gives X_0 and X_N
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int qp = (R - q) % R;
+                if (q > qp && q != 0) continue;
+                const int k = q * NB;
+                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 zk = va[q], zn = va[qp];
+                orow[(long long)k * out_fs] = split_x(zk, zn, w);
+                if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+            }
+            // butterfly NB/2: positions NB/2 + q NB pair with index R-1-q
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int qp = R - 1 - q;
+                if (q > qp) continue;
+                const int k = NB / 2 + q * NB;
+                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 zk = vb[q], zn = vb[qp];
+                orow[(long long)k * out_fs] = split_x(zk, zn, w);
+                if (q != qp) orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+            }
         }
     }
 }
@@ -308,6 +344,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
     k_c2r_fast(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
     using P = FastPlan<N>;
+    using RL = typename P::C2R;
     constexpr int TPC = P::TPC, CS = chan_stride(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
@@ -317,48 +354,86 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
-    __syncthreads();
-
-    // ---- pre-split: Z_k = (1/2N)[(X_k + conj X_{N-k}) + i conj(W_{2N}^k)(X_k - conj X_{N-k})]
-    constexpr int NPAIR = N / 2 + 1;
-    constexpr double inv_len = 0.5 / N;
-    for (int u = threadIdx.x; u < NPAIR * CPB; u += blockDim.x) {
-        const int k = u / CPB;
-        const int bb = u - k * CPB;
-        const int cc = blockIdx.x * CPB + bb;
-        double2* z = sm + bb * CS;
-        double2 xk = make_double2(0.0, 0.0), xn = xk;
-        if (cc < channels) {
-            xk = __ldg(in + (long long)k * in_fs + cc);
-            xn = __ldg(in + (long long)(N - k) * in_fs + cc);
-        }
-        const double2 w = tw_lookup<-1>(plo, phi, k);  // W_{2N}^{N-k} = -conj(W_{2N}^k)
-        {
-            const double2 e = cadd(xk, cconj(xn));
-            const double2 o = cmul(csub(xk, cconj(xn)), cconj(w));
-            z[pad_idx(k == 0 ? 0 : k)] = make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
-        }
-        if (k > 0 && k < N / 2) {
-            const int kk = N - k;
-            const double2 e = cadd(xn, cconj(xk));
-            const double2 o = cmul(csub(xn, cconj(xk)), make_double2(-w.x, -w.y));
-            z[pad_idx(kk)] = make_double2(inv_len * (e.x - o.y), inv_len * (e.y + o.x));
-        }
-    }
-    __syncthreads();
-
-    const int b = threadIdx.x / TPC;
-    const int tc = threadIdx.x - b * TPC;
+    const int b = threadIdx.x % CPB;
+    const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
+    const bool live = c < channels;
     double2* s = sm + b * CS;
-    passes_but_last<N, TPC, 1, +1>(s, tc, lo, hi, typename P::R{});
+    __syncthreads();
 
-    // ---- last pass: outputs p = j + q N/R; keep p < N/2 (t = 2p, 2p+1 < N)
-    constexpr int R = last_radix(typename P::R{});
-    constexpr int NS = ns_before_last<1>(typename P::R{});
+    // ---- pass 1 on butterfly pairs: Z from (X_k, X_{N-k}) loaded frequency-major
+    {
+        constexpr int R = first_radix(RL{});
+        constexpr int NB = N / R;
+        constexpr int NU = NB / 2;
+        constexpr int UF = (NU + TPC - 1) / TPC;
+        constexpr double inv_len = 0.5 / N;
+        const double2* col = in + c;
+        auto X = [&](int k) { return live ? __ldg(col + (long long)k * in_fs) : make_double2(0.0, 0.0); };
+        double2 va[UF][R], vb[UF][R];
+#pragma unroll
+        for (int uf = 0; uf < UF; ++uf) {
+            const int u = tc + uf * TPC;
+            if (NU % TPC != 0 && u >= NU) continue;
+            const int ja = u == 0 ? 0 : u;
+            const int jb = u == 0 ? NB / 2 : NB - u;
+            if (u != 0) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int k = ja + q * NB;  // partner N - k = jb + (R-1-q) NB
+                    const double2 xk = X(k), xn = X(N - k);
+                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    va[uf][q] = presplit_z(xk, xn, w, inv_len);
+                    vb[uf][R - 1 - q] = presplit_z(xn, xk, partner_w(w), inv_len);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int qp = (R - q) % R;
+                    if (q > qp && q != 0) continue;
+                    const int k = q * NB;
+                    const double2 xk = X(k), xn = X(N - k);  // q = 0: X_0 and X_N
+                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    va[uf][q] = presplit_z(xk, xn, w, inv_len);
+                    if (q != qp) va[uf][qp] = presplit_z(xn, xk, partner_w(w), inv_len);
+                }
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int qp = R - 1 - q;
+                    if (q > qp) continue;
+                    const int k = NB / 2 + q * NB;
+                    const double2 xk = X(k), xn = X(N - k);
+                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    vb[uf][q] = presplit_z(xk, xn, w, inv_len);
+                    if (q != qp) vb[uf][qp] = presplit_z(xn, xk, partner_w(w), inv_len);
+                }
+            }
+            dft<R, +1>(va[uf]);
+            dft<R, +1>(vb[uf]);
+        }
+#pragma unroll
+        for (int uf = 0; uf < UF; ++uf) {
+            const int u = tc + uf * TPC;
+            if (NU % TPC != 0 && u >= NU) continue;
+            const int ja = u == 0 ? 0 : u;
+            const int jb = u == 0 ? NB / 2 : NB - u;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                s[pad_idx(ja * R + q)] = va[uf][q];
+                s[pad_idx(jb * R + q)] = vb[uf][q];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- middle passes
+    passes_but_last<N, TPC, first_radix(RL{}), +1>(s, tc, lo, hi, tail(RL{}));
+
+    // ---- last pass: outputs p = j + q NB; keep p < N/2 (t = 2p, 2p+1 < N)
+    constexpr int R = last_radix(RL{});
+    constexpr int NS = ns_of_last(RL{});
     constexpr int NB = N / R;
     constexpr int BF = (NB + TPC - 1) / TPC;
-    if (c >= channels) return;
+    if (!live) return;
     double* orow = out + (long long)c * out_cs;
     const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
 #pragma unroll

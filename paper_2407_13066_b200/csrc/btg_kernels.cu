@@ -223,12 +223,13 @@ __global__ void __launch_bounds__(kThreads) k_c2r(const double2* __restrict__ in
 template <typename TF, int VEC, int ROWS, int UNR>
 __global__ void __launch_bounds__(kThreads, 2)
     k_gemv_fwd(const TF* __restrict__ F, const double2* __restrict__ x, double2* __restrict__ y,
-               int nd, int nm) {
+               int nd, int ld, int j0, int nm, int accumulate) {
+    // columns [j0, j0 + nm) of rows of length ld; accumulate: y += (column-chunk pipelines)
     const int f = blockIdx.y;
     const int i0 = blockIdx.x * ROWS;
     const int nr = min(ROWS, nd - i0);
-    const TF* fb = F + ((size_t)f * nd + i0) * nm;
-    const double2* xf = x + (size_t)f * nm;
+    const TF* fb = F + ((size_t)f * nd + i0) * ld + j0;
+    const double2* xf = x + (size_t)f * ld + j0;
     const uint64_t pol = evict_first_policy();
 
     double ar[ROWS], ai[ROWS];
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
                 if (r < nr) {
-                    FLoad<TF, VEC>::load(fb + (size_t)r * nm + j + u * kStep, pol, fv[u][r]);
+                    FLoad<TF, VEC>::load(fb + (size_t)r * ld + j + u * kStep, pol, fv[u][r]);
                 } else {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) fv[u][r][v] = make_double2(0.0, 0.0);
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const double2 xv = __ldg(xf + j + v);
 #pragma unroll
                 for (int r = 0; r < ROWS; ++r)
-                    if (r < nr) cmac(ar[r], ai[r], FLoad<TF, VEC>::scalar(fb + (size_t)r * nm + j + v), xv);
+                    if (r < nr) cmac(ar[r], ai[r], FLoad<TF, VEC>::scalar(fb + (size_t)r * ld + j + v), xv);
             }
         }
     }
@@ -298,7 +299,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             sr += red[w][threadIdx.x][0];
             si += red[w][threadIdx.x][1];
         }
-        y[(size_t)f * nd + i0 + threadIdx.x] = make_double2(sr, si);
+        double2* yo = y + (size_t)f * nd + i0 + threadIdx.x;
+        if (accumulate) {
+            const double2 prev = *yo;
+            sr = prev.x + sr;
+            si = prev.y + si;
+        }
+        *yo = make_double2(sr, si);
     }
 }
 
@@ -309,7 +316,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 template <typename TF, int VEC, int JPT, int UNR, bool kSmemD>
 __global__ void __launch_bounds__(kThreads, 2)
     k_gemv_adj(const TF* __restrict__ F, const double2* __restrict__ x, double2* __restrict__ y,
-               int nd, int nm) {
+               int nd, int ld, int j0, int nm) {
+    // columns [j0, j0 + nm) of rows of length ld (column-chunk pipelines)
     extern __shared__ double2 sd[];
     const int f = blockIdx.y;
     const double2* xf = x + (size_t)f * nd;
@@ -318,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();
     }
     const double2* dsrc = kSmemD ? sd : xf;
-    const TF* ff = F + (size_t)f * nd * nm;
+    const TF* ff = F + (size_t)f * nd * ld + j0;
+    double2* yf = y + (size_t)f * ld + j0;
     const uint64_t pol = evict_first_policy();
     constexpr int kStep = kThreads * VEC;
     const int jb = blockIdx.x * (kStep * JPT) + threadIdx.x * VEC;
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int u = 0; u < UNR; ++u)
 #pragma unroll
                 for (int q = 0; q < JPT; ++q)
-                    FLoad<TF, VEC>::load(ff + (size_t)(i + u) * nm + jb + q * kStep, pol, fv[u][q]);
+                    FLoad<TF, VEC>::load(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const double2 w = dsrc[i + u];
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int q = 0; q < JPT; ++q) {
                 double2 fv[VEC];
-                FLoad<TF, VEC>::load(ff + (size_t)i * nm + jb + q * kStep, pol, fv);
+                FLoad<TF, VEC>::load(ff + (size_t)i * ld + jb + q * kStep, pol, fv);
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[v], w);
             }
@@ -361,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int q = 0; q < JPT; ++q)
 #pragma unroll
             for (int v = 0; v < VEC; ++v)
-                y[(size_t)f * nm + jb + q * kStep + v] = make_double2(ar[q][v], ai[q][v]);
+                yf[jb + q * kStep + v] = make_double2(ar[q][v], ai[q][v]);
     } else {
         for (int i = 0; i < nd; ++i) {
             const double2 w = dsrc[i];
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int v = 0; v < VEC; ++v) {
                     const int j = jb + q * kStep + v;
                     if (j < nm)
-                        cmac_conj(ar[q][v], ai[q][v], FLoad<TF, VEC>::scalar(ff + (size_t)i * nm + j), w);
+                        cmac_conj(ar[q][v], ai[q][v], FLoad<TF, VEC>::scalar(ff + (size_t)i * ld + j), w);
                 }
         }
 #pragma unroll
@@ -379,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
                 const int j = jb + q * kStep + v;
-                if (j < nm) y[(size_t)f * nm + j] = make_double2(ar[q][v], ai[q][v]);
+                if (j < nm) yf[j] = make_double2(ar[q][v], ai[q][v]);
             }
     }
 }
@@ -469,26 +478,32 @@ cudaError_t launch_c2r(const double2* in, long long in_fs, long long in_cs, doub
 }
 
 template <typename TF>
-cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
-                            cudaStream_t stream) {
+cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
+                                  int nj, bool accumulate, cudaStream_t stream) {
     constexpr int kRows = 8;
     dim3 grid((nd + kRows - 1) / kRows, nf);
     if constexpr (sizeof(TF) == 8) {
-        if ((nm & 1) == 0) {
-            k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+        if ((nm & 1) == 0 && (j0 & 1) == 0) {
+            k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj, accumulate);
             return cudaGetLastError();
         }
     }
-    k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+    k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj, accumulate);
     return cudaGetLastError();
 }
 
+template <typename TF>
+cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream) {
+    return launch_gemv_fwd_range(F, x, y, nf, nd, nm, 0, nm, false, stream);
+}
+
 template <typename TF, int VEC>
-cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0, int nj,
                            cudaStream_t stream) {
     constexpr int kJpt = 2;
     constexpr int kUnr = 8;
-    dim3 grid((nm + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nf);
+    dim3 grid((nj + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nf);
     const size_t smem = (size_t)nd * sizeof(double2);
     // Default: read d-hat_f through the read-only path (a warp-uniform broadcast
     // that hits L1), so a CTA starts streaming F-hat without a fill + barrier.
@@ -497,30 +512,38 @@ cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, in
         auto kern = k_gemv_adj<TF, VEC, kJpt, kUnr, true>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, kThreads, smem, stream>>>(F, x, y, nd, nm);
+        kern<<<grid, kThreads, smem, stream>>>(F, x, y, nd, nm, j0, nj);
     } else {
-        k_gemv_adj<TF, VEC, kJpt, kUnr, false><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm);
+        k_gemv_adj<TF, VEC, kJpt, kUnr, false><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj);
     }
     return cudaGetLastError();
 }
 
 template <typename TF>
-cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
-                            cudaStream_t stream) {
+cudaError_t launch_gemv_adj_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
+                                  int nj, cudaStream_t stream) {
     if constexpr (sizeof(TF) == 8) {
-        if ((nm & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, stream);
+        if ((nm & 1) == 0 && (j0 & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, j0, nj, stream);
     }
-    return launch_adj_vec<TF, 1>(F, x, y, nf, nd, nm, stream);
+    return launch_adj_vec<TF, 1>(F, x, y, nf, nd, nm, j0, nj, stream);
 }
 
-template cudaError_t launch_gemv_fwd<double2>(const double2*, const double2*, double2*, int, int,
-                                              int, cudaStream_t);
-template cudaError_t launch_gemv_fwd<float2>(const float2*, const double2*, double2*, int, int,
-                                             int, cudaStream_t);
-template cudaError_t launch_gemv_adj<double2>(const double2*, const double2*, double2*, int, int,
-                                              int, cudaStream_t);
-template cudaError_t launch_gemv_adj<float2>(const float2*, const double2*, double2*, int, int,
-                                             int, cudaStream_t);
+template <typename TF>
+cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
+                            cudaStream_t stream) {
+    return launch_gemv_adj_range(F, x, y, nf, nd, nm, 0, nm, stream);
+}
+
+#define BTG_INST_GEMV(TF)                                                                                       \
+    template cudaError_t launch_gemv_fwd<TF>(const TF*, const double2*, double2*, int, int, int, cudaStream_t); \
+    template cudaError_t launch_gemv_adj<TF>(const TF*, const double2*, double2*, int, int, int, cudaStream_t); \
+    template cudaError_t launch_gemv_fwd_range<TF>(const TF*, const double2*, double2*, int, int, int, int, int, \
+                                                   bool, cudaStream_t);                                         \
+    template cudaError_t launch_gemv_adj_range<TF>(const TF*, const double2*, double2*, int, int, int, int, int, \
+                                                   cudaStream_t);
+BTG_INST_GEMV(double2)
+BTG_INST_GEMV(float2)
+#undef BTG_INST_GEMV
 
 cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                 uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream) {

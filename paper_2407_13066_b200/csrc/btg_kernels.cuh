@@ -68,6 +68,15 @@ template <typename TF>
 cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
                             cudaStream_t stream);
 
+// Column-chunk variants for host<->device pipelines: columns [j0, j0 + nj)
+// only; the forward one adds into y when `accumulate` (chunks in a fixed order).
+template <typename TF>
+cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
+                                  int nj, bool accumulate, cudaStream_t stream);
+template <typename TF>
+cudaError_t launch_gemv_adj_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
+                                  int nj, cudaStream_t stream);
+
 // Adjoint: y[f][j] = sum_i conj(F[f][i][j]) x[f][i].
 template <typename TF>
 cudaError_t launch_gemv_adj(const TF* F, const double2* x, double2* y, int nf, int nd, int nm,
