@@ -42,7 +42,8 @@ typedef enum {
     BTG_ECUDA = 4,   /* CUDA runtime failure                                                       */
     BTG_ENOMEM = 5,  /* device allocation failed                                                   */
     BTG_EGRID = 6,   /* unserviceable processor grid -> btoep::GridError (distributed.cpp:147-152) */
-    BTG_ESOLVER = 7  /* CG lost positive definiteness -> btoep::SolverError (inverse.cpp:124-136) */
+    BTG_ESOLVER = 7, /* CG lost positive definiteness -> btoep::SolverError (inverse.cpp:124-136) */
+    BTG_EFORMAT = 8  /* malformed / inconsistent file -> btoep::FormatError (io.cpp)              */
 } btg_status;
 
 typedef enum { BTG_F64 = 64, BTG_F32 = 32 } btg_precision;
@@ -164,6 +165,31 @@ btg_status btg_get_dims(btg_op op, size_t* num_sensors, size_t* num_sources,
  * 2*N_t-frequency layout (freq_blocks, block_operator.hpp:40) with the upper
  * half rebuilt by conjugate symmetry; full = 0: the N_t+1 stored frequencies. */
 btg_status btg_export_spectrum(btg_op op, double* out, int full);
+
+/* One stored frequency block f <= N_t (N_d x N_m complex128) to host memory. */
+btg_status btg_export_spectrum_block(btg_op op, size_t f, double* out);
+
+/* ---- reference file formats (proj/include/btoep/io.hpp, src/io.cpp) ---------
+ * "BTOP" operator files (64-byte header; time domain: N_t real64 TOSI blocks;
+ * frequency domain: 2 N_t complex128 blocks) and "BTVC" vector files. */
+typedef struct {
+    int ordering;        /* 0 TOSI, 1 SOTI */
+    int domain;          /* 0 time, 1 frequency */
+    uint64_t num_sensors, num_sources, num_steps;
+    int complex_scalar;
+} btg_file_header;
+
+btg_status btg_peek_operator(const char* path, btg_file_header* out);       /* io::peek_operator */
+/* Build the device operator from a file (streamed; never whole in host memory):
+ * time domain -> setup (Alg. 1); frequency domain -> the N_t+1 stored blocks. */
+btg_status btg_load_operator(const char* path, int precision, int device, btg_op* out);
+/* io::write_operator(SpectralP2O): the reference's 2 N_t frequency-domain file. */
+btg_status btg_save_operator(btg_op op, const char* path);
+btg_status btg_write_vector(const char* path, const double* values, size_t spatial_dim,
+                            size_t num_steps, int ordering);                 /* io::write_vector */
+/* io::read_vector; values == NULL queries the dimensions only. */
+btg_status btg_read_vector(const char* path, double* values, size_t capacity, size_t* spatial_dim,
+                           size_t* num_steps, int* ordering);
 
 /* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */
 btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes);

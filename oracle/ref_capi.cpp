@@ -29,6 +29,7 @@
 #include "btoep/distributed.hpp"
 #include "btoep/errors.hpp"
 #include "btoep/inverse.hpp"
+#include "btoep/io.hpp"
 #include "btoep/rng.hpp"
 #include "btoep/verify.hpp"
 
@@ -184,6 +185,33 @@ int ref_objective(void* h, const double* m, const double* d_obs, double alpha, i
         reg.alpha = alpha;
         *value = objective_eval(op, make_soti(m, op.num_sources, op.num_steps),
                                 make_soti(d_obs, op.num_sensors, op.num_steps), reg);
+    });
+}
+
+// ---- file formats (io.cpp) -----------------------------------------------------
+int ref_write_compact(const char* path, const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt) {
+    return guarded([&] { io::write_operator(path, make_compact(blocks, nd, nm, nt)); });
+}
+
+int ref_save_spectral(void* h, const char* path) {
+    return guarded([&] { io::write_operator(path, *static_cast<SpectralP2O*>(h)); });
+}
+
+void* ref_load_spectral(const char* path) {
+    SpectralP2O* op = nullptr;
+    const int rc = guarded([&] { op = new SpectralP2O(io::read_spectral_operator(path)); });
+    return rc == 0 ? op : nullptr;
+}
+
+int ref_write_vector(const char* path, const double* v, std::size_t dim, std::size_t nt) {
+    return guarded([&] { io::write_vector(path, make_soti(v, dim, nt)); });
+}
+
+int ref_read_vector(const char* path, double* out, std::size_t capacity) {
+    return guarded([&] {
+        const SpaceTimeVector v = with_ordering(io::read_vector(path), Ordering::SOTI);
+        if (v.values.size() > capacity) throw DimensionError("capacity");
+        std::memcpy(out, v.values.data(), v.values.size() * sizeof(double));
     });
 }
 

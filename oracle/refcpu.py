@@ -53,6 +53,12 @@ def lib():
         L.ref_distributed_hessian.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double,
                                               ctypes.c_int, ctypes.c_int]
         L.ref_verify.argtypes = [ctypes.c_uint64, ctypes.c_char_p, _size_t, ctypes.POINTER(ctypes.c_int)]
+        L.ref_write_compact.argtypes = [ctypes.c_char_p, _c_double_p, _size_t, _size_t, _size_t]
+        L.ref_save_spectral.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.ref_load_spectral.argtypes = [ctypes.c_char_p]
+        L.ref_load_spectral.restype = ctypes.c_void_p
+        L.ref_write_vector.argtypes = [ctypes.c_char_p, _c_double_p, _size_t, _size_t]
+        L.ref_read_vector.argtypes = [ctypes.c_char_p, _c_double_p, _size_t]
         L.ref_cg_solve.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int,
                                    ctypes.c_double, _size_t, ctypes.c_int, _c_double_p]
         L.ref_objective.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int,
@@ -151,6 +157,42 @@ class RefSpectralOperator:
         v = np.zeros(1)
         _check(lib().ref_objective(self._h, _p(_f64(m)), _p(_f64(d_obs)), float(alpha), int(reg_kind), _p(v)))
         return float(v[0])
+
+
+def write_compact(path, blocks) -> None:
+    """io::write_operator(CompactP2O) (io.cpp:97-111)."""
+    blocks = _f64(blocks)
+    nt, nd, nm = blocks.shape
+    _check(lib().ref_write_compact(str(path).encode(), _p(blocks), nd, nm, nt))
+
+
+def save_spectral(op: "RefSpectralOperator", path) -> None:
+    """io::write_operator(SpectralP2O) (io.cpp:113-130)."""
+    _check(lib().ref_save_spectral(op._h, str(path).encode()))
+
+
+def load_spectral_spectrum(path, nd, nm, nt) -> np.ndarray:
+    """io::read_spectral_operator (io.cpp:179-205) -> its freq_blocks."""
+    h = lib().ref_load_spectral(str(path).encode())
+    if not h:
+        raise RefError(lib().ref_last_error().decode())
+    out = np.empty((2 * nt, nd, nm), dtype=np.complex128)
+    try:
+        _check(lib().ref_spectrum(ctypes.c_void_p(h), out.ctypes.data_as(_c_double_p)))
+    finally:
+        lib().ref_destroy(ctypes.c_void_p(h))
+    return out
+
+
+def write_vector(path, v) -> None:
+    v = _f64(v)
+    _check(lib().ref_write_vector(str(path).encode(), _p(v), v.shape[0], v.shape[1]))
+
+
+def read_vector(path, shape) -> np.ndarray:
+    out = np.empty(shape)
+    _check(lib().ref_read_vector(str(path).encode(), _p(out), out.size))
+    return out
 
 
 def naive_forward(blocks, m) -> np.ndarray:

@@ -11,7 +11,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
 
-BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER = range(8)
+BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER, BTG_EFORMAT = range(9)
 BTG_F64, BTG_F32 = 64, 32
 BTG_DEVICE_PTRS = 0x1
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's stream 0)
@@ -43,6 +43,12 @@ EXPORTED = (
     "btg_fill_uniform_3d",
     "btg_cg_solve",
     "btg_objective",
+    "btg_export_spectrum_block",
+    "btg_peek_operator",
+    "btg_load_operator",
+    "btg_save_operator",
+    "btg_write_vector",
+    "btg_read_vector",
 )
 
 
@@ -64,6 +70,23 @@ class GridError(ValueError):
 
 class SolverError(RuntimeError):
     """btoep::SolverError (errors.hpp:33-35); the reference binds it to RuntimeError."""
+
+
+class FormatError(ValueError):
+    """btoep::FormatError (errors.hpp:23-25)."""
+
+
+class FileHeader(ctypes.Structure):
+    """btg_file_header == io::OperatorHeader (io.hpp:21-28)."""
+
+    _fields_ = [
+        ("ordering", ctypes.c_int),
+        ("domain", ctypes.c_int),
+        ("num_sensors", ctypes.c_uint64),
+        ("num_sources", ctypes.c_uint64),
+        ("num_steps", ctypes.c_uint64),
+        ("complex_scalar", ctypes.c_int),
+    ]
 
 
 class CgResult(ctypes.Structure):
@@ -160,6 +183,13 @@ def load():
                                ctypes.c_double, _sz, ctypes.c_int, ctypes.c_uint, ctypes.POINTER(CgResult)]
     L.btg_objective.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_double, ctypes.c_int, ctypes.c_uint,
                                 ctypes.POINTER(ctypes.c_double)]
+    L.btg_export_spectrum_block.argtypes = [_vp, _sz, _dp]
+    L.btg_peek_operator.argtypes = [ctypes.c_char_p, ctypes.POINTER(FileHeader)]
+    L.btg_load_operator.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.btg_save_operator.argtypes = [_vp, ctypes.c_char_p]
+    L.btg_write_vector.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, ctypes.c_int]
+    L.btg_read_vector.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_sz),
+                                  ctypes.POINTER(ctypes.c_int)]
     for name in EXPORTED:
         if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
             getattr(L, name).restype = ctypes.c_int
@@ -182,4 +212,6 @@ def check(status: int) -> None:
         raise MemoryError(msg)
     if status == BTG_ESOLVER:
         raise SolverError(msg)
+    if status == BTG_EFORMAT:
+        raise FormatError(msg)
     raise Error(msg)

@@ -99,7 +99,7 @@ struct btg_op_s {
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
-    cudaEvent_t ev[9] = {};              // kHostChunks + 1 chunk / ordering events
+    cudaEvent_t ev[17] = {};              // kHostChunks + 1 chunk / ordering events
     cudaStream_t stream = nullptr;
 
     // workspace (grown on demand)
@@ -356,7 +356,7 @@ btg_status stage_small(btg_op op, const double* src, size_t n, double*& buf, siz
 // overlaps chunk c+1's adjoint GEMV + C2R. Forward partial products are added
 // chunk by chunk in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
-constexpr size_t kHostChunks = 8;
+constexpr size_t kHostChunks = 16;
 
 bool host_pipelined(btg_op op, size_t nrhs) {
     static const bool off = std::getenv("BTG_NO_HOST_PIPELINE") != nullptr;
@@ -772,6 +772,35 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
     return finish_host(op, hv, hvd, hv_len, flags);
 }
 
+// Internal hooks for btg_io.cu (C++ linkage, not part of the C ABI).
+btg_status btg_internal_fail(btg_status s, const char* msg) { return fail(s, "%s", msg); }
+
+btg_status btg_internal_upload_spectrum_block(btg_op op, size_t f, const double* block) {
+    if (!op || !block || f > op->nt) return fail(BTG_EARG, "bad spectrum block upload");
+    std::lock_guard<std::mutex> lock(op->mu);
+    DeviceGuard g(op->device);
+    const size_t blk = op->nd * op->nm;
+    if (op->precision == BTG_F64) {
+        BTG_CUDA(cudaMemcpy(static_cast<double2*>(op->F) + f * blk, block, blk * sizeof(double2),
+                            cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float2> tmp(blk);
+        for (size_t k = 0; k < blk; ++k)
+            tmp[k] = make_float2(static_cast<float>(block[2 * k]), static_cast<float>(block[2 * k + 1]));
+        BTG_CUDA(cudaMemcpy(static_cast<float2*>(op->F) + f * blk, tmp.data(), blk * sizeof(float2),
+                            cudaMemcpyHostToDevice));
+    }
+    return BTG_OK;
+}
+
+btg_status btg_internal_mark_ready(btg_op op) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    std::fill(op->rows_ready.begin(), op->rows_ready.end(), 1);
+    op->rows_ready_count = op->nd;
+    return BTG_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Device-resident CG (inverse.cpp:105-156) and objective (inverse.cpp:93-103)
 // ---------------------------------------------------------------------------
@@ -1076,6 +1105,29 @@ btg_status btg_export_spectrum(btg_op op, double* out, int full) {
         } else {
             const std::complex<double>* src = half.data() + (len - f) * blk;
             for (size_t c = 0; c < blk; ++c) dst[f * blk + c] = std::conj(src[c]);
+        }
+    }
+    return BTG_OK;
+}
+
+btg_status btg_export_spectrum_block(btg_op op, size_t f, double* out) {
+    if (!op || !out) return fail(BTG_EARG, "null argument");
+    std::lock_guard<std::mutex> lock(op->mu);
+    BTG_TRY(check_ready(op));
+    if (f > op->nt) return fail(BTG_EDIM, "frequency %zu outside the stored 0..%zu", f, op->nt);
+    DeviceGuard g(op->device);
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    const size_t blk = op->nd * op->nm;
+    if (op->precision == BTG_F64) {
+        BTG_CUDA(cudaMemcpy(out, static_cast<double2*>(op->F) + f * blk, blk * sizeof(double2),
+                            cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<float2> tmp(blk);
+        BTG_CUDA(cudaMemcpy(tmp.data(), static_cast<float2*>(op->F) + f * blk, blk * sizeof(float2),
+                            cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < blk; ++k) {
+            out[2 * k] = tmp[k].x;
+            out[2 * k + 1] = tmp[k].y;
         }
     }
     return BTG_OK;
