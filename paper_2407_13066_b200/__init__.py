@@ -3,25 +3,33 @@ the reference ``btoep`` library, behind its own operator API.
 
 Compute runs only in ``libbtg.so`` (hand-written sm_100a CUDA, C ABI in
 ``include/btg.h``); this package is the host-side mirror of the reference's
-Python surface plus the multi-GPU grid (``distributed``).
+Python surface (operator, solver, files) plus the multi-GPU grid
+(``distributed``).
 """
 
-from ._lib import DimensionError, Error, GridError, OrderingError, SolverError  # noqa: F401
+from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
+from .io import load_operator, peek_operator, read_vector, save_operator, write_vector  # noqa: F401
 from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
 from .solver import cg_solve, cg_solve_op, objective_eval  # noqa: F401
 
 __all__ = [
     "DimensionError",
     "Error",
+    "FormatError",
     "GridError",
     "OrderingError",
     "SolverError",
-    "cg_solve",
-    "cg_solve_op",
-    "objective_eval",
     "HessianOperator",
     "SpectralOperator",
+    "cg_solve",
+    "cg_solve_op",
     "create",
     "fill_uniform",
+    "load_operator",
+    "objective_eval",
+    "peek_operator",
+    "read_vector",
+    "save_operator",
     "setup",
+    "write_vector",
 ]

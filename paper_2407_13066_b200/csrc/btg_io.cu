@@ -20,10 +20,12 @@
 
 #include "../../include/btg.h"
 
-// shared with btg_capi.cu
+// shared with btg_capi.cu (defined there, C linkage, not declared in btg.h)
+extern "C" {
 btg_status btg_internal_fail(btg_status s, const char* msg);
 btg_status btg_internal_upload_spectrum_block(btg_op op, size_t f, const double* block_c128);
 btg_status btg_internal_mark_ready(btg_op op);
+}
 
 namespace {
 
