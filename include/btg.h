@@ -183,6 +183,12 @@ btg_status btg_peek_operator(const char* path, btg_file_header* out);       /* i
 /* Build the device operator from a file (streamed; never whole in host memory):
  * time domain -> setup (Alg. 1); frequency domain -> the N_t+1 stored blocks. */
 btg_status btg_load_operator(const char* path, int precision, int device, btg_op* out);
+/* The shard of one grid cell: sensors [i0, i1) x sources [j0, j1) of a file.
+ * Time domain -> setup of the rectangle (partition_operator(CompactP2O),
+ * distributed.cpp:179-196); frequency domain -> the rectangle of every stored
+ * block, no re-setup (partition_operator(SpectralP2O), distributed.cpp:198-218). */
+btg_status btg_load_operator_rect(const char* path, size_t i0, size_t i1, size_t j0, size_t j1,
+                                  int precision, int device, btg_op* out);
 /* io::write_operator(SpectralP2O): the reference's 2 N_t frequency-domain file. */
 btg_status btg_save_operator(btg_op op, const char* path);
 btg_status btg_write_vector(const char* path, const double* values, size_t spatial_dim,

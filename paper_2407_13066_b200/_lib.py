@@ -49,6 +49,7 @@ EXPORTED = (
     "btg_save_operator",
     "btg_write_vector",
     "btg_read_vector",
+    "btg_load_operator_rect",
 )
 
 
@@ -187,6 +188,8 @@ def load():
     L.btg_peek_operator.argtypes = [ctypes.c_char_p, ctypes.POINTER(FileHeader)]
     L.btg_load_operator.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
     L.btg_save_operator.argtypes = [_vp, ctypes.c_char_p]
+    L.btg_load_operator_rect.argtypes = [ctypes.c_char_p, _sz, _sz, _sz, _sz, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(_vp)]
     L.btg_write_vector.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, ctypes.c_int]
     L.btg_read_vector.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_sz),
                                   ctypes.POINTER(ctypes.c_int)]

@@ -102,6 +102,14 @@ btg_status btg_peek_operator(const char* path, btg_file_header* out) {
 }
 
 btg_status btg_load_operator(const char* path, int precision, int device, btg_op* out) {
+    btg_file_header h{};
+    btg_status s = btg_peek_operator(path, &h);
+    if (s != BTG_OK) return s;
+    return btg_load_operator_rect(path, 0, h.num_sensors, 0, h.num_sources, precision, device, out);
+}
+
+btg_status btg_load_operator_rect(const char* path, size_t i0, size_t i1, size_t j0, size_t j1, int precision,
+                                  int device, btg_op* out) {
     if (!out) return btg_internal_fail(BTG_EARG, "null output handle");
     *out = nullptr;
     btg_file_header h{};
@@ -110,7 +118,10 @@ btg_status btg_load_operator(const char* path, int precision, int device, btg_op
     if (h.ordering != 0) return ferr(std::string("'") + path + "': operators must be TOSI-ordered");
     if ((h.domain == 0) == (h.complex_scalar != 0))
         return ferr(std::string("'") + path + "': domain and scalar kind disagree");
-    const size_t nd = h.num_sensors, nm = h.num_sources, nt = h.num_steps;
+    const size_t ND = h.num_sensors, NM = h.num_sources, nt = h.num_steps;
+    if (i0 >= i1 || i1 > ND || j0 >= j1 || j1 > NM)
+        return btg_internal_fail(BTG_EDIM, "load_operator_rect: rectangle outside the operator");
+    const size_t nd = i1 - i0, nm = j1 - j0;
     btg_op op = nullptr;
     s = btg_create(nd, nm, nt, precision, device, &op);
     if (s != BTG_OK) return s;
@@ -124,28 +135,34 @@ btg_status btg_load_operator(const char* path, int precision, int device, btg_op
         btg_destroy(op);
         return st;
     };
+    // Rows of the rectangle are contiguous (nm values) in every stored block.
     if (h.domain == 0) {
-        // time domain: sensor-row slabs (N_t, rows, N_m) through btg_setup_rows
+        // time domain: sensor-row slabs (N_t, rows, nm) through btg_setup_rows
+        // (the reference's partition_operator(CompactP2O), distributed.cpp:179-196)
         const size_t row_bytes = nt * nm * sizeof(double);
         const size_t rows = std::max<size_t>(1, std::min<size_t>(nd, (size_t(1) << 30) / row_bytes));
         std::vector<double> slab(rows * nt * nm);
-        for (size_t i0 = 0; i0 < nd; i0 += rows) {
-            const size_t r = std::min(rows, nd - i0);
-            for (size_t k = 0; k < nt; ++k) {
-                const uint64_t off = kHeader + ((uint64_t)k * nd + i0) * nm * sizeof(double);
-                if (!read_at(fh.f, off, slab.data() + k * r * nm, r * nm * sizeof(double)))
-                    return bail(ferr(std::string("'") + path + "': file truncated"));
-            }
-            s = btg_setup_rows(op, slab.data(), i0, i0 + r, 0u);
+        for (size_t r0 = 0; r0 < nd; r0 += rows) {
+            const size_t r = std::min(rows, nd - r0);
+            for (size_t k = 0; k < nt; ++k)
+                for (size_t i = 0; i < r; ++i) {
+                    const uint64_t off = kHeader + (((uint64_t)k * ND + i0 + r0 + i) * NM + j0) * sizeof(double);
+                    if (!read_at(fh.f, off, slab.data() + (k * r + i) * nm, nm * sizeof(double)))
+                        return bail(ferr(std::string("'") + path + "': file truncated"));
+                }
+            s = btg_setup_rows(op, slab.data(), r0, r0 + r, 0u);
             if (s != BTG_OK) return bail(s);
         }
     } else {
-        // frequency domain: blocks f = 0..N_t of the stored 2 N_t
+        // frequency domain: blocks f = 0..N_t of the stored 2 N_t, rectangle only
+        // (partition_operator(SpectralP2O), distributed.cpp:198-218: no re-setup)
         std::vector<double> blk(2 * nd * nm);
         for (size_t f = 0; f <= nt; ++f) {
-            const uint64_t off = kHeader + (uint64_t)f * nd * nm * 16;
-            if (!read_at(fh.f, off, blk.data(), blk.size() * sizeof(double)))
-                return bail(ferr(std::string("'") + path + "': file truncated"));
+            for (size_t i = 0; i < nd; ++i) {
+                const uint64_t off = kHeader + (((uint64_t)f * ND + i0 + i) * NM + j0) * 16;
+                if (!read_at(fh.f, off, blk.data() + 2 * i * nm, nm * 16))
+                    return bail(ferr(std::string("'") + path + "': file truncated"));
+            }
             s = btg_internal_upload_spectrum_block(op, f, blk.data());
             if (s != BTG_OK) return bail(s);
         }

@@ -187,6 +187,27 @@ class GridEngine:
             op = setup(local, precision=precision, device=device)
         return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"))
 
+    @classmethod
+    def from_file(cls, path, grid: Tuple[int, int], precision: int = 64):
+        """Every rank loads only its rectangle of a reference operator file:
+        time domain -> local setup; frequency domain -> the stored blocks of the
+        rectangle, no re-setup (partition_operator(SpectralP2O),
+        distributed.cpp:198-218)."""
+        import torch
+        import torch.distributed as dist
+
+        from .io import load_operator_rect, peek_operator
+
+        h = peek_operator(path)
+        nd, nm, nt = int(h["num_sensors"]), int(h["num_sources"]), int(h["num_steps"])
+        shard = partition_bounds(nd, nm, *grid)[dist.get_rank()]
+        device = torch.cuda.current_device()
+        op = None
+        if not shard.empty:
+            op = load_operator_rect(path, (shard.sensor_begin, shard.sensor_end),
+                                    (shard.source_begin, shard.source_end), precision, device)
+        return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"))
+
     # -- helpers -------------------------------------------------------------------
     def _rank_of(self, i: int, j: int) -> int:
         return i * self.cols + j

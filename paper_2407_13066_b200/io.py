@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import check
 from .operator import SpectralOperator
 
-__all__ = ["peek_operator", "load_operator", "save_operator", "read_vector", "write_vector"]
+__all__ = ["peek_operator", "load_operator", "load_operator_rect", "save_operator", "read_vector", "write_vector"]
 
 
 def peek_operator(path) -> dict:
@@ -39,6 +39,17 @@ def load_operator(path, precision: int = 64, device: int = 0) -> SpectralOperato
     prec = ctypes.c_int()
     check(_lib.load().btg_get_dims(h, ctypes.byref(nd), ctypes.byref(nm), ctypes.byref(nt), ctypes.byref(prec)))
     return SpectralOperator(h.value, nd.value, nm.value, nt.value, prec.value, int(device))
+
+
+def load_operator_rect(path, sensors, sources, precision: int = 64, device: int = 0) -> SpectralOperator:
+    """One grid cell's shard, sensors [i0, i1) x sources [j0, j1), of an operator
+    file (btg_load_operator_rect): setup of the rectangle for a time-domain file,
+    the rectangle of the stored blocks (no re-setup) for a frequency-domain one."""
+    (i0, i1), (j0, j1) = sensors, sources
+    h = ctypes.c_void_p()
+    check(_lib.load().btg_load_operator_rect(str(Path(path)).encode(), i0, i1, j0, j1, int(precision), int(device),
+                                             ctypes.byref(h)))
+    return SpectralOperator(h.value, i1 - i0, j1 - j0, peek_operator(path)["num_steps"], int(precision), int(device))
 
 
 def save_operator(op: SpectralOperator, path) -> None:
