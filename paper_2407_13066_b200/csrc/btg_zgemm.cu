@@ -59,7 +59,7 @@ __device__ __forceinline__ double embed_b(double2 b, int s, int t) {
 // ---------------------------------------------------------------------------
 constexpr int kFwdKc = 16;                  // complex j per stage
 constexpr int kFwdAStride = 2 * kFwdKc + 2;  // doubles per A row (padded)
-constexpr int kFwdBStride = kFwdKc + 1;      // complex per B row (padded)
+constexpr int kFwdBStride = kFwdKc + 2;      // complex per B row (padded: the 4 r x 2 k fragment words hit 8 distinct banks)
 constexpr size_t kFwdStageDoubles = (size_t)kTileM * kFwdAStride + 2 * (size_t)kTileR * kFwdBStride;
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------------------
 constexpr int kAdjKc = 16;                      // complex i per stage
 constexpr int kAdjAStride = kTileM + 4;         // complex per A row (i), padded
-constexpr int kAdjBStride = kAdjKc + 1;         // complex per B row (r)
+constexpr int kAdjBStride = kAdjKc + 2;         // complex per B row (r)
 constexpr size_t kAdjStageDoubles = 2 * ((size_t)kAdjKc * kAdjAStride + (size_t)kTileR * kAdjBStride);
 
 __global__ void __launch_bounds__(kThreads, 1)
