@@ -425,14 +425,23 @@ def run_ours(args):
 
         L = _lib.load()
 
+        e_ops = {"F": [], "F*": [], "H": []}
+
         def e2e_step():
+            t0 = time.perf_counter()
             _lib.check(L.btg_forward(op._h, hm_np.ctypes.data, hm_np.size, out_d.ctypes.data, out_d.size, nrhs, 0))
+            t1 = time.perf_counter()
             _lib.check(L.btg_adjoint(op._h, hd_np.ctypes.data, hd_np.size, out_m.ctypes.data, out_m.size, nrhs, 0))
+            t2 = time.perf_counter()
             _lib.check(L.btg_hessian(op._h, hm_np.ctypes.data, hm_np.size, out_h.ctypes.data, out_h.size, nrhs,
                                      hg.ctypes.data, 1, 0.0, 0, 0))
+            t3 = time.perf_counter()
+            for k, dt in zip(("F", "F*", "H"), (t1 - t0, t2 - t1, t3 - t2)):
+                e_ops[k].append(dt * 1e3)
 
         op._bind_stream(None)
         e2e_step()
+        e_ops = {"F": [], "F*": [], "H": []}
         e_steps = max(3, min(args.steps, 10))
         torch.cuda.synchronize(device)
         t = time.perf_counter()
@@ -444,6 +453,7 @@ def run_ours(args):
                "h2d_bytes_per_step": 8 * nrhs * (2 * nm * nt + nd * nt) + 8 * nd,
                "d2h_bytes_per_step": 8 * nrhs * (nd * nt + 2 * nm * nt),
                "ms_per_step": e_s * 1e3, "steps": e_steps,
+               "ops_ms": {k: statistics.median(v) for k, v in e_ops.items()},
                "path": "btg_forward/btg_adjoint/btg_hessian with pinned host buffers (H2D + compute + D2H per call)"}
 
     cpu = None

@@ -363,9 +363,34 @@ bool host_pipelined(btg_op op, size_t nrhs) {
     return !off && nrhs == 1 && op->legacy_gemv && op->nm >= 4096;
 }
 
-size_t chunk_cols(btg_op op) {
-    const size_t per = (op->nm + kHostChunks - 1) / kHostChunks;
-    return (per + 511) / 512 * 512;
+// Column chunks (multiples of 512 columns): N_m/8-wide, except a geometric
+// ramp of small chunks where the pipeline fills (first H2D) or drains (last
+// D2H) — the only transfers left exposed. At most kHostChunks chunks.
+std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
+    const size_t big = std::max<size_t>(512, (op->nm / 8 + 511) / 512 * 512);
+    std::vector<size_t> sizes;
+    size_t left = op->nm;
+    for (size_t w = 1024; w < big && left > 0; w *= 2) {
+        sizes.push_back(std::min(w, left));
+        left -= sizes.back();
+    }
+    while (left > 0) {
+        sizes.push_back(std::min(big, left));
+        left -= sizes.back();
+    }
+    while (sizes.size() > kHostChunks) {
+        const size_t x = sizes.back();
+        sizes.pop_back();
+        sizes.back() += x;
+    }
+    if (!ramp_first) std::reverse(sizes.begin(), sizes.end());
+    std::vector<std::pair<size_t, size_t>> plan;
+    size_t j0 = 0;
+    for (size_t w : sizes) {
+        plan.emplace_back(j0, w);
+        j0 += w;
+    }
+    return plan;
 }
 
 btg_status ensure_copy_stream(btg_op op) {
@@ -401,12 +426,13 @@ void count_apply(btg_op op) {
 btg_status host_forward_stage(btg_op op, const double* m_host) {
     BTG_TRY(ensure_spectral(op, 1));
     BTG_TRY(ensure_copy_stream(op));
-    const size_t nt = op->nt, cols = chunk_cols(op);
+    const size_t nt = op->nt;
+    const auto plan = chunk_plan(op, true);
     BTG_CUDA(cudaEventRecord(op->ev[kHostChunks], op->stream));  // hin free of earlier readers
     BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[kHostChunks], 0));
     StageClock clk(op, &op->counters.apply);
-    for (size_t c = 0, j0 = 0; j0 < op->nm; ++c, j0 += cols) {
-        const size_t nc = std::min(cols, op->nm - j0);
+    for (size_t c = 0; c < plan.size(); ++c) {
+        const auto [j0, nc] = plan[c];
         BTG_CUDA(cudaMemcpyAsync(op->hin + j0 * nt, m_host + j0 * nt, nc * nt * sizeof(double),
                                  cudaMemcpyHostToDevice, op->copy_stream));
         BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
@@ -421,23 +447,22 @@ btg_status host_forward_stage(btg_op op, const double* m_host) {
 // d-hat spectrum in op->wa -> m (host) through chunked adjoint GEMV + C2R + D2H.
 btg_status host_adjoint_stage(btg_op op, double* m_host, const btg::C2REpilogue& epi) {
     BTG_TRY(ensure_copy_stream(op));
-    const size_t nt = op->nt, cols = chunk_cols(op);
-    size_t nchunks = 0;
+    const size_t nt = op->nt;
+    const auto plan = chunk_plan(op, false);
     {
         StageClock clk(op, &op->counters.apply);
-        for (size_t c = 0, j0 = 0; j0 < op->nm; ++c, j0 += cols) {
-            const size_t nc = std::min(cols, op->nm - j0);
+        for (size_t c = 0; c < plan.size(); ++c) {
+            const auto [j0, nc] = plan[c];
             BTG_TRY(gemv_range(op, true, op->wa, op->wb, j0, nc, false));
             btg::C2REpilogue e = epi;
             if (e.v) e.v = epi.v + j0 * nt;
             BTG_TRY(run_c2r_vec(op, op->wb + j0, nc, op->hout + j0 * nt, e, op->nm));
             BTG_CUDA(cudaEventRecord(op->ev[c], op->stream));
-            nchunks = c + 1;
         }
     }
     count_apply(op);
-    for (size_t c = 0, j0 = 0; c < nchunks; ++c, j0 += cols) {
-        const size_t nc = std::min(cols, op->nm - j0);
+    for (size_t c = 0; c < plan.size(); ++c) {
+        const auto [j0, nc] = plan[c];
         BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[c], 0));
         BTG_CUDA(cudaMemcpyAsync(m_host + j0 * nt, op->hout + j0 * nt, nc * nt * sizeof(double),
                                  cudaMemcpyDeviceToHost, op->copy_stream));
