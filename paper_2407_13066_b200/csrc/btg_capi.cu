@@ -1200,7 +1200,7 @@ btg_status btg_fill_uniform(double* out, size_t n, uint64_t seed, uint64_t offse
 
 btg_status btg_fill_uniform_3d(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                uint64_t stride_a, uint64_t stride_b, double lo, double hi, void* stream) {
-    if (!out && na * nb * nc) return fail(BTG_EARG, "null output pointer");
+    if (!out && na * nb * nc != 0) return fail(BTG_EARG, "null output pointer");
     BTG_CUDA(btg::launch_fill_uniform(out, na, nb, nc, seed, offset, stride_a, stride_b, lo, hi,
                                       static_cast<cudaStream_t>(stream)));
     return BTG_OK;

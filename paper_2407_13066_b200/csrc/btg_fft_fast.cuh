@@ -59,7 +59,7 @@ template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  us
 
 // Register budget: aim for 768 resident threads per SM (<= 85 registers).
 template <int N, int CPB>
-constexpr int kMinBlocks = (768 / (FastPlan<N>::TPC * CPB)) > 0 ? (768 / (FastPlan<N>::TPC * CPB)) : 1;
+constexpr int kMinBlocks = (768 / (FastPlan<N>::TPC * CPB)) < 1 ? 1 : ((768 / (FastPlan<N>::TPC * CPB)) > 16 ? 16 : (768 / (FastPlan<N>::TPC * CPB)));
 
 __host__ __device__ constexpr int pad_idx(int p) { return p + (p >> 4); }
 __host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }
@@ -376,7 +376,6 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
             const int u = tc + uf * TPC;
             if (NU % TPC != 0 && u >= NU) continue;
             const int ja = u == 0 ? 0 : u;
-            const int jb = u == 0 ? NB / 2 : NB - u;
             if (u != 0) {
 #pragma unroll
                 for (int q = 0; q < R; ++q) {

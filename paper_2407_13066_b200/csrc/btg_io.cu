@@ -208,7 +208,7 @@ btg_status btg_save_operator(btg_op op, const char* path) {
 
 btg_status btg_write_vector(const char* path, const double* values, size_t spatial_dim, size_t num_steps,
                             int ordering) {
-    if (!path || (!values && spatial_dim * num_steps)) return btg_internal_fail(BTG_EARG, "null argument");
+    if (!path || (!values && spatial_dim * num_steps != 0)) return btg_internal_fail(BTG_EARG, "null argument");
     if (ordering != 0 && ordering != 1) return btg_internal_fail(BTG_EORDER, "ordering must be 0 (TOSI) or 1 (SOTI)");
     File fh;
     fh.f = std::fopen(path, "wb");
