@@ -48,6 +48,8 @@ CONFIGS = {
                label="profiling slice of configs[3]: 32 RHS, N_t=1024 N_d=128 N_m=4096"),
     "E8": dict(nt=4096, nd=256, nm=8192, nrhs=1,
                label="configs[4] per-GPU shard of the 1x8 grid: N_t=4096 N_d=256 N_m=65536/8 FP64 (F-hat 137 GB)"),
+    "L": dict(nt=10000, nd=100, nm=800, nrhs=1,
+              label="paper long horizon (PAPER.md:912-938): N_t=10000 N_d=100 N_m=800 FP64 (F-hat 12.8 GB)"),
     "E4f32": dict(nt=4096, nd=256, nm=16384, nrhs=1, precision=32,
                   label="configs[4] per-GPU shard of the 1x4 grid, FP32 F-hat: N_t=4096 N_d=256 N_m=65536/4"),
 }

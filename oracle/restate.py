@@ -221,8 +221,9 @@ def dense_block_operator_soti(blocks):
 
 def rel_max_diff(a, b) -> float:
     """tests/oracles.cpp:71-79."""
-    a = np.asarray(a, dtype=np.float64).ravel()
-    b = np.asarray(b, dtype=np.float64).ravel()
+    dt = np.complex128 if np.iscomplexobj(a) or np.iscomplexobj(b) else np.float64
+    a = np.asarray(a, dtype=dt).ravel()
+    b = np.asarray(b, dtype=dt).ravel()
     diff = np.max(np.abs(a - b)) if a.size else 0.0
     scale = max(np.max(np.abs(a)) if a.size else 0.0, np.max(np.abs(b)) if b.size else 0.0)
     return float(diff if scale == 0.0 else diff / scale)
@@ -230,8 +231,9 @@ def rel_max_diff(a, b) -> float:
 
 def rel_l2(got, want) -> float:
     """North-star parity metric: ||got - want||_2 / ||want||_2."""
-    got = np.asarray(got, dtype=np.float64).ravel()
-    want = np.asarray(want, dtype=np.float64).ravel()
+    dt = np.complex128 if np.iscomplexobj(got) or np.iscomplexobj(want) else np.float64
+    got = np.asarray(got, dtype=dt).ravel()
+    want = np.asarray(want, dtype=dt).ravel()
     den = np.linalg.norm(want)
     num = np.linalg.norm(got - want)
     return float(num if den == 0.0 else num / den)

@@ -76,6 +76,7 @@ std::vector<int> factorize(int n) {
 constexpr size_t kFftSmemBudget = 200 * 1024;      // per CTA
 constexpr size_t kFftSmemTarget = 100 * 1024;      // aim for 2 CTAs / SM
 constexpr size_t kHostStageBytes = 512ull << 20;   // host->device setup staging
+constexpr size_t kScratchCapBytes = 1ull << 30;    // global FFT scratch bound
 
 }  // namespace
 
@@ -90,6 +91,7 @@ struct btg_op_s {
     double2* d_tw = nullptr;
     double2* d_post = nullptr;
     double2* d_fast = nullptr;  // split twiddle tables of the compile-time-N FFTs
+    btg::FftScratch gscratch;   // global ping-pong buffers when N_t exceeds shared memory
     btg::FastTables fast{};
     bool fast_ok = false;
     bool no_dmma = false;      // BTG_DISABLE_DMMA: per-RHS GEMV streams instead of the ZGEMM
@@ -240,7 +242,8 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
                                           (int)channels, op->fast, op->stream));
     else
         BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)fs, 1,
-                                          (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream));
+                                          (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream,
+                                          op->gscratch));
     op->counters.launches++;
     op->counters.forward_fft.ops += fft_ops(channels, op->nt);
     op->counters.forward_fft.bytes += 8.0 * channels * op->nt + 16.0 * op->nf * channels;
@@ -256,7 +259,7 @@ btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* ou
                                           (int)channels, op->fast, epi, op->stream));
     else
         BTG_CUDA(btg::launch_c2r(in, (long long)fs, 1, out, (long long)op->nt, (int)channels,
-                                 (int)op->nt, op->plan, op->fft_batch, epi, op->stream));
+                                 (int)op->nt, op->plan, op->fft_batch, epi, op->stream, op->gscratch));
     op->counters.launches++;
     op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
     op->counters.inverse_fft.bytes += 16.0 * op->nf * channels + 8.0 * channels * op->nt;
@@ -562,10 +565,10 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
     const std::vector<int> fac = factorize((int)nt);
     if ((int)fac.size() > btg::kMaxFactors) return fail(BTG_EARG, "N_t=%zu has too many factors", nt);
     const int batch_vec = btg::fft_batch((int)nt, kFftSmemTarget, 4);
-    const int batch_max = btg::fft_batch((int)nt, kFftSmemBudget, 1);
-    if (batch_max < 1)
-        return fail(BTG_EDIM, "N_t=%zu exceeds the shared-memory FFT limit (%zu bytes per channel)", nt,
-                    btg::fft_smem_bytes((int)nt, 1));
+    // Horizons beyond the shared-memory two-buffer transform (N_t > ~6400) run
+    // the generic kernels on a bounded global scratch; lengths with a
+    // compile-time plan (8192, 10000) still take the register path for vectors.
+    const bool smem_fits = btg::fft_batch((int)nt, kFftSmemBudget, 1) >= 1;
 
     DeviceGuard g(device);
     btg_op op = new (std::nothrow) btg_op_s();
@@ -619,6 +622,18 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
     // Default: the register-load GEMV (7.4 TB/s at configs[1]); the TMA ring is
     // opt-in (BTG_GEMV_TMA=1): faster on a 6.7 GB operator, slower at 54 GB.
     op->legacy_gemv = std::getenv("BTG_GEMV_TMA") == nullptr;
+    if (!smem_fits) {
+        const size_t per_cta = btg::fft_smem_bytes((int)nt, 1);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const size_t cap = kScratchCapBytes / per_cta;
+        op->gscratch.ctas = (int)std::max<size_t>(1, std::min<size_t>(2 * (size_t)sms, cap));
+        e = cudaMalloc(&op->gscratch.buf, per_cta * op->gscratch.ctas);
+        if (e != cudaSuccess)
+            return cleanup_fail(fail(BTG_ENOMEM, "FFT scratch (%zu bytes): %s", per_cta * op->gscratch.ctas,
+                                     cudaGetErrorString(e)));
+        op->fft_batch = op->fft_batch_setup = 1;
+    }
     op->plan.n = (int)nt;
     op->plan.nfac = (int)fac.size();
     for (size_t i = 0; i < fac.size(); ++i) op->plan.fac[i] = fac[i];
@@ -651,10 +666,12 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
         const size_t off = i0 * op->nm + c_begin;
         if (op->precision == BTG_F64)
             e = btg::launch_r2c<double2>(src, 1, in_ts, static_cast<double2*>(op->F) + off, out_fs, 1,
-                                         (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream);
+                                         (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream,
+                                         op->gscratch);
         else
             e = btg::launch_r2c<float2>(src, 1, in_ts, static_cast<float2*>(op->F) + off, out_fs, 1,
-                                        (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream);
+                                        (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream,
+                                         op->gscratch);
         BTG_CUDA(e);
         op->counters.launches++;
         return BTG_OK;
@@ -1175,6 +1192,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->d_tw);
         cudaFree(op->d_post);
         cudaFree(op->d_fast);
+        cudaFree(op->gscratch.buf);
         cudaFree(op->wa);
         cudaFree(op->wb);
         cudaFree(op->wt);

@@ -56,6 +56,9 @@ template <> struct FastPlan<1024> { static constexpr int TPC = 64,  CPB = 4;  us
 template <> struct FastPlan<2000> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 5, 5, 5>;  using C2R = Radices<5, 5, 5, 16>; };
 template <> struct FastPlan<2048> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 8, 4, 4>;  using C2R = Radices<4, 4, 8, 16>; };
 template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  using R2C = Radices<16, 16, 4, 4>; using C2R = Radices<4, 4, 16, 16>; };
+// long horizons: the paper's N_t = 10000 runs and 2^13
+template <> struct FastPlan<8192>  { static constexpr int TPC = 512, CPB = 1;  using R2C = Radices<16, 16, 8, 4>;    using C2R = Radices<4, 8, 16, 16>; };
+template <> struct FastPlan<10000> { static constexpr int TPC = 625, CPB = 1;  using R2C = Radices<16, 5, 5, 5, 5>; using C2R = Radices<5, 5, 5, 5, 16>; };
 
 // Register budget: aim for 768 resident threads per SM (<= 85 registers).
 template <int N, int CPB>

@@ -26,6 +26,7 @@ namespace btg {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kFwdWarpMaxCols = 4096;  // forward GEMV rows up to this length: warp-per-row kernel
 
 // ---------------------------------------------------------------------------
 // streaming loads of F-hat
@@ -113,16 +114,20 @@ template <typename TOut>
 __global__ void __launch_bounds__(kThreads) k_r2c(const double* __restrict__ in, long long in_cs,
                                                   long long in_ts, TOut* __restrict__ out,
                                                   long long out_fs, long long out_cs, int channels,
-                                                  int nt, FftPlanDev plan, int batch) {
+                                                  int nt, FftPlanDev plan, int batch,
+                                                  double2* __restrict__ gwork) {
+    // gwork != nullptr: the ping-pong buffers live in a per-CTA global slice
+    // (horizons whose 2-buffer transform exceeds shared memory; setup only)
+    // and the CTAs loop over channel groups.
     extern __shared__ double2 smem[];
     const int n = plan.n;  // == nt
     const int cs = fft_channel_stride(n);
-    double2* buf_a = smem;
-    double2* buf_b = smem + (size_t)batch * cs;
-    const int c0 = blockIdx.x * batch;
-    const int nb = min(batch, channels - c0);
+    double2* buf_a = gwork ? gwork + (size_t)blockIdx.x * 2 * batch * cs : smem;
+    double2* buf_b = buf_a + (size_t)batch * cs;
     const int len = 2 * n;  // padded real length
     double* ad = reinterpret_cast<double*>(buf_a);
+    for (int c0 = blockIdx.x * batch; c0 < channels; c0 += gridDim.x * batch) {
+    const int nb = min(batch, channels - c0);
 
     // Load: z[n] = x[2n] + i x[2n+1] is the real sequence itself viewed as
     // interleaved complex, so sample t of channel b goes to double 2*cs*b + t.
@@ -154,6 +159,8 @@ __global__ void __launch_bounds__(kThreads) k_r2c(const double* __restrict__ in,
         const double2 x = make_double2(0.5 * (a.x + wb.y), 0.5 * (a.y - wb.x));
         out[(long long)k * out_fs + (long long)(c0 + b) * out_cs] = to_out<TOut>(x);
     }
+    __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -162,13 +169,14 @@ __global__ void __launch_bounds__(kThreads) k_r2c(const double* __restrict__ in,
 __global__ void __launch_bounds__(kThreads) k_c2r(const double2* __restrict__ in, long long in_fs,
                                                   long long in_cs, double* __restrict__ out,
                                                   long long out_cs, int channels, int nt,
-                                                  FftPlanDev plan, int batch, C2REpilogue epi) {
+                                                  FftPlanDev plan, int batch, C2REpilogue epi,
+                                                  double2* __restrict__ gwork) {
     extern __shared__ double2 smem[];
     const int n = plan.n;
     const int cs = fft_channel_stride(n);
-    double2* buf_a = smem;
-    double2* buf_b = smem + (size_t)batch * cs;
-    const int c0 = blockIdx.x * batch;
+    double2* buf_a = gwork ? gwork + (size_t)blockIdx.x * 2 * batch * cs : smem;
+    double2* buf_b = buf_a + (size_t)batch * cs;
+    for (int c0 = blockIdx.x * batch; c0 < channels; c0 += gridDim.x * batch) {
     const int nb = min(batch, channels - c0);
 
     for (int u = threadIdx.x; u < nb * (n + 1); u += blockDim.x) {
@@ -214,6 +222,8 @@ __global__ void __launch_bounds__(kThreads) k_c2r(const double2* __restrict__ in
             y += epi.alpha * r;
         }
         out[o] = y;
+    }
+    __syncthreads();
     }
 }
 
@@ -306,6 +316,82 @@ __global__ void __launch_bounds__(kThreads, 2)
             si = prev.y + si;
         }
         *yo = make_double2(sr, si);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7 forward, short rows (N_m up to a few thousand, e.g. the paper's N_t=10000,
+// N_m=800 runs): one warp = RPW consecutive rows of the flattened (f, i) row
+// space, lanes stride the columns, warp-shuffle reduction only — no CTA
+// barrier, so a short row costs no block-wide drain. Fixed order: deterministic.
+// ---------------------------------------------------------------------------
+template <typename TF, int VEC, int RPW, int UNR>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_gemv_fwd_warp(const TF* __restrict__ F, const double2* __restrict__ x, double2* __restrict__ y,
+                    long long rows, int nd, int ld, int j0, int nm, int accumulate) {
+    const int lane = threadIdx.x & 31;
+    const long long row0 = ((long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPW;
+    if (row0 >= rows) return;
+    const uint64_t pol = evict_first_policy();
+    const TF* fr[RPW];
+    const double2* xr[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const long long g = min(row0 + r, rows - 1);  // clamped rows are computed, not stored
+        fr[r] = F + g * ld + j0;
+        xr[r] = x + (g / nd) * ld + j0;
+    }
+    double ar[RPW], ai[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) ar[r] = ai[r] = 0.0;
+
+    constexpr int kStep = 32 * VEC;
+    int j = lane * VEC;
+    for (; j + (UNR - 1) * kStep + VEC <= nm; j += UNR * kStep) {
+        double2 fv[UNR][RPW][VEC], xv[UNR][RPW][VEC];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                FLoad<TF, VEC>::load(fr[r] + j + u * kStep, pol, fv[u][r]);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) xv[u][r][v] = __ldg(xr[r] + j + u * kStep + v);
+            }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int r = 0; r < RPW; ++r)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], fv[u][r][v], xv[u][r][v]);
+    }
+    for (; j < nm; j += kStep) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+            if (j + v < nm) {
+#pragma unroll
+                for (int r = 0; r < RPW; ++r)
+                    cmac(ar[r], ai[r], FLoad<TF, VEC>::scalar(fr[r] + j + v), __ldg(xr[r] + j + v));
+            }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
+            ai[r] += __shfl_xor_sync(0xffffffffu, ai[r], o);
+        }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        if (lane == r && row0 + r < rows) {
+            double2* yo = y + row0 + r;
+            double sr = ar[r], si = ai[r];
+            if (accumulate) {
+                const double2 prev = *yo;
+                sr = prev.x + sr;
+                si = prev.y + si;
+            }
+            *yo = make_double2(sr, si);
+        }
     }
 }
 
@@ -448,38 +534,62 @@ int fft_batch(int n, size_t smem_budget, int want) {
 template <typename TOut>
 cudaError_t launch_r2c(const double* in, long long in_cs, long long in_ts, TOut* out,
                        long long out_fs, long long out_cs, int channels, int nt,
-                       const FftPlanDev& plan, int batch, cudaStream_t stream) {
+                       const FftPlanDev& plan, int batch, cudaStream_t stream, const FftScratch& gs) {
     if (channels <= 0) return cudaSuccess;
-    const size_t smem = fft_smem_bytes(plan.n, batch);
+    const size_t smem = gs.buf ? 0 : fft_smem_bytes(plan.n, batch);
     cudaError_t e = set_smem(k_r2c<TOut>, smem);
     if (e != cudaSuccess) return e;
-    const int grid = (channels + batch - 1) / batch;
+    int grid = (channels + batch - 1) / batch;
+    if (gs.buf) grid = std::min(grid, gs.ctas);
     k_r2c<TOut><<<grid, kThreads, smem, stream>>>(in, in_cs, in_ts, out, out_fs, out_cs, channels,
-                                                  nt, plan, batch);
+                                                  nt, plan, batch, gs.buf);
     return cudaGetLastError();
 }
 
 template cudaError_t launch_r2c<double2>(const double*, long long, long long, double2*, long long,
-                                         long long, int, int, const FftPlanDev&, int, cudaStream_t);
+                                         long long, int, int, const FftPlanDev&, int, cudaStream_t,
+                                         const FftScratch&);
 template cudaError_t launch_r2c<float2>(const double*, long long, long long, float2*, long long,
-                                        long long, int, int, const FftPlanDev&, int, cudaStream_t);
+                                        long long, int, int, const FftPlanDev&, int, cudaStream_t,
+                                        const FftScratch&);
 
 cudaError_t launch_c2r(const double2* in, long long in_fs, long long in_cs, double* out,
                        long long out_cs, int channels, int nt, const FftPlanDev& plan, int batch,
-                       const C2REpilogue& epi, cudaStream_t stream) {
+                       const C2REpilogue& epi, cudaStream_t stream, const FftScratch& gs) {
     if (channels <= 0) return cudaSuccess;
-    const size_t smem = fft_smem_bytes(plan.n, batch);
+    const size_t smem = gs.buf ? 0 : fft_smem_bytes(plan.n, batch);
     cudaError_t e = set_smem(k_c2r, smem);
     if (e != cudaSuccess) return e;
-    const int grid = (channels + batch - 1) / batch;
+    int grid = (channels + batch - 1) / batch;
+    if (gs.buf) grid = std::min(grid, gs.ctas);
     k_c2r<<<grid, kThreads, smem, stream>>>(in, in_fs, in_cs, out, out_cs, channels, nt, plan,
-                                            batch, epi);
+                                            batch, epi, gs.buf);
     return cudaGetLastError();
 }
 
 template <typename TF>
 cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
                                   int nj, bool accumulate, cudaStream_t stream) {
+    static const int warp_max = [] {
+        const char* e = std::getenv("BTG_FWD_WARP_MAX");
+        return e ? std::atoi(e) : kFwdWarpMaxCols;
+    }();
+    if (nj <= warp_max) {
+        constexpr int kRpw = 4;
+        const long long rows = (long long)nf * nd;
+        const long long warps = (rows + kRpw - 1) / kRpw;
+        const unsigned grid = (unsigned)((warps + kThreads / 32 - 1) / (kThreads / 32));
+        if constexpr (sizeof(TF) == 8) {
+            if ((nm & 1) == 0 && (j0 & 1) == 0) {
+                k_gemv_fwd_warp<TF, 2, kRpw, 2><<<grid, kThreads, 0, stream>>>(F, x, y, rows, nd, nm, j0, nj,
+                                                                               accumulate);
+                return cudaGetLastError();
+            }
+        }
+        k_gemv_fwd_warp<TF, 1, kRpw, 4><<<grid, kThreads, 0, stream>>>(F, x, y, rows, nd, nm, j0, nj,
+                                                                       accumulate);
+        return cudaGetLastError();
+    }
     constexpr int kRows = 8;
     dim3 grid((nd + kRows - 1) / kRows, nf);
     if constexpr (sizeof(TF) == 8) {
@@ -632,7 +742,7 @@ cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long lon
     }
 }
 
-#define BTG_FAST_SIZES(X) X(64) X(128) X(256) X(500) X(512) X(1000) X(1024) X(2000) X(2048) X(4096)
+#define BTG_FAST_SIZES(X) X(64) X(128) X(256) X(500) X(512) X(1000) X(1024) X(2000) X(2048) X(4096) X(8192) X(10000)
 
 }  // namespace
 

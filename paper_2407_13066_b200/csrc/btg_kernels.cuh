@@ -48,20 +48,30 @@ __host__ __device__ inline int fft_channel_stride(int n) { return n + 1; }
 int fft_batch(int n, size_t smem_budget, int want);
 size_t fft_smem_bytes(int n, int batch);
 
+// Global-memory ping-pong buffers for horizons whose two-buffer transform does
+// not fit shared memory (generic path; setup and lengths without a fast plan):
+// `ctas` persistent CTAs, each owning 2 * batch * fft_channel_stride(n) elements.
+struct FftScratch {
+    double2* buf = nullptr;
+    int ctas = 0;
+};
+
 // Real-to-complex along time of C channels: channel c sample t at
 // in[c*in_cs + t*in_ts] (t < nt, zero-padded to 2nt); frequency k <= nt lands
 // at out[k*out_fs + c*out_cs]. TOut = double2 (FP64) or float2 (FP32 F-hat).
 template <typename TOut>
 cudaError_t launch_r2c(const double* in, long long in_cs, long long in_ts, TOut* out,
                        long long out_fs, long long out_cs, int channels, int nt,
-                       const FftPlanDev& plan, int batch, cudaStream_t stream);
+                       const FftPlanDev& plan, int batch, cudaStream_t stream,
+                       const FftScratch& gs = FftScratch{});
 
 // Complex-to-real: frequency k <= nt of channel c at in[k*in_fs + c*in_cs];
 // output time t < nt (1/(2nt) normalised, real part) at out[c*out_cs + t],
 // through the epilogue.
 cudaError_t launch_c2r(const double2* in, long long in_fs, long long in_cs, double* out,
                        long long out_cs, int channels, int nt, const FftPlanDev& plan,
-                       int batch, const C2REpilogue& epi, cudaStream_t stream);
+                       int batch, const C2REpilogue& epi, cudaStream_t stream,
+                       const FftScratch& gs = FftScratch{});
 
 // Fourier-space step, one right-hand side: y[f][i] = sum_j F[f][i][j] x[f][j].
 template <typename TF>
