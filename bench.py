@@ -279,9 +279,12 @@ def run_ours(args):
     else:
         from paper_2407_13066_b200 import distributed as bdist
 
-        engine = bdist.GridEngine.synthetic(nd, nm * world, nt, grid=(1, world), seed=1000)
+        # weak scaling at fixed per-GPU (N_d, N_m): the reference planner's rule
+        # (weak_scaling_shape, grid_planner.cpp:195-207) — 1 x p when N_d < N_m
+        _, (gr, gc) = btg.weak_scaling_shape(nd / nm, world)
+        engine = bdist.GridEngine.synthetic(nd * gr, nm * gc, nt, grid=(gr, gc), seed=1000)
         op = engine.local_op
-        grid = f"1x{world}"
+        grid = f"{gr}x{gc}"
     setup_s = time.perf_counter() - t0
     log(f"[bench] rank {rank}: setup {setup_s:.2f} s (F-hat {16 * (nt + 1) * nd * nm / 1e9:.2f} GB/GPU)")
 

@@ -197,6 +197,26 @@ btg_status btg_write_vector(const char* path, const double* values, size_t spati
 btg_status btg_read_vector(const char* path, double* values, size_t capacity, size_t* spatial_dim,
                            size_t* num_steps, int* ordering);
 
+/* partition_operator(const SpectralP2O&) (distributed.hpp:61-66,
+ * distributed.cpp:198-218) without a host round trip: a new handle on `device`
+ * holding sensors [i0, i1) x sources [j0, j1) of every stored frequency block
+ * of `src`, copied HBM->HBM (peer-to-peer over NVLink when the devices differ).
+ * Entries are bit-identical to the source's. Empty/out-of-range -> BTG_EGRID. */
+btg_status btg_slice_operator(btg_op src, size_t i0, size_t i1, size_t j0, size_t j1, int device,
+                              btg_op* out);
+
+/* Grid planner (grid_planner.hpp:43-65): the reference's scale-free cost
+ * (r/p) ln r + (10^l/r) ln(p/r), l = log10(N_d/N_m), its minimiser snapped to
+ * an r x c factorisation of `workers` (select_grid, grid_planner.cpp:123-193),
+ * the weak-scaling choice (:195-207) and the broadcast+reduce model (:105-114). */
+btg_status btg_select_grid(size_t workers, double log_dim_ratio, unsigned gpus_per_node, size_t* rows,
+                           size_t* cols);
+btg_status btg_weak_scaling_shape(double local_ratio, size_t workers, int* indifferent, size_t* rows,
+                                  size_t* cols);
+btg_status btg_modified_cost(double rows, size_t workers, double log_dim_ratio, double* out);
+btg_status btg_comm_cost(size_t rows, size_t cols, size_t num_sources, size_t num_sensors, size_t num_steps,
+                         double latency, double bandwidth, double* out);
+
 /* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */
 btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes);
 

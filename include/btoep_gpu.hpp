@@ -346,4 +346,45 @@ inline double objective_eval(const SpectralP2O& op, const SpaceTimeVector& m, co
     return v;
 }
 
+// ---- grid planner and spectral partition (grid_planner.hpp, distributed.hpp) --
+struct GridShape {
+    std::size_t rows = 1;
+    std::size_t cols = 1;
+    std::size_t workers() const { return rows * cols; }
+    bool operator==(const GridShape&) const = default;
+    std::string to_string() const { return std::to_string(rows) + "x" + std::to_string(cols); }
+};
+
+struct WeakScalingChoice {
+    bool indifferent = false;
+    GridShape shape;
+};
+
+inline GridShape select_grid(std::size_t workers, double log_dim_ratio, unsigned gpus_per_node = 1) {
+    GridShape g;
+    detail::check(btg_select_grid(workers, log_dim_ratio, gpus_per_node, &g.rows, &g.cols));
+    return g;
+}
+inline WeakScalingChoice weak_scaling_shape(double local_ratio, std::size_t workers) {
+    WeakScalingChoice c;
+    int ind = 0;
+    detail::check(btg_weak_scaling_shape(local_ratio, workers, &ind, &c.shape.rows, &c.shape.cols));
+    c.indifferent = ind != 0;
+    return c;
+}
+inline double modified_cost(double rows, std::size_t workers, double log_dim_ratio) {
+    double v = 0.0;
+    detail::check(btg_modified_cost(rows, workers, log_dim_ratio, &v));
+    return v;
+}
+
+// One shard of partition_operator(const SpectralP2O&, grid) (distributed.cpp:198-218):
+// sensors [i0, i1) x sources [j0, j1) of every stored block, copied on the device.
+inline SpectralP2O slice(const SpectralP2O& op, std::size_t i0, std::size_t i1, std::size_t j0, std::size_t j1,
+                         int device = 0) {
+    btg_op h = nullptr;
+    detail::check(btg_slice_operator(op.handle(), i0, i1, j0, j1, device, &h));
+    return SpectralP2O(h);
+}
+
 }  // namespace btoep

@@ -14,6 +14,7 @@
 //   partition + distributed_forward/adjoint  distributed.hpp:57-121
 //   Rng              rng.hpp:12-32  (the seeded inputs of tests/oracles.cpp:87-98)
 //   run_verification verify.hpp:13
+//   select_grid / weak_scaling_shape / modified_cost / comm_cost  grid_planner.hpp:43-65
 //
 // Every entry point returns 0 on success, 1 on a btoep::Error (message in
 // ref_last_error()), 2 on any other exception.
@@ -28,6 +29,7 @@
 #include "btoep/block_operator.hpp"
 #include "btoep/distributed.hpp"
 #include "btoep/errors.hpp"
+#include "btoep/grid_planner.hpp"
 #include "btoep/inverse.hpp"
 #include "btoep/io.hpp"
 #include "btoep/rng.hpp"
@@ -303,6 +305,60 @@ int ref_verify(std::uint64_t seed, char* report, std::size_t report_len, int* pa
             std::strncpy(report, s.c_str(), report_len - 1);
             report[report_len - 1] = '\0';
         }
+    });
+}
+
+// ---- grid planner (grid_planner.cpp:105-207) ------------------------------------
+int ref_select_grid(std::size_t workers, double log_dim_ratio, unsigned gpus_per_node, std::size_t* rc) {
+    return guarded([&] {
+        const GridShape g = select_grid(workers, log_dim_ratio, gpus_per_node);
+        rc[0] = g.rows;
+        rc[1] = g.cols;
+    });
+}
+
+int ref_weak_scaling_shape(double local_ratio, std::size_t workers, std::size_t* out3) {
+    return guarded([&] {
+        const WeakScalingChoice c = weak_scaling_shape(local_ratio, workers);
+        out3[0] = c.indifferent ? 1 : 0;
+        out3[1] = c.shape.rows;
+        out3[2] = c.shape.cols;
+    });
+}
+
+int ref_modified_cost(double rows, std::size_t workers, double log_dim_ratio, double* out) {
+    return guarded([&] { *out = modified_cost(rows, workers, log_dim_ratio); });
+}
+
+int ref_comm_cost(std::size_t rows, std::size_t cols, std::size_t nsrc, std::size_t nsens, std::size_t nt,
+                  double latency, double bandwidth, double* out) {
+    return guarded([&] {
+        CostParams p;
+        p.latency = latency;
+        p.bandwidth = bandwidth;
+        ProblemDims d;
+        d.num_sources = nsrc;
+        d.num_sensors = nsens;
+        d.num_steps = nt;
+        *out = comm_cost(GridShape{rows, cols}, d, p);
+    });
+}
+
+// ---- partition of an operator already in frequency form (distributed.cpp:198-218)
+void* ref_partition_spectral(void* h, std::size_t rows, std::size_t cols) {
+    PartitionHandle* p = nullptr;
+    const int rc = guarded([&] {
+        p = new PartitionHandle{partition_operator(*static_cast<SpectralP2O*>(h), GridShape{rows, cols})};
+    });
+    return rc == 0 ? p : nullptr;
+}
+
+// Shard (r, c)'s frequency blocks in the reference's full 2N_t layout.
+int ref_partition_shard_spectrum(void* h, std::size_t r, std::size_t c, double* out_c128) {
+    return guarded([&] {
+        const Partition& part = static_cast<PartitionHandle*>(h)->partition;
+        const SpectralP2O& s = part.shard(r, c).spectral;
+        std::memcpy(out_c128, s.freq_blocks.data(), sizeof(std::complex<double>) * s.freq_blocks.size());
     });
 }
 

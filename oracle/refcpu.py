@@ -63,6 +63,15 @@ def lib():
                                    ctypes.c_double, _size_t, ctypes.c_int, _c_double_p]
         L.ref_objective.argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_double, ctypes.c_int,
                                     _c_double_p]
+        _sz_p = ctypes.POINTER(_size_t)
+        L.ref_select_grid.argtypes = [_size_t, ctypes.c_double, ctypes.c_uint, _sz_p]
+        L.ref_weak_scaling_shape.argtypes = [ctypes.c_double, _size_t, _sz_p]
+        L.ref_modified_cost.argtypes = [ctypes.c_double, _size_t, ctypes.c_double, _c_double_p]
+        L.ref_comm_cost.argtypes = [_size_t, _size_t, _size_t, _size_t, _size_t, ctypes.c_double,
+                                    ctypes.c_double, _c_double_p]
+        L.ref_partition_spectral.argtypes = [ctypes.c_void_p, _size_t, _size_t]
+        L.ref_partition_spectral.restype = ctypes.c_void_p
+        L.ref_partition_shard_spectrum.argtypes = [ctypes.c_void_p, _size_t, _size_t, _c_double_p]
         _lib = L
     return _lib
 
@@ -267,3 +276,53 @@ def host_cores() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+# ---- grid planner (grid_planner.hpp:43-65) ----------------------------------------
+def select_grid(workers: int, log_dim_ratio: float, gpus_per_node: int = 1):
+    rc = (_size_t * 2)()
+    _check(lib().ref_select_grid(workers, log_dim_ratio, gpus_per_node, rc))
+    return int(rc[0]), int(rc[1])
+
+
+def weak_scaling_shape(local_ratio: float, workers: int):
+    out = (_size_t * 3)()
+    _check(lib().ref_weak_scaling_shape(local_ratio, workers, out))
+    return bool(out[0]), (int(out[1]), int(out[2]))
+
+
+def modified_cost(rows: float, workers: int, log_dim_ratio: float) -> float:
+    v = ctypes.c_double()
+    _check(lib().ref_modified_cost(rows, workers, log_dim_ratio, ctypes.byref(v)))
+    return v.value
+
+
+def comm_cost(rows, cols, num_sources, num_sensors, num_steps, latency=1e-6, bandwidth=1e10) -> float:
+    v = ctypes.c_double()
+    _check(lib().ref_comm_cost(rows, cols, num_sources, num_sensors, num_steps, latency, bandwidth,
+                               ctypes.byref(v)))
+    return v.value
+
+
+def spectral_partition_shards(op: "RefSpectralOperator", rows: int, cols: int):
+    """partition_operator(const SpectralP2O&) (distributed.cpp:198-218): the full
+    2N_t frequency blocks of every shard, keyed by (row, col)."""
+    L = lib()
+    h = L.ref_partition_spectral(op._h, rows, cols)
+    if not h:
+        raise RefError(L.ref_last_error().decode())
+    try:
+        b = (_size_t * (4 * rows * cols))()
+        _check(L.ref_partition_bounds(h, b))
+        out = {}
+        for k in range(rows * cols):
+            r, c = divmod(k, cols)
+            s0, s1, m0, m1 = (int(x) for x in b[4 * k: 4 * k + 4])
+            if s1 == s0 or m1 == m0:
+                continue
+            spec = np.empty((2 * op.num_steps, s1 - s0, m1 - m0), dtype=np.complex128)
+            _check(L.ref_partition_shard_spectrum(h, r, c, spec.ctypes.data_as(_c_double_p)))
+            out[(r, c)] = (s0, s1, m0, m1, spec)
+        return out
+    finally:
+        L.ref_partition_destroy(h)

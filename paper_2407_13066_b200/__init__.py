@@ -10,6 +10,7 @@ Python surface (operator, solver, files) plus the multi-GPU grid
 from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
 from .io import load_operator, peek_operator, read_vector, save_operator, write_vector  # noqa: F401
 from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
+from .planner import comm_cost, modified_cost, parse_grid, plan_grid, select_grid, weak_scaling_shape  # noqa: F401
 from .solver import cg_solve, cg_solve_op, objective_eval  # noqa: F401
 
 __all__ = [
@@ -22,6 +23,12 @@ __all__ = [
     "HessianOperator",
     "SpectralOperator",
     "cg_solve",
+    "comm_cost",
+    "modified_cost",
+    "parse_grid",
+    "plan_grid",
+    "select_grid",
+    "weak_scaling_shape",
     "cg_solve_op",
     "create",
     "fill_uniform",

@@ -50,6 +50,11 @@ EXPORTED = (
     "btg_write_vector",
     "btg_read_vector",
     "btg_load_operator_rect",
+    "btg_slice_operator",
+    "btg_select_grid",
+    "btg_weak_scaling_shape",
+    "btg_modified_cost",
+    "btg_comm_cost",
 )
 
 
@@ -193,6 +198,13 @@ def load():
     L.btg_write_vector.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, ctypes.c_int]
     L.btg_read_vector.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_sz),
                                   ctypes.POINTER(ctypes.c_int)]
+    L.btg_slice_operator.argtypes = [_vp, _sz, _sz, _sz, _sz, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.btg_select_grid.argtypes = [_sz, ctypes.c_double, ctypes.c_uint, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]
+    L.btg_weak_scaling_shape.argtypes = [ctypes.c_double, _sz, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_sz),
+                                         ctypes.POINTER(_sz)]
+    L.btg_modified_cost.argtypes = [ctypes.c_double, _sz, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+    L.btg_comm_cost.argtypes = [_sz, _sz, _sz, _sz, _sz, ctypes.c_double, ctypes.c_double,
+                                ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTED:
         if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
             getattr(L, name).restype = ctypes.c_int

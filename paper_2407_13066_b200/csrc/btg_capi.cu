@@ -814,6 +814,49 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
     return finish_host(op, hv, hvd, hv_len, flags);
 }
 
+// partition_operator(const SpectralP2O&) (distributed.cpp:198-218) on the
+// device: the shard's rectangle of every stored frequency block is copied
+// HBM->HBM (or peer-to-peer over NVLink when `device` differs) with one 3-D
+// copy — no re-setup, no host round trip. Entries are bit-identical.
+btg_status btg_slice_operator(btg_op src, size_t i0, size_t i1, size_t j0, size_t j1, int device,
+                              btg_op* out) {
+    if (!src) return fail(BTG_EARG, "null operator handle");
+    if (!out) return fail(BTG_EARG, "null output handle");
+    *out = nullptr;
+    if (i0 >= i1 || i1 > src->nd || j0 >= j1 || j1 > src->nm)
+        return fail(BTG_EGRID, "slice [%zu,%zu) x [%zu,%zu) outside the %zu x %zu operator (or empty)", i0, i1,
+                    j0, j1, src->nd, src->nm);
+    {
+        std::lock_guard<std::mutex> lock(src->mu);
+        for (size_t i = i0; i < i1; ++i)
+            if (!src->rows_ready[i]) return fail(BTG_EARG, "slice: sensor row %zu of the source is not set up", i);
+    }
+    btg_op dst = nullptr;
+    BTG_TRY(btg_create(i1 - i0, j1 - j0, src->nt, src->precision, device, &dst));
+    cudaMemcpy3DPeerParms p = {};
+    p.srcPtr = make_cudaPitchedPtr(static_cast<char*>(src->F) + (i0 * src->nm + j0) * src->F_elem,
+                                   src->nm * src->F_elem, (j1 - j0) * src->F_elem, src->nd);
+    p.srcDevice = src->device;
+    p.dstPtr = make_cudaPitchedPtr(dst->F, dst->nm * dst->F_elem, dst->nm * dst->F_elem, dst->nd);
+    p.dstDevice = dst->device;
+    p.extent = make_cudaExtent((j1 - j0) * src->F_elem, i1 - i0, src->nf);
+    cudaError_t e;
+    {
+        DeviceGuard g(src->device);
+        std::lock_guard<std::mutex> lock(src->mu);
+        e = cudaMemcpy3DPeerAsync(&p, src->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(src->stream);
+    }
+    if (e != cudaSuccess) {
+        btg_destroy(dst);
+        return fail(BTG_ECUDA, "slice copy: %s", cudaGetErrorString(e));
+    }
+    std::fill(dst->rows_ready.begin(), dst->rows_ready.end(), 1);
+    dst->rows_ready_count = dst->nd;
+    *out = dst;
+    return BTG_OK;
+}
+
 // Internal hooks for btg_io.cu (C++ linkage, not part of the C ABI).
 btg_status btg_internal_fail(btg_status s, const char* msg) { return fail(s, "%s", msg); }
 

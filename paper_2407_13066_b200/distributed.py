@@ -208,6 +208,36 @@ class GridEngine:
                                     (shard.source_begin, shard.source_end), precision, device)
         return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"))
 
+    @classmethod
+    def from_operator(cls, op, grid: Tuple[int, int]):
+        """partition_operator(const SpectralP2O&) (distributed.cpp:198-218) of an
+        operator already resident on this rank's GPU (e.g. a replicated load):
+        the rank keeps only its rectangle (btg_slice_operator, HBM->HBM)."""
+        import torch
+        import torch.distributed as dist
+
+        nd, nm, nt = op.num_sensors, op.num_sources, op.num_steps
+        shard = partition_bounds(nd, nm, *grid)[dist.get_rank()]
+        device = torch.cuda.current_device()
+        local = None
+        if not shard.empty:
+            local = op.slice((shard.sensor_begin, shard.sensor_end), (shard.source_begin, shard.source_end),
+                             device)
+        return cls(nd, nm, nt, grid, local, device=torch.device(f"cuda:{device}"))
+
+    @staticmethod
+    def plan(num_sensors: int, num_sources: int, workers: Optional[int] = None,
+             gpus_per_node: int = 1) -> Tuple[int, int]:
+        """The planner's grid (select_grid, grid_planner.cpp:123-193) for the
+        world size (or ``workers``)."""
+        from .planner import plan_grid
+
+        if workers is None:
+            import torch.distributed as dist
+
+            workers = dist.get_world_size()
+        return plan_grid(num_sensors, num_sources, workers, gpus_per_node)
+
     # -- helpers -------------------------------------------------------------------
     def _rank_of(self, i: int, j: int) -> int:
         return i * self.cols + j

@@ -147,6 +147,16 @@ class SpectralOperator:
         check(_lib.load().btg_spectrum_device(self._h, ctypes.byref(p), ctypes.byref(sz)))
         return p.value, sz.value
 
+    def slice(self, sensors, sources, device: int | None = None) -> "SpectralOperator":
+        """The shard sensors [i0, i1) x sources [j0, j1) of every stored frequency
+        block as a new operator on ``device`` (partition_operator(SpectralP2O),
+        distributed.cpp:198-218): an HBM->HBM / NVLink peer copy, no re-setup."""
+        (i0, i1), (j0, j1) = sensors, sources
+        dev = self.device if device is None else int(device)
+        h = ctypes.c_void_p()
+        check(_lib.load().btg_slice_operator(self._h, int(i0), int(i1), int(j0), int(j1), dev, ctypes.byref(h)))
+        return SpectralOperator(h.value, i1 - i0, j1 - j0, self.num_steps, self.precision, dev)
+
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
             _lib.load().btg_destroy(self._h)

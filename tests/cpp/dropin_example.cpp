@@ -78,6 +78,20 @@ int main() {
     CHECK(r.converged);
     for (std::size_t k = 0; k < m.values.size(); ++k) CHECK(std::abs(r.solution.values[k] - 0.5 * m.values[k]) < 1e-12);
 
+    // grid planner (test_grid_planner.cpp:93-99) and a spectral shard (distributed.cpp:198-218)
+    CHECK((select_grid(80, -2.0, 4) == GridShape{4, 20}));
+    CHECK((select_grid(48, -3.0, 1) == GridShape{1, 48}));
+    CHECK(weak_scaling_shape(1.0, 4).indifferent);
+    SpectralP2O part = slice(op, 1, 3, 0, 2);
+    CHECK(part.num_sensors == 2 && part.num_sources == 2 && part.num_steps == 8);
+    SpaceTimeVector m2 = SpaceTimeVector::zeros(2, 8, Ordering::SOTI);
+    for (std::size_t k = 0; k < m2.values.size(); ++k) m2.values[k] = std::cos(0.7 * k);
+    SpaceTimeVector d2 = apply_forward(part, m2);  // identity rows 1,2 x cols 0,1: d2[0] = m2[1], d2[1] = 0
+    for (std::size_t t = 0; t < 8; ++t) {
+        CHECK(std::abs(d2.at(0, t) - m2.at(1, t)) < 1e-12);
+        CHECK(std::abs(d2.at(1, t)) < 1e-12);
+    }
+
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
