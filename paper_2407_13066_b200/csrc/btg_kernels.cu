@@ -26,7 +26,8 @@ namespace btg {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kFwdWarpMaxCols = 4096;  // forward GEMV rows up to this length: warp-per-row kernel
+constexpr int kFwdWarpMaxCols = 4096;
+constexpr int kMaxGridY = 65535;        // frequency batches per launch (grid.y limit)  // forward GEMV rows up to this length: warp-per-row kernel
 
 // ---------------------------------------------------------------------------
 // streaming loads of F-hat
@@ -591,14 +592,20 @@ cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int
         return cudaGetLastError();
     }
     constexpr int kRows = 8;
-    dim3 grid((nd + kRows - 1) / kRows, nf);
-    if constexpr (sizeof(TF) == 8) {
-        if ((nm & 1) == 0 && (j0 & 1) == 0) {
-            k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj, accumulate);
-            return cudaGetLastError();
+    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
+        const int nb = std::min(kMaxGridY, nf - f0);
+        const TF* Fb = F + (size_t)f0 * nd * nm;
+        const double2* xb = x + (size_t)f0 * nm;
+        double2* yb = y + (size_t)f0 * nd;
+        dim3 grid((nd + kRows - 1) / kRows, nb);
+        if constexpr (sizeof(TF) == 8) {
+            if ((nm & 1) == 0 && (j0 & 1) == 0) {
+                k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+                continue;
+            }
         }
+        k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
     }
-    k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj, accumulate);
     return cudaGetLastError();
 }
 
@@ -613,18 +620,25 @@ cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, in
                            cudaStream_t stream) {
     constexpr int kJpt = 2;
     constexpr int kUnr = 8;
-    dim3 grid((nj + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nf);
     const size_t smem = (size_t)nd * sizeof(double2);
     // Default: read d-hat_f through the read-only path (a warp-uniform broadcast
     // that hits L1), so a CTA starts streaming F-hat without a fill + barrier.
     static const bool use_smem = std::getenv("BTG_ADJ_SMEM") != nullptr;
-    if (use_smem && smem <= 96 * 1024) {
-        auto kern = k_gemv_adj<TF, VEC, kJpt, kUnr, true>;
-        cudaError_t e = set_smem(kern, smem);
+    const bool smem_d = use_smem && smem <= 96 * 1024;
+    if (smem_d) {
+        cudaError_t e = set_smem(k_gemv_adj<TF, VEC, kJpt, kUnr, true>, smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, kThreads, smem, stream>>>(F, x, y, nd, nm, j0, nj);
-    } else {
-        k_gemv_adj<TF, VEC, kJpt, kUnr, false><<<grid, kThreads, 0, stream>>>(F, x, y, nd, nm, j0, nj);
+    }
+    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
+        const int nb = std::min(kMaxGridY, nf - f0);
+        const TF* Fb = F + (size_t)f0 * nd * nm;
+        const double2* xb = x + (size_t)f0 * nd;
+        double2* yb = y + (size_t)f0 * nm;
+        dim3 grid((nj + kThreads * VEC * kJpt - 1) / (kThreads * VEC * kJpt), nb);
+        if (smem_d)
+            k_gemv_adj<TF, VEC, kJpt, kUnr, true><<<grid, kThreads, smem, stream>>>(Fb, xb, yb, nd, nm, j0, nj);
+        else
+            k_gemv_adj<TF, VEC, kJpt, kUnr, false><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj);
     }
     return cudaGetLastError();
 }

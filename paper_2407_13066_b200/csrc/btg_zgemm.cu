@@ -16,6 +16,7 @@
 // tile of one frequency with 8 warps (4 x 2), each warp 2 x 4 m16n8k4 tiles,
 // the K loop fed by a 4-stage cp.async pipeline. K is reduced in a fixed order
 // inside one CTA: results are deterministic.
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -272,6 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 }
 
+constexpr int kMaxGridY = 65535;
+
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -284,8 +287,12 @@ cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int
     const size_t smem = kStages * kFwdStageDoubles * sizeof(double);
     cudaError_t e = set_smem(k_zgemm_fwd, smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((nd + kTileM - 1) / kTileM, nf, (nrhs + kTileR - 1) / kTileR);
-    k_zgemm_fwd<<<grid, kThreads, smem, stream>>>(F, X, Y, nd, nm, nrhs);
+    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
+        const int nb = std::min(kMaxGridY, nf - f0);
+        dim3 grid((nd + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
+        k_zgemm_fwd<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nm,
+                                                      Y + (size_t)f0 * nrhs * nd, nd, nm, nrhs);
+    }
     return cudaGetLastError();
 }
 
@@ -294,8 +301,12 @@ cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int
     const size_t smem = kStages * kAdjStageDoubles * sizeof(double);
     cudaError_t e = set_smem(k_zgemm_adj, smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((nm + kTileM - 1) / kTileM, nf, (nrhs + kTileR - 1) / kTileR);
-    k_zgemm_adj<<<grid, kThreads, smem, stream>>>(F, X, Y, nd, nm, nrhs);
+    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {
+        const int nb = std::min(kMaxGridY, nf - f0);
+        dim3 grid((nm + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
+        k_zgemm_adj<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nd,
+                                                      Y + (size_t)f0 * nrhs * nm, nd, nm, nrhs);
+    }
     return cudaGetLastError();
 }
 

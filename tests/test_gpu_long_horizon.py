@@ -72,3 +72,22 @@ def test_long_horizon_multi_rhs(btg):
         out = op.apply_forward(ms)
         for r in range(k):
             assert R.rel_l2(out[r], R.apply_forward(spec, ms[r])) <= TOL64
+
+
+def test_horizon_beyond_grid_y_limit(btg):
+    """N_t + 1 > 65535 frequencies: the Fourier-space kernels run in frequency
+    batches (grid.y limit), single- and multi-RHS."""
+    nt = 70000
+    blocks, m, d = R.random_problem(9, 2, 3, nt)
+    spec = R.setup_full(blocks)
+    with btg.setup(blocks) as op:
+        assert R.rel_l2(op.apply_forward(m), R.apply_forward(spec, m)) <= TOL64
+        assert R.rel_l2(op.apply_adjoint(d), R.apply_adjoint(spec, d)) <= TOL64
+        ms = np.stack([m, 2.0 * m[::-1]])
+        out = op.apply_forward(ms)
+        for r in range(2):
+            assert R.rel_l2(out[r], R.apply_forward(spec, ms[r])) <= TOL64
+        ds = np.stack([d, -d])
+        outa = op.apply_adjoint(ds)
+        for r in range(2):
+            assert R.rel_l2(outa[r], R.apply_adjoint(spec, ds[r])) <= TOL64
