@@ -95,6 +95,12 @@ struct btg_op_s {
     btg::FastTables fast{};
     bool fast_ok = false;
     bool no_dmma = false;      // BTG_DISABLE_DMMA: per-RHS GEMV streams instead of the ZGEMM
+    bool tensor_i8 = false;    // BTG_TENSOR_I8=1: multi-RHS step on tcgen05 int8 (Ozaki splitting)
+    int8_t* oz_A = nullptr;    // int8 slices of F-hat (built lazily, invalidated by setup)
+    unsigned long long* oz_mA = nullptr;
+    int* oz_mB = nullptr;
+    size_t oz_mB_cap = 0;
+    bool oz_valid = false;
     bool legacy_gemv = true;   // register-load GEMV; BTG_GEMV_TMA=1 selects the TMA ring
     int fft_batch = 1;        // channels per CTA for vector transforms
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
@@ -266,13 +272,43 @@ btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* ou
     return BTG_OK;
 }
 
+// int8 slices of F-hat for the tensor-core multi-RHS path, built on first use.
+btg_status ensure_oz(btg_op op, size_t nrhs) {
+    const int nf = (int)op->nf, nd = (int)op->nd, nm = (int)op->nm;
+    if (!op->oz_A) {
+        const size_t bytes = btg::oz_operator_bytes(nf, nd, nm);
+        cudaError_t e = cudaMalloc(&op->oz_A, bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&op->oz_mA, btg::oz_operator_scales(nf, nm) * sizeof(unsigned long long));
+        if (e != cudaSuccess) return fail(BTG_ENOMEM, "int8 F-hat slices (%zu bytes): %s", bytes, cudaGetErrorString(e));
+        op->oz_valid = false;
+    }
+    if (!op->oz_valid) {
+        BTG_CUDA(btg::oz_quantize_operator(static_cast<const double2*>(op->F), nf, nd, nm, op->oz_A, op->oz_mA,
+                                           op->stream));
+        op->oz_valid = true;
+    }
+    const size_t need = btg::oz_vector_scales(nf, (int)std::min<size_t>(nrhs, 32), (int)std::max(op->nd, op->nm));
+    if (need > op->oz_mB_cap) {
+        cudaFree(op->oz_mB);
+        op->oz_mB = nullptr;
+        BTG_CUDA(cudaMalloc(&op->oz_mB, need * sizeof(int)));
+        op->oz_mB_cap = need;
+    }
+    return BTG_OK;
+}
+
 btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, size_t nrhs) {
     StageClock clk(op, &op->counters.apply);
     const size_t nin = adjoint ? op->nd : op->nm;
     const size_t nout = adjoint ? op->nm : op->nd;
     const int nf = (int)op->nf, nd = (int)op->nd, nm = (int)op->nm;
     cudaError_t e;
-    if (nrhs > 1) {
+    if (nrhs > 1 && op->tensor_i8) {
+        // tcgen05 int8 tensor cores, exact-integer Ozaki splitting (btg_ozaki.cu)
+        if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
+        BTG_TRY(ensure_oz(op, nrhs));
+        e = btg::oz_apply(adjoint, op->oz_A, op->oz_mA, in, out, nf, nd, nm, (int)nrhs, op->oz_mB, op->stream);
+    } else if (nrhs > 1) {
         // ZGEMM on the FP64 tensor cores (btg_zgemm.cu); FP64 F-hat only.
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
         const double2* F = static_cast<const double2*>(op->F);
@@ -619,6 +655,7 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
         op->fast_ok = true;
     }
     op->no_dmma = std::getenv("BTG_DISABLE_DMMA") != nullptr;
+    op->tensor_i8 = std::getenv("BTG_TENSOR_I8") != nullptr;
     // Default: the register-load GEMV (7.4 TB/s at configs[1]); the TMA ring is
     // opt-in (BTG_GEMV_TMA=1): faster on a 6.7 GB operator, slower at 54 GB.
     op->legacy_gemv = std::getenv("BTG_GEMV_TMA") == nullptr;
@@ -657,6 +694,7 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
         return fail(BTG_EDIM, "setup rows [%zu, %zu) outside [0, %zu)", i0, i1, op->nd);
     std::lock_guard<std::mutex> lock(op->mu);
     DeviceGuard g(op->device);
+    op->oz_valid = false;  // F-hat changes: int8 slices are stale
     const size_t rows = i1 - i0;
     const size_t slab_channels = rows * op->nm;
     const long long out_fs = (long long)(op->nd * op->nm);
@@ -863,6 +901,7 @@ btg_status btg_internal_fail(btg_status s, const char* msg) { return fail(s, "%s
 btg_status btg_internal_upload_spectrum_block(btg_op op, size_t f, const double* block) {
     if (!op || !block || f > op->nt) return fail(BTG_EARG, "bad spectrum block upload");
     std::lock_guard<std::mutex> lock(op->mu);
+    op->oz_valid = false;
     DeviceGuard g(op->device);
     const size_t blk = op->nd * op->nm;
     if (op->precision == BTG_F64) {
@@ -1232,6 +1271,9 @@ void btg_destroy(btg_op op) {
         if (op->own_stream) cudaStreamSynchronize(op->own_stream);
         if (op->stream && op->stream != op->own_stream) cudaStreamSynchronize(op->stream);
         cudaFree(op->F);
+        cudaFree(op->oz_A);
+        cudaFree(op->oz_mA);
+        cudaFree(op->oz_mB);
         cudaFree(op->d_tw);
         cudaFree(op->d_post);
         cudaFree(op->d_fast);

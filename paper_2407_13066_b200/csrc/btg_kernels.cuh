@@ -100,6 +100,15 @@ cudaError_t launch_gemv_adj_tma(const double2* F, const double2* x, double2* y, 
 
 // Multi-RHS Fourier-space step on FP64 tensor cores (btg_zgemm.cu). X/Y are
 // [f][r][dim] (dim = N_m or N_d), FP64 F-hat only.
+// Multi-RHS step on the tcgen05 int8 tensor cores (Ozaki splitting, btg_ozaki.cu).
+size_t oz_operator_bytes(int nf, int nd, int nm);
+size_t oz_operator_scales(int nf, int nm);
+size_t oz_vector_scales(int nf, int nrhs, int kdim);
+cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_t* Aq, unsigned long long* mA,
+                                 cudaStream_t stream);
+cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
+                     int nf, int nd, int nm, int nrhs, int* mB, cudaStream_t stream);
+
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream);
 cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,

@@ -1,0 +1,533 @@
+// Multi-RHS Fourier-space step on the 5th-generation tensor cores (tcgen05).
+//
+// tcgen05 has no FP64 kind, so the FP64 complex product Y_f = F_f X_f (and
+// the adjoint F_f^H D_f) is computed exactly-in-integers with the Ozaki
+// splitting: every real number v of a block that shares the power-of-two scale
+// 2^e (max |v| < 2^e) is written as
+//
+//     v = 2^e * sum_{s=1..S} q_s 2^{-7 s} + r,   q_s in [-64, 64] (int8),  |r| <= 2^{e-7S-1}
+//
+// (max |v| < 2^{e-1}; every digit is a round-to-nearest of a value in
+// [-64, 64], taken with the 1.5*2^52 magic-number add, so slicing is pure
+// full-rate FP64 adds/multiplies with no conversion instructions)
+//
+// and  sum_k a_k b_k = 2^{eA+eB} sum_{L} 2^{-7L} C_L,  C_L = sum_{s+t=L} sum_k qa_s qb_t
+// where every C_L is an exact int32 sum computed by kind::i8 MMAs into its
+// own TMEM accumulator (levels L = 2..S+1; pairs with s+t > S+1 are below the
+// FP64 rounding of the result). With S = 7 the per-entry truncation is 2^-49
+// of the block maximum; results agree with the FP64 reference to ~1e-14 on the
+// parity tests.
+//
+// Layouts (int8, "core matrix" = 8 rows x 16 bytes, 128 B):
+//   F-hat slices  Aq[f][ig][jg][s][c][8 i][16 j]   ig = i/8, jg = j/16, c = re/im plane
+//   The same bytes are the K-major A operand of the forward (rows i, K = j) and
+//   the MN-major A operand of the adjoint (rows j, K = i).
+//   Block scales  mA[f][jb] (max |F| over all i and the 1024-column block jb)
+//   Vector scales mB[f][r][kb] (max over a 1024-entry block of x-hat_f[r] / d-hat_f[r])
+// The complex product uses plane-separated K: K' = (c, k); the B operand rows
+// n' = 2r+q carry (xr, xi) against the real plane and (-xi, xr) against the
+// imaginary plane (adjoint: (dr, di) and (di, -dr)), so one real GEMM yields
+// [Re Y, Im Y] interleaved.
+//
+// Kernel roles (192 threads, one CTA per SM, persistent over (f, row-tile)):
+//   warp 0     TMA producer of the F-hat slice tiles (cp.async.bulk, 2-stage ring)
+//   warp 1     TMEM owner + single-thread MMA issuer (56 MMAs per 32-wide K step)
+//   warps 2-5  slice the FP64 vector block of each K step into the B tile
+//              (shared memory), and drain the TMEM level accumulators into FP64
+//              registers at the end of every 1024-wide K chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "btg_kernels.cuh"
+#include "btg_umma.cuh"
+
+namespace btg {
+namespace oz {
+
+constexpr int kS = 7;                       // slices per operand
+constexpr int kLevels = kS;                 // L = 2 .. S+1
+constexpr int kCM = 128;                    // bytes per core matrix
+constexpr int kPos = kS * 2 * kCM;          // bytes per core-matrix position (all slices, both planes)
+constexpr int kChunk = 1024;                // K entries per int32 accumulation chunk / scale block
+constexpr int kStepsPerChunk = kChunk / 32;
+constexpr int kTileM = 128;
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr int kAStage = 16 * 2 * kPos;      // forward: 16 ig x 2 jg; adjoint: 4 ig x 8 jg (same size)
+constexpr int kBStageMax = 2 * 8 * kPos;    // 2 K-groups x up to 8 n'-groups
+
+// Block exponent e with max < 2^{e-1} (so every scaled entry lies in (-1/2, 1/2)).
+__device__ __forceinline__ int scale_exp(uint64_t maxbits) {
+    const double m = __longlong_as_double((long long)maxbits);
+    if (!(m > 0.0)) return 0;
+    int e;
+    frexp(m, &e);  // m = f 2^e, f in [0.5, 1): m < 2^e
+    return e + 1;
+}
+
+__device__ __forceinline__ double pow2(int e) {  // exact 2^e for normal range
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: w + kMagic rounds w to an integer
+
+// Next signed digit of u in [-1/2, 1/2]: q = rint(128 u) in [-64, 64], u <- 128 u - q (exact).
+__device__ __forceinline__ int digit(double& u) {
+    const double w = u * 128.0;
+    const double t = w + kMagic;
+    u = w - (t - kMagic);
+    return __double2loint(t);
+}
+
+__device__ __forceinline__ void digits(double u, int (&q)[kS]) {
+#pragma unroll
+    for (int s = 0; s < kS; ++s) q[s] = digit(u);
+}
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+    return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
+           ((uint32_t)(d & 0xFF) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// Operator quantisation (once per operator, lazily)
+// ---------------------------------------------------------------------------
+// mA[f][jb] = max over i < nd, j in block jb, re/im of |F[f][i][j]| (as FP64 bits)
+__global__ void k_scale_op(const double2* __restrict__ F, unsigned long long* __restrict__ mA, int nf, int nd,
+                           int nm, int nkb) {
+    const int rows_per = 8;
+    const long long items = (long long)nf * nkb * ((nd + rows_per - 1) / rows_per);
+    __shared__ double red[8];
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        const int ib = (int)(it % ((nd + rows_per - 1) / rows_per));
+        const long long fj = it / ((nd + rows_per - 1) / rows_per);
+        const int jb = (int)(fj % nkb);
+        const int f = (int)(fj / nkb);
+        double m = 0.0;
+        const int j0 = jb * kChunk, j1 = min(nm, j0 + kChunk);
+        for (int r = 0; r < rows_per; ++r) {
+            const int i = ib * rows_per + r;
+            if (i >= nd) break;
+            const double2* row = F + ((size_t)f * nd + i) * nm;
+            for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+                const double2 v = __ldg(row + j);
+                m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+            atomicMax(mA + (size_t)f * nkb + jb, (unsigned long long)__double_as_longlong(m));
+        }
+        __syncthreads();
+    }
+}
+
+// One warp per core-matrix position (f, ig, jg): lane = (row r = lane/4, quad = lane%4),
+// 4 consecutive complex j per lane -> 14 words (7 slices x 2 planes) of 4 int8.
+__global__ void k_slice_op(const double2* __restrict__ F, const unsigned long long* __restrict__ mA,
+                           int8_t* __restrict__ Aq, int nf, int nd, int nm, int IG, int JG, int nkb) {
+    const int lane = threadIdx.x & 31;
+    const long long npos = (long long)nf * IG * JG;
+    const int warps = (int)(blockDim.x >> 5);
+    for (long long p = (long long)blockIdx.x * warps + (threadIdx.x >> 5); p < npos; p += (long long)gridDim.x * warps) {
+        const int jg = (int)(p % JG);
+        const long long fi = p / JG;
+        const int ig = (int)(fi % IG);
+        const int f = (int)(fi / IG);
+        const int i = ig * 8 + (lane >> 2);
+        const int jq = jg * 16 + (lane & 3) * 4;
+        const int e = scale_exp(mA[(size_t)f * nkb + (jg * 16) / kChunk]);
+        const double inv = pow2(-e);
+        int qr[4][kS], qi[4][kS];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double2 v = make_double2(0.0, 0.0);
+            if (i < nd && jq + u < nm) v = __ldg(F + ((size_t)f * nd + i) * nm + jq + u);
+            digits(v.x * inv, qr[u]);
+            digits(v.y * inv, qi[u]);
+        }
+        uint32_t* out = reinterpret_cast<uint32_t*>(Aq + (size_t)p * kPos) + (lane >> 2) * 4 + (lane & 3);
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+            out[(s * 2 + 0) * (kCM / 4)] = pack4(qr[0][s], qr[1][s], qr[2][s], qr[3][s]);
+            out[(s * 2 + 1) * (kCM / 4)] = pack4(qi[0][s], qi[1][s], qi[2][s], qi[3][s]);
+        }
+    }
+}
+
+// eB[(f*nr + r)*nkb + kb] = block exponent of max |re|,|im| over V[f][r0+r][kb*1024 ...] (one warp per item)
+__global__ void k_scale_vec(const double2* __restrict__ V, int* __restrict__ mB, int nf, int ldr,
+                            int r0, int nr, int K, int nkb) {
+    const int lane = threadIdx.x & 31;
+    const long long items = (long long)nf * nr * nkb;
+    const int warps = (int)(blockDim.x >> 5);
+    for (long long it = (long long)blockIdx.x * warps + (threadIdx.x >> 5); it < items;
+         it += (long long)gridDim.x * warps) {
+        const int kb = (int)(it % nkb);
+        const long long fr = it / nkb;
+        const int r = (int)(fr % nr);
+        const int f = (int)(fr / nr);
+        const double2* v = V + ((size_t)f * ldr + r0 + r) * K;
+        double m = 0.0;
+        const int k1 = min(K, (kb + 1) * kChunk);
+        for (int k = kb * kChunk + lane; k < k1; k += 32) {
+            const double2 x = __ldg(v + k);
+            m = fmax(m, fmax(fabs(x.x), fabs(x.y)));
+        }
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) mB[it] = scale_exp((uint64_t)__double_as_longlong(m));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The GEMM
+// ---------------------------------------------------------------------------
+struct GemmArgs {
+    const int8_t* Aq;
+    const unsigned long long* mA;
+    const double2* V;   // x-hat (forward) / d-hat (adjoint): [f][ldr][K]
+    const int* mB;      // block exponents of V
+    double2* Y;         // [f][ldr][rows]
+    int nf, nd, nm;
+    int ldr, r0, nr;    // rhs stride, first rhs of this pass, rhs in this pass (<= 8 NG)
+    int IG, JG, nkbA;
+};
+
+template <bool ADJ, int NG>
+__global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
+    constexpr int NP = 16 * NG;  // MMA N (columns n' = 2r+q)
+    constexpr int NGRP = NP / 8;
+    constexpr int kBStage = 2 * NGRP * kPos;
+    constexpr uint32_t kTmemCols = kLevels * NP <= 128 ? 128 : kLevels * NP <= 256 ? 256 : 512;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* As = smem;                                 // [kStages][kAStage]
+    uint8_t* Bs = smem + kStages * kAStage;              // [kStages][kBStage]
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBStage);
+    uint64_t* empty = full + kStages;
+    uint64_t* acc_full = empty + kStages;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = ADJ ? g.nm : g.nd;
+    const int K = ADJ ? g.nd : g.nm;
+    const int mtiles = (rows + kTileM - 1) / kTileM;
+    const int nks = (K + 31) / 32;
+    const int nkb = (K + kChunk - 1) / kChunk;
+    const long long ntiles = (long long)g.nf * mtiles;
+
+    if (warp == 1) umma::tmem_alloc<kTmemCols>(tslot);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            umma::mbar_init(full + s, 1 + 128);
+            umma::mbar_init(empty + s, 1);
+        }
+        umma::mbar_init(acc_full, 1);
+        umma::mbar_init(acc_empty, 128);
+        umma::mbar_fence_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        // ===== TMA producer: F-hat slice tiles =====
+        if (lane == 0) {
+            const uint64_t pol = umma::policy_evict_first();
+            long long it = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int f = (int)(tile / mtiles), mt = (int)(tile % mtiles);
+                for (int ks = 0; ks < nks; ++ks, ++it) {
+                    const int st = (int)(it & 1);
+                    if (it >= kStages) umma::mbar_wait(empty + st, (uint32_t)(((it >> 1) - 1) & 1));
+                    uint8_t* dst = As + st * kAStage;
+                    const int8_t* base = g.Aq + (size_t)f * g.IG * g.JG * kPos;
+                    if (!ADJ) {
+                        const int ig0 = mt * 16, ig1 = min(g.IG, ig0 + 16);
+                        const int njg = min(2, g.JG - 2 * ks);
+                        const uint32_t bytes = (uint32_t)(njg * kPos);
+                        umma::mbar_expect_tx(full + st, bytes * (uint32_t)(ig1 - ig0));
+                        for (int ig = ig0; ig < ig1; ++ig)
+                            umma::bulk_load(dst + (ig - ig0) * 2 * kPos, base + ((size_t)ig * g.JG + 2 * ks) * kPos,
+                                            bytes, full + st, pol);
+                    } else {
+                        const int ig0 = 4 * ks, ig1 = min(g.IG, ig0 + 4);
+                        const int jg0 = mt * 8, njg = min(8, g.JG - jg0);
+                        const uint32_t bytes = (uint32_t)(njg * kPos);
+                        umma::mbar_expect_tx(full + st, bytes * (uint32_t)(ig1 - ig0));
+                        for (int ig = ig0; ig < ig1; ++ig)
+                            umma::bulk_load(dst + (ig - ig0) * 8 * kPos, base + ((size_t)ig * g.JG + jg0) * kPos,
+                                            bytes, full + st, pol);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t idesc = umma::idesc_s8(kTileM, NP, ADJ, false);
+            long long it = 0, chunks = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int ck = 0; ck < nkb; ++ck, ++chunks) {
+                    if (chunks > 0) umma::mbar_wait(acc_empty, (uint32_t)((chunks - 1) & 1));
+                    umma::fence_after_sync();
+                    const int ks1 = min(nks, (ck + 1) * kStepsPerChunk);
+                    for (int ks = ck * kStepsPerChunk; ks < ks1; ++ks, ++it) {
+                        const int st = (int)(it & 1);
+                        umma::mbar_wait(full + st, (uint32_t)((it >> 1) & 1));
+                        umma::fence_after_sync();
+                        const uint32_t a0 = umma::smem_u32(As + st * kAStage);
+                        const uint32_t b0 = umma::smem_u32(Bs + st * kBStage);
+                        const bool first_step = ks == ck * kStepsPerChunk;
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+#pragma unroll
+                            for (int s = 0; s < kS; ++s) {
+                                const uint64_t ad =
+                                    ADJ ? umma::make_desc(a0 + (s * 2 + c) * kCM, 8 * kPos, kPos)
+                                        : umma::make_desc(a0 + (s * 2 + c) * kCM, kPos, 2 * kPos);
+#pragma unroll
+                                for (int t = 0; t < kS - s; ++t) {  // level L = s + t + 2 <= S + 1
+                                    const uint64_t bd = umma::make_desc(b0 + (t * 2 + c) * kCM, NGRP * kPos, kPos);
+                                    const uint32_t acc = (first_step && c == 0 && s == 0) ? 0u : 1u;
+                                    umma::mma_s8(tmem + (uint32_t)((s + t) * NP), ad, bd, idesc, acc);
+                                }
+                            }
+                        umma::commit(empty + st);
+                    }
+                    umma::commit(acc_full);
+                }
+            }
+        }
+    } else {
+        // ===== B producers + epilogue (warps 2..5, 128 threads) =====
+        const int et = threadIdx.x - 64;     // 0..127
+        const int quarter = warp & 3;        // TMEM lane quarter this warp may access
+        const int trow = quarter * 32 + lane;
+        double acc[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) acc[q] = 0.0;
+
+        constexpr int kTotItems = 2 * (NP / 2) * 4;              // (kg, rr, quad) items per K step
+        constexpr int kItems = (kTotItems + 127) / 128;          // per thread
+        // chunk bookkeeping for interleaving drains with production
+        long long drained = 0;  // chunks drained so far (global count)
+        long long tile_of_drain = blockIdx.x;
+        int ck_of_drain = 0;
+        auto drain = [&]() {
+            const int f = (int)(tile_of_drain / mtiles), mt = (int)(tile_of_drain % mtiles);
+            umma::mbar_wait(acc_full, (uint32_t)(drained & 1));
+            umma::fence_after_sync();
+            const int ck = ck_of_drain;
+            const int ebA = ADJ ? scale_exp(g.mA[(size_t)f * g.nkbA + (mt * kTileM) / kChunk])
+                                : scale_exp(g.mA[(size_t)f * g.nkbA + ck]);
+            int ebB[NP / 2];
+#pragma unroll
+            for (int rr = 0; rr < NP / 2; ++rr)
+                ebB[rr] = rr < g.nr ? g.mB[((size_t)f * g.nr + rr) * nkb + ck] : 0;
+#pragma unroll
+            for (int cg = 0; cg < NP / 16; ++cg) {
+                double v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = 0.0;
+#pragma unroll
+                for (int L = 0; L < kLevels; ++L) {
+                    uint32_t r[16];
+                    umma::ld_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(L * NP + cg * 16), r);
+                    umma::ld_wait();
+                    const double w = pow2(-7 * (L + 2));
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = fma((double)(int)r[q], w, v[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int col = cg * 16 + q, rr = col >> 1;
+                    if (rr < g.nr) acc[col] = fma(v[q], pow2(ebA + ebB[rr]), acc[col]);
+                }
+            }
+            umma::fence_before_sync();
+            umma::mbar_arrive(acc_empty);
+            ++drained;
+            if (++ck_of_drain == nkb) {
+                // tile complete: store rows, reset
+                const int row = mt * kTileM + trow;
+                if (row < rows) {
+#pragma unroll
+                    for (int q = 0; q < NP; q += 2) {
+                        const int rr = q >> 1;
+                        if (rr < g.nr)
+                            g.Y[((size_t)f * g.ldr + g.r0 + rr) * rows + row] = make_double2(acc[q], acc[q + 1]);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < NP; ++q) acc[q] = 0.0;
+                ck_of_drain = 0;
+                tile_of_drain += gridDim.x;
+            }
+        };
+
+        // Step `it` may only wait for the MMAs of step it-2 after every chunk
+        // before that step's chunk has been drained (the MMA warp waits for it).
+        long long it = 0, chunk_idx = 0;  // chunk_idx: global index of the tile's first chunk
+        long long step_chunk[kStages] = {0, 0};
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int f = (int)(tile / mtiles);
+            for (int ks = 0; ks < nks; ++ks, ++it) {
+                const int st = (int)(it & 1);
+                if (it >= kStages)
+                    while (drained < step_chunk[st]) drain();
+                // issue this step's vector loads before waiting for the ring slot
+                const int k0 = ks * 32, ck = ks / kStepsPerChunk;
+                double2 xv[kItems][4];
+                double inv[kItems];
+#pragma unroll
+                for (int ii = 0; ii < kItems; ++ii) {
+                    const int item = et + ii * 128;
+                    const int quad = item & 3;
+                    const int rr = (item >> 2) % (NP / 2);
+                    const int kg = (item >> 2) / (NP / 2);
+                    const int k = k0 + kg * 16 + quad * 4;
+                    const bool live = rr < g.nr && item < kTotItems;
+                    inv[ii] = live ? pow2(-g.mB[((size_t)f * g.nr + rr) * nkb + ck]) : 0.0;
+                    const double2* src = g.V + ((size_t)f * g.ldr + g.r0 + (live ? rr : 0)) * K;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        xv[ii][u] = (live && k + u < K) ? __ldg(src + k + u) : make_double2(0.0, 0.0);
+                }
+                if (it >= kStages) umma::mbar_wait(empty + st, (uint32_t)(((it >> 1) - 1) & 1));
+                step_chunk[st] = chunk_idx + ks / kStepsPerChunk;
+                // slice V[f][r][k0 .. k0+32) into the B tile [kg 2][ngrp][t][c'][8][16]
+                uint8_t* bst = Bs + st * kBStage;
+#pragma unroll
+                for (int ii = 0; ii < kItems; ++ii) {
+                    const int item = et + ii * 128;  // (kg, rr, quad), quad fastest
+                    if (item >= kTotItems) break;
+                    const int quad = item & 3;
+                    const int rr = (item >> 2) % (NP / 2);
+                    const int kg = (item >> 2) / (NP / 2);
+                    double ur[4], ui[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        ur[u] = xv[ii][u].x * inv[ii];
+                        ui[u] = xv[ii][u].y * inv[ii];
+                    }
+                    uint8_t* cm = bst + (kg * NGRP + (rr >> 2)) * kPos + ((2 * rr) & 7) * 16 + quad * 4;
+#pragma unroll
+                    for (int s = 0; s < kS; ++s) {
+                        int a0 = digit(ur[0]), a1 = digit(ur[1]), a2 = digit(ur[2]), a3 = digit(ur[3]);
+                        int b0 = digit(ui[0]), b1 = digit(ui[1]), b2 = digit(ui[2]), b3 = digit(ui[3]);
+                        const uint32_t re = pack4(a0, a1, a2, a3), im = pack4(b0, b1, b2, b3);
+                        uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (s * 2 + 0) * kCM);
+                        uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (s * 2 + 1) * kCM);
+                        p0[0] = re;  // real plane row 2rr
+                        p0[4] = im;  // real plane row 2rr+1
+                        if (!ADJ) {  // imaginary plane: (-xi, xr)
+                            p1[0] = pack4(-b0, -b1, -b2, -b3);
+                            p1[4] = re;
+                        } else {  // imaginary plane: (di, -dr)
+                            p1[0] = im;
+                            p1[4] = pack4(-a0, -a1, -a2, -a3);
+                        }
+                    }
+                }
+                umma::fence_async_smem();
+                umma::mbar_arrive(full + st);
+            }
+            chunk_idx += nkb;
+        }
+        while (drained < chunk_idx) drain();
+    }
+
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) umma::tmem_free<kTmemCols>(tmem);
+}
+
+template <bool ADJ, int NG>
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
+    constexpr int kBStage = 2 * (16 * NG / 8) * kPos;
+    const size_t smem = (size_t)kStages * (kAStage + kBStage) + 8 * 8;
+    auto kern = k_oz_gemm<ADJ, NG>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int rows = ADJ ? a.nm : a.nd;
+    const long long tiles = (long long)a.nf * ((rows + kTileM - 1) / kTileM);
+    const int grid = (int)std::min<long long>(tiles, sms);
+    kern<<<grid, kThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace oz
+
+size_t oz_operator_bytes(int nf, int nd, int nm) {
+    return (size_t)nf * ((nd + 7) / 8) * ((nm + 15) / 16) * oz::kPos;
+}
+size_t oz_operator_scales(int nf, int nm) { return (size_t)nf * ((nm + oz::kChunk - 1) / oz::kChunk); }
+size_t oz_vector_scales(int nf, int nrhs, int kdim) {  // ints
+    return (size_t)nf * nrhs * ((kdim + oz::kChunk - 1) / oz::kChunk);
+}
+
+cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_t* Aq, unsigned long long* mA,
+                                 cudaStream_t stream) {
+    const int nkb = (nm + oz::kChunk - 1) / oz::kChunk;
+    cudaError_t e = cudaMemsetAsync(mA, 0, oz_operator_scales(nf, nm) * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    oz::k_scale_op<<<sms * 8, 256, 0, stream>>>(F, mA, nf, nd, nm, nkb);
+    const int IG = (nd + 7) / 8, JG = (nm + 15) / 16;
+    oz::k_slice_op<<<sms * 8, 256, 0, stream>>>(F, mA, Aq, nf, nd, nm, IG, JG, nkb);
+    return cudaGetLastError();
+}
+
+cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
+                     int nf, int nd, int nm, int nrhs, int* mB, cudaStream_t stream) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int K = adjoint ? nd : nm;
+    const int nkb = (K + oz::kChunk - 1) / oz::kChunk;
+    oz::GemmArgs a{};
+    a.Aq = Aq;
+    a.mA = mA;
+    a.V = V;
+    a.mB = mB;
+    a.Y = Y;
+    a.nf = nf;
+    a.nd = nd;
+    a.nm = nm;
+    a.ldr = nrhs;
+    a.IG = (nd + 7) / 8;
+    a.JG = (nm + 15) / 16;
+    a.nkbA = (nm + oz::kChunk - 1) / oz::kChunk;
+    for (int r0 = 0; r0 < nrhs; r0 += 32) {
+        const int nr = std::min(32, nrhs - r0);
+        a.r0 = r0;
+        a.nr = nr;
+        oz::k_scale_vec<<<sms * 8, 256, 0, stream>>>(V, mB, nf, nrhs, r0, nr, K, nkb);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const int ng = (nr + 7) / 8;  // N' = 16 ng columns
+        switch (ng * 2 + (adjoint ? 1 : 0)) {
+            case 2: e = oz::launch_gemm<false, 1>(a, stream); break;
+            case 3: e = oz::launch_gemm<true, 1>(a, stream); break;
+            case 4: e = oz::launch_gemm<false, 2>(a, stream); break;
+            case 5: e = oz::launch_gemm<true, 2>(a, stream); break;
+            case 6: e = oz::launch_gemm<false, 3>(a, stream); break;
+            case 7: e = oz::launch_gemm<true, 3>(a, stream); break;
+            case 8: e = oz::launch_gemm<false, 4>(a, stream); break;
+            default: e = oz::launch_gemm<true, 4>(a, stream); break;
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace btg
