@@ -30,10 +30,15 @@
 // [Re Y, Im Y] interleaved.
 //
 // Kernel roles (192 threads, one CTA per SM, persistent over (f, row-tile)):
-//   warp 0     TMA producer of the F-hat slice tiles (cp.async.bulk, 2-stage ring)
-//   warp 1     TMEM owner + single-thread MMA issuer (56 MMAs per 32-wide K step)
-//   warps 2-5  slice the FP64 vector block of each K step into the B tile
-//              (shared memory), and drain the TMEM level accumulators into FP64
+//   warp 0     TMA producer of the F-hat slice tiles (cp.async.bulk ring, 2-3 stages)
+//   warp 1     TMEM owner + single-thread MMA issuer. B is stored slice after
+//              slice with a uniform 8-row stride, so A slice s meets the B
+//              slices t = 0..S-1-s in ONE descriptor window (N = NP (S-s), split
+//              at 256) whose products land in the consecutive level accumulators
+//              s + t: 20 MMAs per 32-wide K step at N = 64 (instead of 56 small ones).
+//   warps 2-5  prefetch the FP64 vector block of step it+2 (cp.async into a
+//              thread-private ring), slice step it into the B tile (shared
+//              memory), and drain the TMEM level accumulators into FP64
 //              registers at the end of every 1024-wide K chunk.
 #include <cuda_runtime.h>
 
@@ -53,10 +58,34 @@ constexpr int kPos = kS * 2 * kCM;          // bytes per core-matrix position (a
 constexpr int kChunk = 1024;                // K entries per int32 accumulation chunk / scale block
 constexpr int kStepsPerChunk = kChunk / 32;
 constexpr int kTileM = 128;
-constexpr int kStages = 2;
+constexpr int kBStages = 2;                 // sliced-vector ring (B producers)
+constexpr size_t kSmemMax = 232448;
 constexpr int kThreads = 192;
 constexpr int kAStage = 16 * 2 * kPos;      // forward: 16 ig x 2 jg; adjoint: 4 ig x 8 jg (same size)
 constexpr int kBStageMax = 2 * 8 * kPos;    // 2 K-groups x up to 8 n'-groups
+constexpr int kVAhead = 2;                  // vector prefetch distance (steps)
+constexpr int kVSlots = kVAhead + 1;
+// Per-step vector staging: (kg, rr, quad) items, 4 complex + 1 exponent each, per B-producer thread.
+template <int NG>
+__host__ __device__ constexpr int VItems() { return (64 * NG + 127) / 128; }
+template <int NG>
+__host__ __device__ constexpr int VSlotBytes() { return VItems<NG>() * 128 * (4 * 16 + 4); }
+constexpr size_t kBarBytes = 16 * 8;
+template <int NG>
+__host__ __device__ constexpr size_t RingBytes(int a_stages) {
+    return (size_t)a_stages * kAStage + (size_t)kBStages * 2 * (16 * NG / 8) * kPos;
+}
+// F-hat slice ring depth (TMA): 3 stages when they fit beside the vector
+// prefetch ring, else 2 (the vector prefetch matters more: ncu shows the B
+// producers stalled on vector loads without it).
+template <int NG>
+__host__ __device__ constexpr int AStages() {
+    return RingBytes<NG>(3) + (size_t)kVSlots * VSlotBytes<NG>() + kBarBytes <= kSmemMax ? 3 : 2;
+}
+template <int NG>
+__host__ __device__ constexpr size_t GemmSmemBytes() {
+    return RingBytes<NG>(AStages<NG>()) + (size_t)kVSlots * VSlotBytes<NG>() + kBarBytes;
+}
 
 // Block exponent e with max < 2^{e-1} (so every scaled entry lies in (-1/2, 1/2)).
 __device__ __forceinline__ int scale_exp(uint64_t maxbits) {
@@ -205,11 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
     constexpr int kBStage = 2 * NGRP * kPos;
     constexpr uint32_t kTmemCols = kLevels * NP <= 128 ? 128 : kLevels * NP <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* As = smem;                                 // [kStages][kAStage]
-    uint8_t* Bs = smem + kStages * kAStage;              // [kStages][kBStage]
-    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBStage);
-    uint64_t* empty = full + kStages;
-    uint64_t* acc_full = empty + kStages;
+    constexpr bool kVRing = true;
+    constexpr int kAStages = AStages<NG>();
+    uint8_t* As = smem;                                 // [kAStages][kAStage]
+    uint8_t* Bs = smem + kAStages * kAStage;             // [kBStages][kBStage]
+    uint8_t* Vs = Bs + kBStages * kBStage;               // [kVSlots][VSlotBytes] (kVRing)
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + GemmSmemBytes<NG>() - kBarBytes);
+    uint64_t* emptyA = fullA + kAStages;
+    uint64_t* fullB = emptyA + kAStages;
+    uint64_t* emptyB = fullB + kBStages;
+    uint64_t* acc_full = emptyB + kBStages;
     uint64_t* acc_empty = acc_full + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
@@ -223,9 +257,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
 
     if (warp == 1) umma::tmem_alloc<kTmemCols>(tslot);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            umma::mbar_init(full + s, 1 + 128);
-            umma::mbar_init(empty + s, 1);
+        for (int s = 0; s < kAStages; ++s) {
+            umma::mbar_init(fullA + s, 1);
+            umma::mbar_init(emptyA + s, 1);
+        }
+        for (int s = 0; s < kBStages; ++s) {
+            umma::mbar_init(fullB + s, 128);
+            umma::mbar_init(emptyB + s, 1);
         }
         umma::mbar_init(acc_full, 1);
         umma::mbar_init(acc_empty, 128);
@@ -244,26 +282,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 const int f = (int)(tile / mtiles), mt = (int)(tile % mtiles);
                 for (int ks = 0; ks < nks; ++ks, ++it) {
-                    const int st = (int)(it & 1);
-                    if (it >= kStages) umma::mbar_wait(empty + st, (uint32_t)(((it >> 1) - 1) & 1));
+                    const int st = (int)(it % kAStages);
+                    if (it >= kAStages) umma::mbar_wait(emptyA + st, (uint32_t)(((it / kAStages) - 1) & 1));
                     uint8_t* dst = As + st * kAStage;
                     const int8_t* base = g.Aq + (size_t)f * g.IG * g.JG * kPos;
                     if (!ADJ) {
                         const int ig0 = mt * 16, ig1 = min(g.IG, ig0 + 16);
                         const int njg = min(2, g.JG - 2 * ks);
                         const uint32_t bytes = (uint32_t)(njg * kPos);
-                        umma::mbar_expect_tx(full + st, bytes * (uint32_t)(ig1 - ig0));
+                        umma::mbar_expect_tx(fullA + st, bytes * (uint32_t)(ig1 - ig0));
                         for (int ig = ig0; ig < ig1; ++ig)
                             umma::bulk_load(dst + (ig - ig0) * 2 * kPos, base + ((size_t)ig * g.JG + 2 * ks) * kPos,
-                                            bytes, full + st, pol);
+                                            bytes, fullA + st, pol);
                     } else {
                         const int ig0 = 4 * ks, ig1 = min(g.IG, ig0 + 4);
                         const int jg0 = mt * 8, njg = min(8, g.JG - jg0);
                         const uint32_t bytes = (uint32_t)(njg * kPos);
-                        umma::mbar_expect_tx(full + st, bytes * (uint32_t)(ig1 - ig0));
+                        umma::mbar_expect_tx(fullA + st, bytes * (uint32_t)(ig1 - ig0));
                         for (int ig = ig0; ig < ig1; ++ig)
                             umma::bulk_load(dst + (ig - ig0) * 8 * kPos, base + ((size_t)ig * g.JG + jg0) * kPos,
-                                            bytes, full + st, pol);
+                                            bytes, fullA + st, pol);
                     }
                 }
             }
@@ -271,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            const uint32_t idesc = umma::idesc_s8(kTileM, NP, ADJ, false);
+            constexpr int kPiece = 256 / NP;  // B slices per MMA (N <= 256)
             long long it = 0, chunks = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int ck = 0; ck < nkb; ++ck, ++chunks) {
@@ -279,11 +317,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                     umma::fence_after_sync();
                     const int ks1 = min(nks, (ck + 1) * kStepsPerChunk);
                     for (int ks = ck * kStepsPerChunk; ks < ks1; ++ks, ++it) {
-                        const int st = (int)(it & 1);
-                        umma::mbar_wait(full + st, (uint32_t)((it >> 1) & 1));
+                        const int sa = (int)(it % kAStages), sb = (int)(it % kBStages);
+                        umma::mbar_wait(fullA + sa, (uint32_t)((it / kAStages) & 1));
+                        umma::mbar_wait(fullB + sb, (uint32_t)((it / kBStages) & 1));
                         umma::fence_after_sync();
-                        const uint32_t a0 = umma::smem_u32(As + st * kAStage);
-                        const uint32_t b0 = umma::smem_u32(Bs + st * kBStage);
+                        const uint32_t a0 = umma::smem_u32(As + sa * kAStage);
+                        const uint32_t b0 = umma::smem_u32(Bs + sb * kBStage);
                         const bool first_step = ks == ck * kStepsPerChunk;
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
@@ -292,14 +331,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                                 const uint64_t ad =
                                     ADJ ? umma::make_desc(a0 + (s * 2 + c) * kCM, 8 * kPos, kPos)
                                         : umma::make_desc(a0 + (s * 2 + c) * kCM, kPos, 2 * kPos);
+                                // A slice s against the B slices t = 0 .. S-1-s at once: the
+                                // B planes are stored slice after slice with a uniform 8-row
+                                // stride, so one descriptor spans several slices and the
+                                // products land in consecutive level accumulators (s + t).
 #pragma unroll
-                                for (int t = 0; t < kS - s; ++t) {  // level L = s + t + 2 <= S + 1
-                                    const uint64_t bd = umma::make_desc(b0 + (t * 2 + c) * kCM, NGRP * kPos, kPos);
+                                for (int t0 = 0; t0 < kS - s; t0 += kPiece) {
+                                    const int ns = (kS - s - t0) < kPiece ? (kS - s - t0) : kPiece;
+                                    const uint64_t bd =
+                                        umma::make_desc(b0 + (c * kS + t0) * NGRP * 256, 128, 256);
                                     const uint32_t acc = (first_step && c == 0 && s == 0) ? 0u : 1u;
-                                    umma::mma_s8(tmem + (uint32_t)((s + t) * NP), ad, bd, idesc, acc);
+                                    umma::mma_s8(tmem + (uint32_t)((s + t0) * NP), ad, bd,
+                                                 umma::idesc_s8(kTileM, ns * NP, ADJ, false), acc);
                                 }
                             }
-                        umma::commit(empty + st);
+                        umma::commit(emptyA + sa);
+                        umma::commit(emptyB + sb);
                     }
                     umma::commit(acc_full);
                 }
@@ -315,7 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
         for (int q = 0; q < NP; ++q) acc[q] = 0.0;
 
         constexpr int kTotItems = 2 * (NP / 2) * 4;              // (kg, rr, quad) items per K step
-        constexpr int kItems = (kTotItems + 127) / 128;          // per thread
+        constexpr int kItems = VItems<NG>();                      // per thread
+        static_assert(kItems == (kTotItems + 127) / 128, "item count");
         // chunk bookkeeping for interleaving drains with production
         long long drained = 0;  // chunks drained so far (global count)
         long long tile_of_drain = blockIdx.x;
@@ -372,38 +420,97 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
             }
         };
 
-        // Step `it` may only wait for the MMAs of step it-2 after every chunk
-        // before that step's chunk has been drained (the MMA warp waits for it).
+        // With kVRing, the vector data of step `itp` is fetched kVAhead steps early
+        // with per-thread cp.async into a ring of thread-private shared slots: each
+        // thread later reads back exactly the 16-byte words it copied (no
+        // cross-thread sync). Otherwise the loads go to registers right before the
+        // ring-slot wait.
+        auto item_pos = [&](int ii, int k0, int& rr, int& k, bool& live) {
+            const int item = et + ii * 128;
+            const int quad = item & 3;
+            rr = (item >> 2) % (NP / 2);
+            const int kg = (item >> 2) / (NP / 2);
+            k = k0 + kg * 16 + quad * 4;
+            live = rr < g.nr && item < kTotItems;
+        };
+        auto prefetch = [&](long long itp) {
+            const long long tl = (long long)blockIdx.x + (itp / nks) * gridDim.x;
+            if (tl < ntiles) {
+                const int f = (int)(tl / mtiles), ks = (int)(itp % nks);
+                const int ck = ks / kStepsPerChunk;
+                uint8_t* slot = Vs + (int)(itp % kVSlots) * VSlotBytes<NG>();
+#pragma unroll
+                for (int ii = 0; ii < kItems; ++ii) {
+                    int rr, k;
+                    bool live;
+                    item_pos(ii, ks * 32, rr, k, live);
+                    if (!live) continue;
+                    umma::cp_async4(slot + kItems * 4 * 16 * 128 + (ii * 128 + et) * 4,
+                                    g.mB + ((size_t)f * g.nr + rr) * nkb + ck);
+                    const double2* src = g.V + ((size_t)f * g.ldr + g.r0 + rr) * K + k;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (k + u < K) umma::cp_async16(slot + ((ii * 4 + u) * 128 + et) * 16, src + u);
+                }
+            }
+            umma::cp_async_commit();  // one group per step, empty past the end
+        };
+
+        // Step `it` may only wait for the MMAs of step it-kBStages after every
+        // chunk before that step's chunk has been drained (the MMA warp waits for it).
         long long it = 0, chunk_idx = 0;  // chunk_idx: global index of the tile's first chunk
-        long long step_chunk[kStages] = {0, 0};
+        long long step_chunk[kBStages] = {};
+        if constexpr (kVRing) {
+#pragma unroll
+            for (int a = 0; a < kVAhead; ++a) prefetch(a);
+        }
         for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int f = (int)(tile / mtiles);
             for (int ks = 0; ks < nks; ++ks, ++it) {
-                const int st = (int)(it & 1);
-                if (it >= kStages)
-                    while (drained < step_chunk[st]) drain();
-                // issue this step's vector loads before waiting for the ring slot
-                const int k0 = ks * 32, ck = ks / kStepsPerChunk;
+                const int sb = (int)(it % kBStages);
+                if (it >= kBStages)
+                    while (drained < step_chunk[sb]) drain();
+                const int k0 = ks * 32;
                 double2 xv[kItems][4];
                 double inv[kItems];
+                if constexpr (kVRing) {
+                    prefetch(it + kVAhead);
+                } else {
+                    const int ck = ks / kStepsPerChunk;
 #pragma unroll
-                for (int ii = 0; ii < kItems; ++ii) {
-                    const int item = et + ii * 128;
-                    const int quad = item & 3;
-                    const int rr = (item >> 2) % (NP / 2);
-                    const int kg = (item >> 2) / (NP / 2);
-                    const int k = k0 + kg * 16 + quad * 4;
-                    const bool live = rr < g.nr && item < kTotItems;
-                    inv[ii] = live ? pow2(-g.mB[((size_t)f * g.nr + rr) * nkb + ck]) : 0.0;
-                    const double2* src = g.V + ((size_t)f * g.ldr + g.r0 + (live ? rr : 0)) * K;
+                    for (int ii = 0; ii < kItems; ++ii) {
+                        int rr, k;
+                        bool live;
+                        item_pos(ii, k0, rr, k, live);
+                        inv[ii] = live ? pow2(-g.mB[((size_t)f * g.nr + rr) * nkb + ck]) : 0.0;
+                        const double2* src = g.V + ((size_t)f * g.ldr + g.r0 + (live ? rr : 0)) * K;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        xv[ii][u] = (live && k + u < K) ? __ldg(src + k + u) : make_double2(0.0, 0.0);
+                        for (int u = 0; u < 4; ++u)
+                            xv[ii][u] = (live && k + u < K) ? __ldg(src + k + u) : make_double2(0.0, 0.0);
+                    }
                 }
-                if (it >= kStages) umma::mbar_wait(empty + st, (uint32_t)(((it >> 1) - 1) & 1));
-                step_chunk[st] = chunk_idx + ks / kStepsPerChunk;
-                // slice V[f][r][k0 .. k0+32) into the B tile [kg 2][ngrp][t][c'][8][16]
-                uint8_t* bst = Bs + st * kBStage;
+                if (it >= kBStages) umma::mbar_wait(emptyB + sb, (uint32_t)(((it / kBStages) - 1) & 1));
+                step_chunk[sb] = chunk_idx + ks / kStepsPerChunk;
+                if constexpr (kVRing) {
+                    umma::cp_async_wait<kVAhead>();  // this step's group has landed
+                    const uint8_t* slot = Vs + (int)(it % kVSlots) * VSlotBytes<NG>();
+#pragma unroll
+                    for (int ii = 0; ii < kItems; ++ii) {
+                        int rr, k;
+                        bool live;
+                        item_pos(ii, k0, rr, k, live);
+                        inv[ii] = live ? pow2(-*reinterpret_cast<const int*>(slot + kItems * 4 * 16 * 128 +
+                                                                             (ii * 128 + et) * 4))
+                                       : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            xv[ii][u] = (live && k + u < K) ? *reinterpret_cast<const double2*>(
+                                                                  slot + ((ii * 4 + u) * 128 + et) * 16)
+                                                            : make_double2(0.0, 0.0);
+                    }
+                }
+                // slice V[f][r][k0 .. k0+32) into the B tile
+                uint8_t* bst = Bs + sb * kBStage;
 #pragma unroll
                 for (int ii = 0; ii < kItems; ++ii) {
                     const int item = et + ii * 128;  // (kg, rr, quad), quad fastest
@@ -417,14 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                         ur[u] = xv[ii][u].x * inv[ii];
                         ui[u] = xv[ii][u].y * inv[ii];
                     }
-                    uint8_t* cm = bst + (kg * NGRP + (rr >> 2)) * kPos + ((2 * rr) & 7) * 16 + quad * 4;
+                    // B tile [c][t][n-group][kg][8 rows][16 B]
+                    uint8_t* cm = bst + (rr >> 2) * 256 + kg * 128 + ((2 * rr) & 7) * 16 + quad * 4;
 #pragma unroll
                     for (int s = 0; s < kS; ++s) {
                         int a0 = digit(ur[0]), a1 = digit(ur[1]), a2 = digit(ur[2]), a3 = digit(ur[3]);
                         int b0 = digit(ui[0]), b1 = digit(ui[1]), b2 = digit(ui[2]), b3 = digit(ui[3]);
                         const uint32_t re = pack4(a0, a1, a2, a3), im = pack4(b0, b1, b2, b3);
-                        uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (s * 2 + 0) * kCM);
-                        uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (s * 2 + 1) * kCM);
+                        uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (0 * kS + s) * NGRP * 256);
+                        uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (1 * kS + s) * NGRP * 256);
                         p0[0] = re;  // real plane row 2rr
                         p0[4] = im;  // real plane row 2rr+1
                         if (!ADJ) {  // imaginary plane: (-xi, xr)
@@ -437,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                     }
                 }
                 umma::fence_async_smem();
-                umma::mbar_arrive(full + st);
+                umma::mbar_arrive(fullB + sb);
             }
             chunk_idx += nkb;
         }
@@ -451,8 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
 
 template <bool ADJ, int NG>
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
-    constexpr int kBStage = 2 * (16 * NG / 8) * kPos;
-    const size_t smem = (size_t)kStages * (kAStage + kBStage) + 8 * 8;
+    constexpr size_t smem = GemmSmemBytes<NG>();
+    static_assert(smem <= 232448, "shared memory");
     auto kern = k_oz_gemm<ADJ, NG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
