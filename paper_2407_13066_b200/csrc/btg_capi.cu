@@ -253,6 +253,9 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
     op->counters.launches++;
     op->counters.forward_fft.ops += fft_ops(channels, op->nt);
     op->counters.forward_fft.bytes += 8.0 * channels * op->nt + 16.0 * op->nf * channels;
+    // the zero-pad is fused into the R2C loads: the reference's op model
+    // (block_operator.cpp:67-68), no separate bytes moved
+    op->counters.pad.ops += 2.0 * channels * op->nt;
     return BTG_OK;
 }
 
@@ -269,6 +272,8 @@ btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* ou
     op->counters.launches++;
     op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
     op->counters.inverse_fft.bytes += 16.0 * op->nf * channels + 8.0 * channels * op->nt;
+    // unpad fused into the C2R stores (block_operator.cpp:105-106 op model)
+    op->counters.unpad.ops += 2.0 * channels * op->nt;
     return BTG_OK;
 }
 
