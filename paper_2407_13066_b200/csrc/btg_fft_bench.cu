@@ -1,0 +1,126 @@
+// Development micro-benchmark for the vector transforms K5 (R2C) / K9 (C2R):
+// times the compile-time-N kernels on C channels with CUDA events and checks
+// the round trip C2R(R2C(x)) == x. Not part of the product library.
+//   btg_fft_bench [N_t=1024] [channels=524288] [reps=10]
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "btg_fft_fast.cuh"
+
+using namespace btg;
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) {                                                                \
+            std::printf("{\"error\": \"%s at %s:%d\"}\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            std::exit(1);                                                                       \
+        }                                                                                       \
+    } while (0)
+
+static double2 root(long long num, long long den) {
+    num %= den;
+    if (num < 0) num += den;
+    const long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)num / (long double)den;
+    return make_double2((double)cosl(a), (double)(-sinl(a)));
+}
+
+template <int N>
+struct Run {
+    static void go(int C, int reps) {
+        using P = fast::FastPlan<N>;
+        constexpr int CPB = P::CPB;
+        const int hi = fast::tw_hi_count<N>();
+        std::vector<double2> t(32 + hi + 32 + hi + 1);
+        for (int i = 0; i < 32; ++i) t[i] = root(i, N);
+        for (int h = 0; h < hi; ++h) t[32 + h] = root(32LL * h, N);
+        for (int i = 0; i < 32; ++i) t[32 + hi + i] = root(i, 2LL * N);
+        for (int h = 0; h <= hi; ++h) t[64 + hi + h] = root(32LL * h, 2LL * N);
+        double2* dt;
+        CK(cudaMalloc(&dt, t.size() * sizeof(double2)));
+        CK(cudaMemcpy(dt, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        FastTables tabs{dt, dt + 32, dt + 32 + hi, dt + 64 + hi};
+
+        const size_t nx = (size_t)C * N, nf = (size_t)(N + 1) * C;
+        double *x, *y;
+        double2* X;
+        CK(cudaMalloc(&x, nx * 8));
+        CK(cudaMalloc(&y, nx * 8));
+        CK(cudaMalloc(&X, nf * 16));
+        std::vector<double> hx(nx);
+        srand(7);
+        for (size_t i = 0; i < nx; ++i) hx[i] = (double)rand() / RAND_MAX - 0.5;
+        CK(cudaMemcpy(x, hx.data(), nx * 8, cudaMemcpyHostToDevice));
+
+        auto r2c = fast::k_r2c_fast<N, CPB>;
+        auto c2r = fast::k_c2r_fast<N, CPB>;
+        constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int grid = (C + CPB - 1) / CPB;
+        C2REpilogue epi{};
+        cudaEvent_t e0, e1, e2;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventCreate(&e2);
+        float tr = 0, tc = 0;
+        for (int r = -2; r < reps; ++r) {
+            cudaEventRecord(e0);
+            r2c<<<grid, P::TPC * CPB, smem>>>(x, N, X, C, C, tabs);
+            cudaEventRecord(e1);
+            c2r<<<grid, P::TPC * CPB, smem>>>(X, C, y, N, C, tabs, epi);
+            cudaEventRecord(e2);
+            CK(cudaEventSynchronize(e2));
+            float a, b;
+            cudaEventElapsedTime(&a, e0, e1);
+            cudaEventElapsedTime(&b, e1, e2);
+            if (r >= 0) {
+                tr += a;
+                tc += b;
+            }
+        }
+        CK(cudaGetLastError());
+        std::vector<double> hy(nx);
+        CK(cudaMemcpy(hy.data(), y, nx * 8, cudaMemcpyDeviceToHost));
+        double num = 0, den = 0;
+        for (size_t i = 0; i < nx; ++i) {
+            num += (hy[i] - hx[i]) * (hy[i] - hx[i]);
+            den += hx[i] * hx[i];
+        }
+        tr /= reps;
+        tc /= reps;
+        const double bytes = 8.0 * nx + 16.0 * nf;
+        std::printf(
+            "{\"N_t\": %d, \"channels\": %d, \"cpb\": %d, \"r2c_ms\": %.4f, \"r2c_tbs\": %.3f, \"c2r_ms\": %.4f, "
+            "\"c2r_tbs\": %.3f, \"roundtrip_rel_l2\": %.3e}\n",
+            N, C, CPB, tr, bytes / tr / 1e9, tc, bytes / tc / 1e9, std::sqrt(num / den));
+        cudaFree(x);
+        cudaFree(y);
+        cudaFree(X);
+        cudaFree(dt);
+    }
+};
+
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? std::atoi(argv[1]) : 1024;
+    const int C = argc > 2 ? std::atoi(argv[2]) : 524288;
+    const int reps = argc > 3 ? std::atoi(argv[3]) : 10;
+    switch (n) {
+        case 64: Run<64>::go(C, reps); break;
+        case 128: Run<128>::go(C, reps); break;
+        case 256: Run<256>::go(C, reps); break;
+        case 500: Run<500>::go(C, reps); break;
+        case 512: Run<512>::go(C, reps); break;
+        case 1000: Run<1000>::go(C, reps); break;
+        case 1024: Run<1024>::go(C, reps); break;
+        case 2000: Run<2000>::go(C, reps); break;
+        case 2048: Run<2048>::go(C, reps); break;
+        case 4096: Run<4096>::go(C, reps); break;
+        default: std::printf("{\"error\": \"unsupported N_t %d\"}\n", n); return 1;
+    }
+    return 0;
+}

@@ -39,30 +39,55 @@
 namespace btg {
 namespace fast {
 
+// Plans: TPC threads per channel, default CPB channels per CTA, pass radices
+// for R2C (small radix last: it runs on butterfly pairs) and C2R (small first),
+// and the resident threads per SM each direction is compiled for (register
+// budget = 64K / RES): measured on B200 (profiles/r01s2_fft_sweep.md) — the
+// longer transforms prefer fewer, fatter threads, most of all the C2R.
 template <int... Rs>
 struct Radices {};
-
-// Plans: TPC threads per channel, default CPB channels per CTA, pass radices
-// for R2C (small radix last: it runs on butterfly pairs) and C2R (small first).
 template <int N>
 struct FastPlan;
-template <> struct FastPlan<64>   { static constexpr int TPC = 8,   CPB = 32; using R2C = Radices<16, 4>;        using C2R = Radices<4, 16>; };
-template <> struct FastPlan<128>  { static constexpr int TPC = 16,  CPB = 16; using R2C = Radices<8, 4, 4>;      using C2R = Radices<4, 4, 8>; };
-template <> struct FastPlan<256>  { static constexpr int TPC = 16,  CPB = 16; using R2C = Radices<16, 4, 4>;     using C2R = Radices<4, 4, 16>; };
-template <> struct FastPlan<500>  { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<4, 5, 5, 5>;   using C2R = Radices<5, 5, 5, 4>; };
-template <> struct FastPlan<512>  { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<16, 8, 4>;     using C2R = Radices<4, 8, 16>; };
-template <> struct FastPlan<1000> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<8, 5, 5, 5>;   using C2R = Radices<5, 5, 5, 8>; };
-template <> struct FastPlan<1024> { static constexpr int TPC = 64,  CPB = 4;  using R2C = Radices<16, 16, 4>;    using C2R = Radices<4, 16, 16>; };
-template <> struct FastPlan<2000> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 5, 5, 5>;  using C2R = Radices<5, 5, 5, 16>; };
-template <> struct FastPlan<2048> { static constexpr int TPC = 128, CPB = 2;  using R2C = Radices<16, 8, 4, 4>;  using C2R = Radices<4, 4, 8, 16>; };
-template <> struct FastPlan<4096> { static constexpr int TPC = 256, CPB = 1;  using R2C = Radices<16, 16, 4, 4>; using C2R = Radices<4, 4, 16, 16>; };
+#define BTG_PLAN(N, tpc, cpb, res_r2c, res_c2r, R2CL, C2RL)                                    \
+    template <>                                                                                  \
+    struct FastPlan<N> {                                                                         \
+        static constexpr int TPC = tpc, CPB = cpb, RES_R2C = res_r2c, RES_C2R = res_c2r;         \
+        using R2C = R2CL;                                                                        \
+        using C2R = C2RL;                                                                        \
+    };
+#define BTG_R(...) Radices<__VA_ARGS__>
+BTG_PLAN(64,    8,   32, 768,  768,  BTG_R(16, 4),           BTG_R(4, 16))
+BTG_PLAN(128,   16,  16, 1024, 1024, BTG_R(8, 4, 4),         BTG_R(4, 4, 8))
+BTG_PLAN(256,   16,  16, 512,  512,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
+BTG_PLAN(500,   64,  4,  1024, 768,  BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
+BTG_PLAN(512,   64,  4,  256,  768,  BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
+BTG_PLAN(1000,  128, 2,  1024, 1024, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
+BTG_PLAN(1024,  64,  4,  768,  256,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
+BTG_PLAN(2000,  128, 2,  512,  384,  BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
+BTG_PLAN(2048,  128, 2,  512,  256,  BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
+BTG_PLAN(4096,  256, 1,  512,  256,  BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
 // long horizons: the paper's N_t = 10000 runs and 2^13
-template <> struct FastPlan<8192>  { static constexpr int TPC = 512, CPB = 1;  using R2C = Radices<16, 16, 8, 4>;    using C2R = Radices<4, 8, 16, 16>; };
-template <> struct FastPlan<10000> { static constexpr int TPC = 625, CPB = 1;  using R2C = Radices<16, 5, 5, 5, 5>; using C2R = Radices<5, 5, 5, 5, 16>; };
+BTG_PLAN(8192,  512, 1,  768,  768,  BTG_R(16, 16, 8, 4),    BTG_R(4, 8, 16, 16))
+BTG_PLAN(10000, 625, 1,  768,  768,  BTG_R(16, 5, 5, 5, 5),  BTG_R(5, 5, 5, 5, 16))
+#undef BTG_R
+#undef BTG_PLAN
 
-// Register budget: aim for 768 resident threads per SM (<= 85 registers).
+// Minimum CTAs per SM for __launch_bounds__ from a resident-thread target.
+// BTG_FFT_RESIDENT_THREADS (sweeps) overrides every plan.
+constexpr int min_blocks(int res, int cta_threads) {
+    return res / cta_threads < 1 ? 1 : (res / cta_threads > 16 ? 16 : res / cta_threads);
+}
+#ifdef BTG_FFT_RESIDENT_THREADS
 template <int N, int CPB>
-constexpr int kMinBlocks = (768 / (FastPlan<N>::TPC * CPB)) < 1 ? 1 : ((768 / (FastPlan<N>::TPC * CPB)) > 16 ? 16 : (768 / (FastPlan<N>::TPC * CPB)));
+constexpr int kMinBlocksR2C = min_blocks(BTG_FFT_RESIDENT_THREADS, FastPlan<N>::TPC * CPB);
+template <int N, int CPB>
+constexpr int kMinBlocksC2R = min_blocks(BTG_FFT_RESIDENT_THREADS, FastPlan<N>::TPC * CPB);
+#else
+template <int N, int CPB>
+constexpr int kMinBlocksR2C = min_blocks(FastPlan<N>::RES_R2C, FastPlan<N>::TPC * CPB);
+template <int N, int CPB>
+constexpr int kMinBlocksC2R = min_blocks(FastPlan<N>::RES_C2R, FastPlan<N>::TPC * CPB);
+#endif
 
 __host__ __device__ constexpr int pad_idx(int p) { return p + (p >> 4); }
 __host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }
@@ -223,11 +248,30 @@ __device__ __forceinline__ double2 presplit_z(double2 xk, double2 xn, double2 w,
 // W_{2N}^{N-k} = -conj(W_{2N}^k)
 __device__ __forceinline__ double2 partner_w(double2 w) { return make_double2(-w.x, w.y); }
 
+// Both members of a split pair with ONE complex product (bit-identical to
+// split_x(zk, zn, w) and split_x(zn, zk, partner_w(w))): with A = Z_k + conj Z_{N-k},
+// B = Z_k - conj Z_{N-k}:  X_k = (A - i wB)/2,  X_{N-k} = conj((A + i wB)/2).
+__device__ __forceinline__ void split_pair(double2 zk, double2 zn, double2 w, double2& xk, double2& xn) {
+    const double ax = zk.x + zn.x, ay = zk.y - zn.y;
+    const double2 wb = cmul(w, make_double2(zk.x - zn.x, zk.y + zn.y));
+    xk = make_double2(0.5 * (ax + wb.y), 0.5 * (ay - wb.x));
+    xn = make_double2(0.5 * (ax - wb.y), 0.5 * (-ay - wb.x));
+}
+// Inverse pair (bit-identical to presplit_z(xk, xn, w, s), presplit_z(xn, xk, partner_w(w), s)):
+// with c = conj(w) B:  Z_k = s (A + i c),  Z_{N-k} = s conj(A - i c).
+__device__ __forceinline__ void presplit_pair(double2 xk, double2 xn, double2 w, double inv_len, double2& zk,
+                                              double2& zn) {
+    const double ax = xk.x + xn.x, ay = xk.y - xn.y;
+    const double2 c = cmul(make_double2(xk.x - xn.x, xk.y + xn.y), cconj(w));
+    zk = make_double2(inv_len * (ax - c.y), inv_len * (ay + c.x));
+    zn = make_double2(inv_len * (ax + c.y), inv_len * (-ay + c.x));
+}
+
 // ---------------------------------------------------------------------------
 // r2c: SOTI rows (time contiguous) -> frequency-major out[k*out_fs + c]
 // ---------------------------------------------------------------------------
 template <int N, int CPB>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     k_r2c_fast(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
                int channels, FastTables tabs) {
     using P = FastPlan<N>;
@@ -308,9 +352,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
             for (int q = 0; q < R; ++q) {
                 const int k = ja + q * NB;
                 const double2 w = tw_lookup<-1>(plo, phi, k);
-                const double2 zk = va[q], zn = vb[R - 1 - q];
-                orow[(long long)k * out_fs] = split_x(zk, zn, w);
-                orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+                double2 xk, xn;
+                split_pair(va[q], vb[R - 1 - q], w, xk, xn);
+                orow[(long long)k * out_fs] = xk;
+                orow[(long long)(N - k) * out_fs] = xn;
             }
         } else {
             // butterfly 0: positions q NB pair with ((R - q) % R) NB; q = 0 gives X_0 and X_N
@@ -320,9 +365,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
                 if (q > qp && q != 0) continue;
                 const int k = q * NB;
                 const double2 w = tw_lookup<-1>(plo, phi, k);
-                const double2 zk = va[q], zn = va[qp];
-                orow[(long long)k * out_fs] = split_x(zk, zn, w);
-                if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+                double2 xk, xn;
+                split_pair(va[q], va[qp], w, xk, xn);
+                orow[(long long)k * out_fs] = xk;
+                if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
             }
             // butterfly NB/2: positions NB/2 + q NB pair with index R-1-q
 #pragma unroll
@@ -331,9 +377,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
                 if (q > qp) continue;
                 const int k = NB / 2 + q * NB;
                 const double2 w = tw_lookup<-1>(plo, phi, k);
-                const double2 zk = vb[q], zn = vb[qp];
-                orow[(long long)k * out_fs] = split_x(zk, zn, w);
-                if (q != qp) orow[(long long)(N - k) * out_fs] = split_x(zn, zk, partner_w(w));
+                double2 xk, xn;
+                split_pair(vb[q], vb[qp], w, xk, xn);
+                orow[(long long)k * out_fs] = xk;
+                if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
             }
         }
     }
@@ -343,7 +390,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
 // c2r: frequency-major in[k*in_fs + c] -> SOTI rows out[c*out_cs + t], t < N
 // ---------------------------------------------------------------------------
 template <int N, int CPB>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     k_c2r_fast(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
     using P = FastPlan<N>;
@@ -385,8 +432,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
                     const int k = ja + q * NB;  // partner N - k = jb + (R-1-q) NB
                     const double2 xk = X(k), xn = X(N - k);
                     const double2 w = tw_lookup<-1>(plo, phi, k);
-                    va[uf][q] = presplit_z(xk, xn, w, inv_len);
-                    vb[uf][R - 1 - q] = presplit_z(xn, xk, partner_w(w), inv_len);
+                    presplit_pair(xk, xn, w, inv_len, va[uf][q], vb[uf][R - 1 - q]);
                 }
             } else {
 #pragma unroll
@@ -396,8 +442,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
                     const int k = q * NB;
                     const double2 xk = X(k), xn = X(N - k);  // q = 0: X_0 and X_N
                     const double2 w = tw_lookup<-1>(plo, phi, k);
-                    va[uf][q] = presplit_z(xk, xn, w, inv_len);
-                    if (q != qp) va[uf][qp] = presplit_z(xn, xk, partner_w(w), inv_len);
+                    double2 zk, zn;
+                    presplit_pair(xk, xn, w, inv_len, zk, zn);
+                    va[uf][q] = zk;
+                    if (q != qp) va[uf][qp] = zn;
                 }
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
@@ -406,8 +454,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocks<N, CPB>)
                     const int k = NB / 2 + q * NB;
                     const double2 xk = X(k), xn = X(N - k);
                     const double2 w = tw_lookup<-1>(plo, phi, k);
-                    vb[uf][q] = presplit_z(xk, xn, w, inv_len);
-                    if (q != qp) vb[uf][qp] = presplit_z(xn, xk, partner_w(w), inv_len);
+                    double2 zk, zn;
+                    presplit_pair(xk, xn, w, inv_len, zk, zn);
+                    vb[uf][q] = zk;
+                    if (q != qp) vb[uf][qp] = zn;
                 }
             }
             dft<R, +1>(va[uf]);
