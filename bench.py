@@ -254,11 +254,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    device = local
+    # one rank per GPU; the modulo and BTG_BENCH_BACKEND=gloo only exist so the
+    # N > 1 path can be exercised with several ranks sharing one GPU (NCCL
+    # refuses duplicate devices) — the driver's runs use NCCL, one GPU per rank
+    device = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(device)
+    if world > 1:
+        backend = os.environ.get("BTG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+        else:
+            dist.init_process_group(backend)
     cfg = dict(CONFIGS["B" if world == 1 else "C"])
     if args.config:
         cfg = dict(CONFIGS[args.config])
@@ -373,9 +379,12 @@ def run_ours(args):
     # Per-kernel durations: CUDA-event stage timers inside the library (same
     # stream), F then F* separately so forward / adjoint GEMV are distinct.
     kernels = {}
-    if engine is None:
+    if op is not None:
+        # on a grid rank: the local shard's kernels (no collectives in between)
+        d_loc = d if engine is None else torch.empty((nd, nt) if nrhs == 1 else (nrhs, nd, nt),
+                                                      dtype=torch.float64, device=dev).uniform_(-1, 1)
         op.set_timing(True)
-        for name, fn, arg in (("fwd", do_f, m), ("adj", do_a, d)):
+        for name, fn, arg in (("fwd", op.apply_forward, m), ("adj", op.apply_adjoint, d_loc)):
             op.reset_counters()
             reps = 3
             for _ in range(reps):
