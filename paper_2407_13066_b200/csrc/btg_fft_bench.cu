@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -56,12 +57,18 @@ struct Run {
         for (size_t i = 0; i < nx; ++i) hx[i] = (double)rand() / RAND_MAX - 0.5;
         CK(cudaMemcpy(x, hx.data(), nx * 8, cudaMemcpyHostToDevice));
 
-        auto r2c = fast::k_r2c_fast<N, CPB>;
-        auto c2r = fast::k_c2r_fast<N, CPB>;
+        auto r2c = P::PF_R2C ? fast::k_r2c_pf<N, CPB> : fast::k_r2c_fast<N, CPB>;
+        auto c2r = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
         constexpr size_t smem = fast::smem_bytes<N, CPB>();
         CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int grid = (C + CPB - 1) / CPB;
+        int occ_r = 1, occ_c = 1, sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, r2c, P::TPC * CPB, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c2r, P::TPC * CPB, smem);
+        const int groups = (C + CPB - 1) / CPB;
+        const int grid_r = P::PF_R2C ? std::min(groups, occ_r * sms) : groups;
+        const int grid_c = P::PF_C2R ? std::min(groups, occ_c * sms) : groups;
         C2REpilogue epi{};
         cudaEvent_t e0, e1, e2;
         cudaEventCreate(&e0);
@@ -70,9 +77,9 @@ struct Run {
         float tr = 0, tc = 0;
         for (int r = -2; r < reps; ++r) {
             cudaEventRecord(e0);
-            r2c<<<grid, P::TPC * CPB, smem>>>(x, N, X, C, C, tabs);
+            r2c<<<grid_r, P::TPC * CPB, smem>>>(x, N, X, C, C, tabs);
             cudaEventRecord(e1);
-            c2r<<<grid, P::TPC * CPB, smem>>>(X, C, y, N, C, tabs, epi);
+            c2r<<<grid_c, P::TPC * CPB, smem>>>(X, C, y, N, C, tabs, epi);
             cudaEventRecord(e2);
             CK(cudaEventSynchronize(e2));
             float a, b;

@@ -42,33 +42,38 @@ namespace fast {
 // Plans: TPC threads per channel, default CPB channels per CTA, pass radices
 // for R2C (small radix last: it runs on butterfly pairs) and C2R (small first),
 // and the resident threads per SM each direction is compiled for (register
-// budget = 64K / RES): measured on B200 (profiles/r01s2_fft_sweep.md) — the
-// longer transforms prefer fewer, fatter threads, most of all the C2R.
+// budget = 64K / RES) and whether the kernel runs persistent with the next
+// channel group's first-pass loads prefetched into registers (PF): measured on
+// B200 (profiles/r01s2_fft_sweep.md) — the longer transforms prefer fewer,
+// fatter threads, most of all the C2R; the prefetch pays where its registers
+// do not cost occupancy (short transforms, the N_t = 1024 C2R).
 template <int... Rs>
 struct Radices {};
 template <int N>
 struct FastPlan;
-#define BTG_PLAN(N, tpc, cpb, res_r2c, res_c2r, R2CL, C2RL)                                    \
+#define BTG_PLAN(N, tpc, cpb, res_r2c, res_c2r, pf_r2c, pf_c2r, R2CL, C2RL)                    \
     template <>                                                                                  \
     struct FastPlan<N> {                                                                         \
         static constexpr int TPC = tpc, CPB = cpb, RES_R2C = res_r2c, RES_C2R = res_c2r;         \
+        static constexpr bool PF_R2C = pf_r2c, PF_C2R = pf_c2r;                                  \
         using R2C = R2CL;                                                                        \
         using C2R = C2RL;                                                                        \
     };
 #define BTG_R(...) Radices<__VA_ARGS__>
-BTG_PLAN(64,    8,   32, 768,  768,  BTG_R(16, 4),           BTG_R(4, 16))
-BTG_PLAN(128,   16,  16, 1024, 1024, BTG_R(8, 4, 4),         BTG_R(4, 4, 8))
-BTG_PLAN(256,   16,  16, 512,  512,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
-BTG_PLAN(500,   64,  4,  1024, 768,  BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
-BTG_PLAN(512,   64,  4,  256,  768,  BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
-BTG_PLAN(1000,  128, 2,  1024, 1024, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
-BTG_PLAN(1024,  64,  4,  768,  256,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
-BTG_PLAN(2000,  128, 2,  512,  384,  BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
-BTG_PLAN(2048,  128, 2,  512,  256,  BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
-BTG_PLAN(4096,  256, 1,  512,  256,  BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
+//       N      TPC  CPB  RES r2c/c2r  prefetch r2c/c2r
+BTG_PLAN(64,    8,   32, 512,  512,  true,  true,  BTG_R(16, 4),           BTG_R(4, 16))
+BTG_PLAN(128,   16,  16, 1024, 1024, false, false, BTG_R(8, 4, 4),         BTG_R(4, 4, 8))
+BTG_PLAN(256,   16,  16, 512,  256,  true,  true,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
+BTG_PLAN(500,   64,  4,  1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
+BTG_PLAN(512,   64,  4,  256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
+BTG_PLAN(1000,  128, 2,  1024, 1024, false, false, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
+BTG_PLAN(1024,  64,  4,  768,  256,  false, true,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
+BTG_PLAN(2000,  128, 2,  512,  384,  false, false, BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
+BTG_PLAN(2048,  128, 2,  512,  256,  false, false, BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
+BTG_PLAN(4096,  256, 1,  512,  256,  false, false, BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
 // long horizons: the paper's N_t = 10000 runs and 2^13
-BTG_PLAN(8192,  512, 1,  768,  768,  BTG_R(16, 16, 8, 4),    BTG_R(4, 8, 16, 16))
-BTG_PLAN(10000, 625, 1,  768,  768,  BTG_R(16, 5, 5, 5, 5),  BTG_R(5, 5, 5, 5, 16))
+BTG_PLAN(8192,  512, 1,  768,  768,  false, false, BTG_R(16, 16, 8, 4),    BTG_R(4, 8, 16, 16))
+BTG_PLAN(10000, 625, 1,  768,  768,  false, false, BTG_R(16, 5, 5, 5, 5),  BTG_R(5, 5, 5, 5, 16))
 #undef BTG_R
 #undef BTG_PLAN
 
@@ -528,6 +533,322 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                 reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent variants (plans with PF_R2C / PF_C2R): the same passes, looping
+// over channel groups (group g = blockIdx.x + i gridDim.x); the first pass's
+// global loads for the NEXT group are issued into registers right after this
+// group's first pass consumed them, so they are in flight during the
+// shared-memory passes and the stores.
+// ---------------------------------------------------------------------------
+template <int N, int CPB>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
+    k_r2c_pf(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
+               int channels, FastTables tabs) {
+    using P = FastPlan<N>;
+    using RL = typename P::R2C;
+    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int HI = tw_hi_count<N>();
+    constexpr int R1 = first_radix(RL{});
+    constexpr int NB1 = N / R1;
+    constexpr int BF1 = (NB1 + TPC - 1) / TPC;
+    constexpr int QH = R1 / 2;  // z[n], n = j + q NB1 < N/2 iff q < R1/2: the rest is zero pad
+    extern __shared__ double2 sm[];
+    double2* lo = sm + CPB * CS;
+    double2* hi = lo + kTwLo;
+    double2* plo = hi + HI;  // W_{2N} tables
+    double2* phi = plo + kTwLo;
+    load_tables(lo, hi, HI, tabs.lo, tabs.hi);
+    load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    const int b = threadIdx.x % CPB;
+    const int tc = threadIdx.x / CPB;
+    double2* s = sm + b * CS;
+    const int groups = (channels + CPB - 1) / CPB;
+
+    double2 pre[BF1][QH];
+    auto prefetch = [&](int g) {
+        const int c = g * CPB + b;
+        const bool ok = g < groups && c < channels;
+        const double2* row = reinterpret_cast<const double2*>(in + (long long)(ok ? c : 0) * in_cs);
+#pragma unroll
+        for (int bf = 0; bf < BF1; ++bf) {
+            const int j = tc + bf * TPC;
+            const bool jl = ok && (NB1 % TPC == 0 || j < NB1);
+#pragma unroll
+            for (int q = 0; q < QH; ++q) pre[bf][q] = jl ? __ldg(row + j + q * NB1) : make_double2(0.0, 0.0);
+        }
+    };
+    prefetch(blockIdx.x);
+    __syncthreads();
+
+    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+        const int c = g * CPB + b;
+        const bool live = c < channels;
+        // ---- pass 1 from the prefetched registers: z[n] = (x[2n], x[2n+1])
+        {
+            double2 v[BF1][R1];
+#pragma unroll
+            for (int bf = 0; bf < BF1; ++bf) {
+#pragma unroll
+                for (int q = 0; q < R1; ++q) v[bf][q] = q < QH ? pre[bf][q] : make_double2(0.0, 0.0);
+                dft<R1, -1>(v[bf]);
+            }
+            prefetch(g + gridDim.x);
+#pragma unroll
+            for (int bf = 0; bf < BF1; ++bf) {
+                const int j = tc + bf * TPC;
+                if (NB1 % TPC == 0 || j < NB1) {
+#pragma unroll
+                    for (int q = 0; q < R1; ++q) s[pad_idx(j * R1 + q)] = v[bf][q];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- middle passes
+        passes_but_last<N, TPC, R1, -1>(s, tc, lo, hi, tail(RL{}));
+
+        // ---- last pass on butterfly pairs (j, NB-j) + split in registers
+        constexpr int R = last_radix(RL{});
+        constexpr int NS = ns_of_last(RL{});
+        constexpr int NB = N / R;  // == NS
+        constexpr int NU = NB / 2;
+        constexpr int UF = (NU + TPC - 1) / TPC;
+        if (live) {
+            double2* orow = out + c;
+#pragma unroll
+            for (int uf = 0; uf < UF; ++uf) {
+                const int u = tc + uf * TPC;
+                if (NU % TPC != 0 && u >= NU) break;
+                const int ja = u == 0 ? 0 : u;
+                const int jb = u == 0 ? NB / 2 : NB - u;
+                double2 va[R], vb[R];
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    va[q] = s[pad_idx(ja + q * NB)];
+                    vb[q] = s[pad_idx(jb + q * NB)];
+                }
+                twiddle_inputs<N, R, NS, -1>(va, ja, lo, hi);
+                twiddle_inputs<N, R, NS, -1>(vb, jb, lo, hi);
+                dft<R, -1>(va);
+                dft<R, -1>(vb);
+                if (u != 0) {
+                    // position ja + q NB pairs with jb + (R-1-q) NB
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int k = ja + q * NB;
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        double2 xk, xn;
+                        split_pair(va[q], vb[R - 1 - q], w, xk, xn);
+                        orow[(long long)k * out_fs] = xk;
+                        orow[(long long)(N - k) * out_fs] = xn;
+                    }
+                } else {
+                    // butterfly 0: positions q NB pair with ((R - q) % R) NB; q = 0 gives X_0 and X_N
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int qp = (R - q) % R;
+                        if (q > qp && q != 0) continue;
+                        const int k = q * NB;
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        double2 xk, xn;
+                        split_pair(va[q], va[qp], w, xk, xn);
+                        orow[(long long)k * out_fs] = xk;
+                        if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                    }
+                    // butterfly NB/2: positions NB/2 + q NB pair with index R-1-q
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int qp = R - 1 - q;
+                        if (q > qp) continue;
+                        const int k = NB / 2 + q * NB;
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        double2 xk, xn;
+                        split_pair(vb[q], vb[qp], w, xk, xn);
+                        orow[(long long)k * out_fs] = xk;
+                        if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // the next group's first pass overwrites s
+    }
+}
+
+// c2r, persistent: the (X_k, X_{N-k}) pairs of the next group's first pass are
+// loaded into registers while this group finishes.
+template <int N, int CPB>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
+    k_c2r_pf(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
+               int channels, FastTables tabs, C2REpilogue epi) {
+    using P = FastPlan<N>;
+    using RL = typename P::C2R;
+    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int HI = tw_hi_count<N>();
+    constexpr int R1 = first_radix(RL{});
+    constexpr int NB1 = N / R1;
+    constexpr int NU1 = NB1 / 2;
+    constexpr int UF1 = (NU1 + TPC - 1) / TPC;
+    constexpr double inv_len = 0.5 / N;
+    extern __shared__ double2 sm[];
+    double2* lo = sm + CPB * CS;
+    double2* hi = lo + kTwLo;
+    double2* plo = hi + HI;
+    double2* phi = plo + kTwLo;
+    load_tables(lo, hi, HI, tabs.lo, tabs.hi);
+    load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    const int b = threadIdx.x % CPB;
+    const int tc = threadIdx.x / CPB;
+    double2* s = sm + b * CS;
+    const int groups = (channels + CPB - 1) / CPB;
+
+    // xa/xb[uf][q] = X(k), X(N-k) for k = ja + q NB1; xc/xd[q] = X(k), X(N-k) for
+    // k = NB1/2 + q NB1 (butterfly NB1/2, only on the thread that owns u = 0)
+    double2 xa[UF1][R1], xb[UF1][R1], xc[R1], xd[R1];
+    auto prefetch = [&](int g) {
+        const int c = g * CPB + b;
+        const bool ok = g < groups && c < channels;
+        const double2* col = in + (ok ? c : 0);
+        auto X = [&](int k, bool use) {
+            return (ok && use) ? __ldg(col + (long long)k * in_fs) : make_double2(0.0, 0.0);
+        };
+#pragma unroll
+        for (int uf = 0; uf < UF1; ++uf) {
+            const int u = tc + uf * TPC;
+            const bool ul = NU1 % TPC == 0 || u < NU1;
+#pragma unroll
+            for (int q = 0; q < R1; ++q) {
+                const int k = u + q * NB1;
+                xa[uf][q] = X(k, ul);
+                xb[uf][q] = X(N - k, ul);
+            }
+        }
+        const bool owner = tc == 0;
+#pragma unroll
+        for (int q = 0; q < R1; ++q) {
+            const int k = NB1 / 2 + q * NB1;
+            xc[q] = X(k, owner && q <= R1 - 1 - q);
+            xd[q] = X(N - k, owner && q <= R1 - 1 - q);
+        }
+    };
+    prefetch(blockIdx.x);
+    __syncthreads();
+
+    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+        const int c = g * CPB + b;
+        const bool live = c < channels;
+        // ---- pass 1 on butterfly pairs: Z from (X_k, X_{N-k})
+        {
+            double2 va[UF1][R1], vb[UF1][R1];
+#pragma unroll
+            for (int uf = 0; uf < UF1; ++uf) {
+                const int u = tc + uf * TPC;
+                if (NU1 % TPC != 0 && u >= NU1) continue;
+                const int ja = u;
+                if (u != 0) {
+#pragma unroll
+                    for (int q = 0; q < R1; ++q) {
+                        const int k = ja + q * NB1;  // partner N - k = jb + (R-1-q) NB
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        presplit_pair(xa[uf][q], xb[uf][q], w, inv_len, va[uf][q], vb[uf][R1 - 1 - q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < R1; ++q) {
+                        const int qp = (R1 - q) % R1;
+                        if (q > qp && q != 0) continue;
+                        const int k = q * NB1;  // q = 0: X_0 and X_N
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        double2 zk, zn;
+                        presplit_pair(xa[uf][q], xb[uf][q], w, inv_len, zk, zn);
+                        va[uf][q] = zk;
+                        if (q != qp) va[uf][qp] = zn;
+                    }
+#pragma unroll
+                    for (int q = 0; q < R1; ++q) {
+                        const int qp = R1 - 1 - q;
+                        if (q > qp) continue;
+                        const int k = NB1 / 2 + q * NB1;
+                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        double2 zk, zn;
+                        presplit_pair(xc[q], xd[q], w, inv_len, zk, zn);
+                        vb[uf][q] = zk;
+                        if (q != qp) vb[uf][qp] = zn;
+                    }
+                }
+                dft<R1, +1>(va[uf]);
+                dft<R1, +1>(vb[uf]);
+            }
+            prefetch(g + gridDim.x);
+#pragma unroll
+            for (int uf = 0; uf < UF1; ++uf) {
+                const int u = tc + uf * TPC;
+                if (NU1 % TPC != 0 && u >= NU1) continue;
+                const int ja = u == 0 ? 0 : u;
+                const int jb = u == 0 ? NB1 / 2 : NB1 - u;
+#pragma unroll
+                for (int q = 0; q < R1; ++q) {
+                    s[pad_idx(ja * R1 + q)] = va[uf][q];
+                    s[pad_idx(jb * R1 + q)] = vb[uf][q];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- middle passes
+        passes_but_last<N, TPC, R1, +1>(s, tc, lo, hi, tail(RL{}));
+
+        // ---- last pass: outputs p = j + q NB; keep p < N/2 (t = 2p, 2p+1 < N)
+        constexpr int R = last_radix(RL{});
+        constexpr int NS = ns_of_last(RL{});
+        constexpr int NB = N / R;
+        constexpr int BF = (NB + TPC - 1) / TPC;
+        if (live) {
+            double* orow = out + (long long)c * out_cs;
+            const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+#pragma unroll
+            for (int bf = 0; bf < BF; ++bf) {
+                const int j = tc + bf * TPC;
+                if (NB % TPC == 0 || j < NB) {
+                    double2 v[R];
+#pragma unroll
+                    for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
+                    twiddle_inputs<N, R, NS, +1>(v, j, lo, hi);
+                    dft<R, +1>(v);
+#pragma unroll
+                    for (int q = 0; q < (R + 1) / 2; ++q) {  // keep p = j + q*NB < N/2 (unpad)
+                        const int p = j + q * NB;
+                        if ((R % 2 == 1) && q == R / 2 && p >= N / 2) break;
+                        double y0 = v[q].x, y1 = v[q].y;
+                        const int t0 = 2 * p;
+                        if (epi.gamma_mode == 1) {
+                            const double gm = __ldg(epi.gamma + (c % epi.gamma_dim));
+                            y0 *= gm;
+                            y1 *= gm;
+                        } else if (epi.gamma_mode == 2) {
+                            const double* gr = epi.gamma + (long long)(c % epi.gamma_dim) * N;
+                            y0 *= __ldg(gr + t0);
+                            y1 *= __ldg(gr + t0 + 1);
+                        }
+                        if (vrow) {
+                            double r0 = __ldg(vrow + t0), r1 = __ldg(vrow + t0 + 1);
+                            if (epi.reg_kind == 1) {
+                                const double l = t0 > 0 ? __ldg(vrow + t0 - 1) : 0.0;
+                                const double h = t0 + 2 < N ? __ldg(vrow + t0 + 2) : 0.0;
+                                const double a0 = 2.0 * r0 - l - r1;  // reference order: 2x - x[t-1] - x[t+1]
+                                const double a1 = 2.0 * r1 - r0 - h;
+                                r0 = a0;
+                                r1 = a1;
+                            }
+                            y0 += epi.alpha * r0;
+                            y1 += epi.alpha * r1;
+                        }
+                        reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // the next group's first pass overwrites s
     }
 }
 

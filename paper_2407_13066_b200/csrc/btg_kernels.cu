@@ -698,6 +698,17 @@ int fft_cpb(int dflt) {
     return env > 0 ? env : dflt;
 }
 
+// Persistent grid for the vector FFT kernels: as many CTAs as fit on the device
+// at once (they loop over channel groups and prefetch the next group's inputs).
+template <typename K>
+int persistent_grid(K kern, int threads, size_t smem, int groups) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return std::max(1, std::min(groups, occ * sms));
+}
+
 template <int N, int CPB>
 cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
                         const FastTables& tabs, cudaStream_t stream) {
@@ -706,10 +717,11 @@ cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long lo
         return cudaErrorNotSupported;
     } else {
         constexpr size_t smem = fast::smem_bytes<N, CPB>();
-        auto kern = fast::k_r2c_fast<N, CPB>;
+        auto kern = P::PF_R2C ? fast::k_r2c_pf<N, CPB> : fast::k_r2c_fast<N, CPB>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        const int grid = (channels + CPB - 1) / CPB;
+        const int groups = (channels + CPB - 1) / CPB;
+        const int grid = P::PF_R2C ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
         kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs);
         return cudaGetLastError();
     }
@@ -723,10 +735,11 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         return cudaErrorNotSupported;
     } else {
         constexpr size_t smem = fast::smem_bytes<N, CPB>();
-        auto kern = fast::k_c2r_fast<N, CPB>;
+        auto kern = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        const int grid = (channels + CPB - 1) / CPB;
+        const int groups = (channels + CPB - 1) / CPB;
+        const int grid = P::PF_C2R ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
         kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
         return cudaGetLastError();
     }
