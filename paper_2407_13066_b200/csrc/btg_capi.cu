@@ -100,6 +100,8 @@ struct btg_op_s {
     unsigned long long* oz_mA = nullptr;
     int* oz_mB = nullptr;
     size_t oz_mB_cap = 0;
+    uint8_t* oz_B = nullptr;  // adjoint: d-hat slices pre-sliced once per frequency
+    size_t oz_B_cap = 0;
     bool oz_valid = false;
     bool legacy_gemv = true;   // register-load GEMV; BTG_GEMV_TMA=1 selects the TMA ring
     int fft_batch = 1;        // channels per CTA for vector transforms
@@ -299,6 +301,14 @@ btg_status ensure_oz(btg_op op, size_t nrhs) {
         BTG_CUDA(cudaMalloc(&op->oz_mB, need * sizeof(int)));
         op->oz_mB_cap = need;
     }
+    const size_t bneed = btg::oz_presliced_bytes((int)op->nf, (int)op->nd);
+    if (bneed > op->oz_B_cap) {
+        cudaFree(op->oz_B);
+        op->oz_B = nullptr;
+        cudaError_t e = cudaMalloc(&op->oz_B, bneed);
+        if (e != cudaSuccess) return fail(BTG_ENOMEM, "int8 d-hat tiles (%zu bytes): %s", bneed, cudaGetErrorString(e));
+        op->oz_B_cap = bneed;
+    }
     return BTG_OK;
 }
 
@@ -312,7 +322,8 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
         // tcgen05 int8 tensor cores, exact-integer Ozaki splitting (btg_ozaki.cu)
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
         BTG_TRY(ensure_oz(op, nrhs));
-        e = btg::oz_apply(adjoint, op->oz_A, op->oz_mA, in, out, nf, nd, nm, (int)nrhs, op->oz_mB, op->stream);
+        e = btg::oz_apply(adjoint, op->oz_A, op->oz_mA, in, out, nf, nd, nm, (int)nrhs, op->oz_mB, op->oz_B,
+                          op->stream);
     } else if (nrhs > 1) {
         // ZGEMM on the FP64 tensor cores (btg_zgemm.cu); FP64 F-hat only.
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
@@ -1278,6 +1289,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->F);
         cudaFree(op->oz_A);
         cudaFree(op->oz_mA);
+        cudaFree(op->oz_B);
         cudaFree(op->oz_mB);
         cudaFree(op->d_tw);
         cudaFree(op->d_post);

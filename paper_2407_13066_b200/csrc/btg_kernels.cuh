@@ -106,8 +106,10 @@ size_t oz_operator_scales(int nf, int nm);
 size_t oz_vector_scales(int nf, int nrhs, int kdim);
 cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_t* Aq, unsigned long long* mA,
                                  cudaStream_t stream);
+// Bq: workspace of oz_presliced_bytes(nf, nd) for the adjoint's pre-sliced d-hat tiles.
+size_t oz_presliced_bytes(int nf, int nd);
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
-                     int nf, int nd, int nm, int nrhs, int* mB, cudaStream_t stream);
+                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream);
 
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream);

@@ -78,13 +78,24 @@ __host__ __device__ constexpr size_t RingBytes(int a_stages) {
 // F-hat slice ring depth (TMA): 3 stages when they fit beside the vector
 // prefetch ring, else 2 (the vector prefetch matters more: ncu shows the B
 // producers stalled on vector loads without it).
-template <int NG>
-__host__ __device__ constexpr int AStages() {
-    return RingBytes<NG>(3) + (size_t)kVSlots * VSlotBytes<NG>() + kBarBytes <= kSmemMax ? 3 : 2;
+template <int NG, bool BPRE>
+__host__ __device__ constexpr size_t VRingBytes() {
+    return BPRE ? 0 : (size_t)kVSlots * VSlotBytes<NG>();
 }
-template <int NG>
+template <int NG, bool BPRE>
+__host__ __device__ constexpr int AStages() {
+    return RingBytes<NG>(3) + VRingBytes<NG, BPRE>() + kBarBytes <= kSmemMax ? 3 : 2;
+}
+template <int NG, bool BPRE>
 __host__ __device__ constexpr size_t GemmSmemBytes() {
-    return RingBytes<NG>(AStages<NG>()) + (size_t)kVSlots * VSlotBytes<NG>() + kBarBytes;
+    return RingBytes<NG>(AStages<NG, BPRE>()) + VRingBytes<NG, BPRE>() + kBarBytes;
+}
+// Pre-sliced B (the adjoint: every row tile of a frequency reuses the same
+// d-hat_f, so it is sliced once per frequency instead of once per tile):
+// Bq[f][ks][B tile] in exactly the shared-memory tile layout.
+template <int NG>
+__host__ __device__ constexpr size_t BTileBytes() {
+    return (size_t)2 * (16 * NG / 8) * kPos;
 }
 
 // Block exponent e with max < 2^{e-1} (so every scaled entry lies in (-1/2, 1/2)).
@@ -213,6 +224,64 @@ __global__ void k_scale_vec(const double2* __restrict__ V, int* __restrict__ mB,
     }
 }
 
+// Digits of item (kg, rr, quad) of a 32-wide K step into a B tile
+// [c][t][n-group][kg][8 rows][16 B]: 4 complex values x (S slices, 2 planes).
+template <bool ADJ, int NGRP>
+__device__ __forceinline__ void slice_item(uint8_t* bst, int kg, int rr, int quad, const double2 (&xv)[4],
+                                           double inv) {
+    double ur[4], ui[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        ur[u] = xv[u].x * inv;
+        ui[u] = xv[u].y * inv;
+    }
+    uint8_t* cm = bst + (rr >> 2) * 256 + kg * 128 + ((2 * rr) & 7) * 16 + quad * 4;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+        int a0 = digit(ur[0]), a1 = digit(ur[1]), a2 = digit(ur[2]), a3 = digit(ur[3]);
+        int b0 = digit(ui[0]), b1 = digit(ui[1]), b2 = digit(ui[2]), b3 = digit(ui[3]);
+        const uint32_t re = pack4(a0, a1, a2, a3), im = pack4(b0, b1, b2, b3);
+        uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (0 * kS + s) * NGRP * 256);
+        uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (1 * kS + s) * NGRP * 256);
+        p0[0] = re;  // real plane row 2rr
+        p0[4] = im;  // real plane row 2rr+1
+        if (!ADJ) {  // imaginary plane: (-xi, xr)
+            p1[0] = pack4(-b0, -b1, -b2, -b3);
+            p1[4] = re;
+        } else {  // imaginary plane: (di, -dr)
+            p1[0] = im;
+            p1[4] = pack4(-a0, -a1, -a2, -a3);
+        }
+    }
+}
+
+// Pre-slice V[f][r0 .. r0+nr)[0 .. K) into Bq[f][ks][tile], one thread per item.
+template <bool ADJ, int NG>
+__global__ void k_slice_vec(const double2* __restrict__ V, const int* __restrict__ mB, uint8_t* __restrict__ Bq,
+                            int nf, int ldr, int r0, int nr, int K) {
+    constexpr int NP = 16 * NG, NGRP = NP / 8, kTot = 64 * NG;
+    const int nks = (K + 31) / 32, nkb = (K + kChunk - 1) / kChunk;
+    const long long total = (long long)nf * nks * kTot;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int item = (int)(idx % kTot);
+        const long long fk = idx / kTot;
+        const int ks = (int)(fk % nks);
+        const int f = (int)(fk / nks);
+        const int quad = item & 3;
+        const int rr = (item >> 2) % (NP / 2);
+        const int kg = (item >> 2) / (NP / 2);
+        const int k = ks * 32 + kg * 16 + quad * 4;
+        const bool live = rr < nr;
+        const double inv = live ? pow2(-mB[((size_t)f * nr + rr) * nkb + ks / kStepsPerChunk]) : 0.0;
+        const double2* src = V + ((size_t)f * ldr + r0 + (live ? rr : 0)) * K;
+        double2 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = (live && k + u < K) ? __ldg(src + k + u) : make_double2(0.0, 0.0);
+        slice_item<ADJ, NGRP>(Bq + ((size_t)f * nks + ks) * BTileBytes<NG>(), kg, rr, quad, xv, inv);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // The GEMM
 // ---------------------------------------------------------------------------
@@ -225,21 +294,23 @@ struct GemmArgs {
     int nf, nd, nm;
     int ldr, r0, nr;    // rhs stride, first rhs of this pass, rhs in this pass (<= 8 NG)
     int IG, JG, nkbA;
+    const uint8_t* Bq;  // pre-sliced B tiles (BPRE)
 };
 
-template <bool ADJ, int NG>
+template <bool ADJ, int NG, bool BPRE>
 __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
     constexpr int NP = 16 * NG;  // MMA N (columns n' = 2r+q)
     constexpr int NGRP = NP / 8;
     constexpr int kBStage = 2 * NGRP * kPos;
     constexpr uint32_t kTmemCols = kLevels * NP <= 128 ? 128 : kLevels * NP <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr bool kVRing = true;
-    constexpr int kAStages = AStages<NG>();
+    constexpr bool kVRing = !BPRE;
+    constexpr int kAStages = AStages<NG, BPRE>();
+    static_assert(BTileBytes<NG>() == (size_t)kBStage, "B tile");
     uint8_t* As = smem;                                 // [kAStages][kAStage]
     uint8_t* Bs = smem + kAStages * kAStage;             // [kBStages][kBStage]
     uint8_t* Vs = Bs + kBStages * kBStage;               // [kVSlots][VSlotBytes] (kVRing)
-    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + GemmSmemBytes<NG>() - kBarBytes);
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + GemmSmemBytes<NG, BPRE>() - kBarBytes);
     uint64_t* emptyA = fullA + kAStages;
     uint64_t* fullB = emptyA + kAStages;
     uint64_t* emptyB = fullB + kBStages;
@@ -262,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
             umma::mbar_init(emptyA + s, 1);
         }
         for (int s = 0; s < kBStages; ++s) {
-            umma::mbar_init(fullB + s, 128);
+            umma::mbar_init(fullB + s, BPRE ? 1 : 128);
             umma::mbar_init(emptyB + s, 1);
         }
         umma::mbar_init(acc_full, 1);
@@ -278,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
         // ===== TMA producer: F-hat slice tiles =====
         if (lane == 0) {
             const uint64_t pol = umma::policy_evict_first();
+            const uint64_t pol_b = umma::policy_evict_last();  // B tiles are reused by every row tile of f
             long long it = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 const int f = (int)(tile / mtiles), mt = (int)(tile % mtiles);
@@ -302,6 +374,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                         for (int ig = ig0; ig < ig1; ++ig)
                             umma::bulk_load(dst + (ig - ig0) * 8 * kPos, base + ((size_t)ig * g.JG + jg0) * kPos,
                                             bytes, fullA + st, pol);
+                    }
+                    if constexpr (BPRE) {
+                        const int sb = (int)(it % kBStages);
+                        if (it >= kBStages) umma::mbar_wait(emptyB + sb, (uint32_t)(((it / kBStages) - 1) & 1));
+                        umma::mbar_expect_tx(fullB + sb, (uint32_t)kBStage);
+                        umma::bulk_load(Bs + sb * kBStage, g.Bq + ((size_t)f * nks + ks) * kBStage, (uint32_t)kBStage,
+                                        fullB + sb, pol_b);
                     }
                 }
             }
@@ -460,6 +539,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
         // chunk before that step's chunk has been drained (the MMA warp waits for it).
         long long it = 0, chunk_idx = 0;  // chunk_idx: global index of the tile's first chunk
         long long step_chunk[kBStages] = {};
+        if constexpr (BPRE) {  // B arrives by TMA: these warps only drain
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) chunk_idx += nkb;
+            while (drained < chunk_idx) drain();
+        } else {
         if constexpr (kVRing) {
 #pragma unroll
             for (int a = 0; a < kVAhead; ++a) prefetch(a);
@@ -515,34 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                 for (int ii = 0; ii < kItems; ++ii) {
                     const int item = et + ii * 128;  // (kg, rr, quad), quad fastest
                     if (item >= kTotItems) break;
-                    const int quad = item & 3;
-                    const int rr = (item >> 2) % (NP / 2);
-                    const int kg = (item >> 2) / (NP / 2);
-                    double ur[4], ui[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        ur[u] = xv[ii][u].x * inv[ii];
-                        ui[u] = xv[ii][u].y * inv[ii];
-                    }
-                    // B tile [c][t][n-group][kg][8 rows][16 B]
-                    uint8_t* cm = bst + (rr >> 2) * 256 + kg * 128 + ((2 * rr) & 7) * 16 + quad * 4;
-#pragma unroll
-                    for (int s = 0; s < kS; ++s) {
-                        int a0 = digit(ur[0]), a1 = digit(ur[1]), a2 = digit(ur[2]), a3 = digit(ur[3]);
-                        int b0 = digit(ui[0]), b1 = digit(ui[1]), b2 = digit(ui[2]), b3 = digit(ui[3]);
-                        const uint32_t re = pack4(a0, a1, a2, a3), im = pack4(b0, b1, b2, b3);
-                        uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (0 * kS + s) * NGRP * 256);
-                        uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (1 * kS + s) * NGRP * 256);
-                        p0[0] = re;  // real plane row 2rr
-                        p0[4] = im;  // real plane row 2rr+1
-                        if (!ADJ) {  // imaginary plane: (-xi, xr)
-                            p1[0] = pack4(-b0, -b1, -b2, -b3);
-                            p1[4] = re;
-                        } else {  // imaginary plane: (di, -dr)
-                            p1[0] = im;
-                            p1[4] = pack4(-a0, -a1, -a2, -a3);
-                        }
-                    }
+                    slice_item<ADJ, NGRP>(bst, (item >> 2) / (NP / 2), (item >> 2) % (NP / 2), item & 3, xv[ii],
+                                          inv[ii]);
                 }
                 umma::fence_async_smem();
                 umma::mbar_arrive(fullB + sb);
@@ -550,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
             chunk_idx += nkb;
         }
         while (drained < chunk_idx) drain();
+        }
     }
 
     umma::fence_before_sync();
@@ -559,13 +617,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
 
 template <bool ADJ, int NG>
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t stream) {
-    constexpr size_t smem = GemmSmemBytes<NG>();
+    constexpr bool BPRE = ADJ;  // the adjoint's B (d-hat slices) is shared by all row tiles of f
+    constexpr size_t smem = GemmSmemBytes<NG, BPRE>();
     static_assert(smem <= 232448, "shared memory");
-    auto kern = k_oz_gemm<ADJ, NG>;
+    auto kern = k_oz_gemm<ADJ, NG, BPRE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if constexpr (BPRE) {
+        if (!a.Bq) return cudaErrorInvalidValue;
+        k_slice_vec<ADJ, NG><<<sms * 8, 256, 0, stream>>>(a.V, a.mB, const_cast<uint8_t*>(a.Bq), a.nf, a.ldr,
+                                                          a.r0, a.nr, ADJ ? a.nd : a.nm);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     const int rows = ADJ ? a.nm : a.nd;
     const long long tiles = (long long)a.nf * ((rows + kTileM - 1) / kTileM);
     const int grid = (int)std::min<long long>(tiles, sms);
@@ -596,8 +662,12 @@ cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_
     return cudaGetLastError();
 }
 
+size_t oz_presliced_bytes(int nf, int nd) {  // adjoint B tiles, up to 32 RHS per pass
+    return (size_t)nf * ((nd + 31) / 32) * oz::BTileBytes<4>();
+}
+
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
-                     int nf, int nd, int nm, int nrhs, int* mB, cudaStream_t stream) {
+                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int K = adjoint ? nd : nm;
@@ -615,6 +685,7 @@ cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* m
     a.IG = (nd + 7) / 8;
     a.JG = (nm + 15) / 16;
     a.nkbA = (nm + oz::kChunk - 1) / oz::kChunk;
+    a.Bq = Bq;
     for (int r0 = 0; r0 < nrhs; r0 += 32) {
         const int nr = std::min(32, nrhs - r0);
         a.r0 = r0;
