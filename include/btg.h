@@ -156,6 +156,15 @@ btg_status btg_adjoint_ex(btg_op op, const double* d, size_t d_len, double* m, s
 btg_status btg_set_stream(btg_op op, void* stream);
 btg_status btg_synchronize(btg_op op);
 btg_status btg_set_timing(btg_op op, int enabled);
+
+/* Engine of the multi-right-hand-side Fourier step (nrhs > 1, FP64 F-hat):
+ * BTG_MRHS_DMMA (default) = ZGEMM on the FP64 tensor cores (mma.sync f64);
+ * BTG_MRHS_TENSOR_I8 = exact-integer Ozaki splitting on the tcgen05 int8 tensor
+ * cores (7 signed 7-bit digits per 1024-wide block scale; int8 slices of F-hat
+ * are built on first use, 14 B per complex entry). The environment variable
+ * BTG_TENSOR_I8 selects the latter at creation. */
+typedef enum { BTG_MRHS_DMMA = 0, BTG_MRHS_TENSOR_I8 = 1 } btg_mrhs_engine;
+btg_status btg_set_multi_rhs_engine(btg_op op, int engine);
 btg_status btg_get_counters(btg_op op, btg_counters* out);
 btg_status btg_reset_counters(btg_op op);
 btg_status btg_get_dims(btg_op op, size_t* num_sensors, size_t* num_sources,

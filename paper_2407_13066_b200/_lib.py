@@ -31,6 +31,7 @@ EXPORTED = (
     "btg_set_stream",
     "btg_synchronize",
     "btg_set_timing",
+    "btg_set_multi_rhs_engine",
     "btg_get_counters",
     "btg_reset_counters",
     "btg_get_dims",
@@ -171,6 +172,7 @@ def load():
     L.btg_set_stream.argtypes = [_vp, _vp]
     L.btg_synchronize.argtypes = [_vp]
     L.btg_set_timing.argtypes = [_vp, ctypes.c_int]
+    L.btg_set_multi_rhs_engine.argtypes = [_vp, ctypes.c_int]
     L.btg_get_counters.argtypes = [_vp, ctypes.POINTER(Counters)]
     L.btg_reset_counters.argtypes = [_vp]
     L.btg_get_dims.argtypes = [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz), ctypes.POINTER(_sz),

@@ -1196,6 +1196,15 @@ btg_status btg_set_timing(btg_op op, int enabled) {
     return BTG_OK;
 }
 
+btg_status btg_set_multi_rhs_engine(btg_op op, int engine) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (engine != BTG_MRHS_DMMA && engine != BTG_MRHS_TENSOR_I8)
+        return fail(BTG_EARG, "unknown multi-RHS engine %d", engine);
+    std::lock_guard<std::mutex> lock(op->mu);
+    op->tensor_i8 = engine == BTG_MRHS_TENSOR_I8;
+    return BTG_OK;
+}
+
 btg_status btg_get_counters(btg_op op, btg_counters* out) {
     if (!op || !out) return fail(BTG_EARG, "null argument");
     *out = op->counters;

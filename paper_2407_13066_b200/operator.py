@@ -130,6 +130,14 @@ class SpectralOperator:
     def set_timing(self, enabled: bool) -> None:
         check(_lib.load().btg_set_timing(self._h, int(enabled)))
 
+    def set_multi_rhs_engine(self, engine: str) -> None:
+        """nrhs > 1 Fourier step: "dmma" (ZGEMM on FP64 tensor cores, default)
+        or "tensor_i8" (Ozaki splitting on tcgen05 int8 tensor cores)."""
+        codes = {"dmma": 0, "tensor_i8": 1}
+        if engine not in codes:
+            raise ValueError(f"unknown multi-RHS engine {engine!r}; expected one of {sorted(codes)}")
+        check(_lib.load().btg_set_multi_rhs_engine(self._h, codes[engine]))
+
     def counters(self) -> dict:
         c = _lib.Counters()
         check(_lib.load().btg_get_counters(self._h, ctypes.byref(c)))

@@ -57,3 +57,26 @@ def test_tensor_i8_wide_dynamic_range(btg, monkeypatch):
         F = op.apply_forward(M)
     for r in range(nrhs):
         assert R.rel_l2(F[r], R.apply_forward(spec, M[r])) <= TOL64
+
+
+def test_engine_switch_on_one_handle(btg):
+    """btg_set_multi_rhs_engine: the same handle alternates DMMA and tcgen05
+    int8 engines; both meet the FP64 bar against the oracle."""
+    nd, nm, nt, nrhs = 40, 1500, 24, 5
+    blocks, _, _ = R.random_problem(950, nd, nm, nt)
+    spec = R.setup_full(blocks)
+    M = R.Mt19937_64(951).uniform(nrhs * nm * nt, -1, 1).reshape(nrhs, nm, nt)
+    with btg.setup(blocks) as op:
+        F_dmma = op.apply_forward(M)
+        op.set_multi_rhs_engine("tensor_i8")
+        F_i8 = op.apply_forward(M)
+        A_i8 = op.apply_adjoint(F_i8)
+        op.set_multi_rhs_engine("dmma")
+        A_dmma = op.apply_adjoint(F_dmma)
+        with pytest.raises(ValueError):
+            op.set_multi_rhs_engine("tf32")
+    for r in range(nrhs):
+        want = R.apply_forward(spec, M[r])
+        assert R.rel_l2(F_dmma[r], want) <= TOL64
+        assert R.rel_l2(F_i8[r], want) <= TOL64
+        assert R.rel_l2(A_i8[r], A_dmma[r]) <= TOL64
