@@ -126,6 +126,28 @@ __device__ __forceinline__ void digits(double u, int (&q)[kS]) {
     for (int s = 0; s < kS; ++s) q[s] = digit(u);
 }
 
+// The same 7 balanced digits with two FP64 roundings and integer shifts (the
+// vector slicing is on the critical path of the forward GEMM): H = rint(2^21 u)
+// carries digits 1-3, L = rint(2^28 (2^21 u - H)) digits 4-7; every digit is a
+// rounding shift, in [-64, 64], and the truncation is the same 2^-50.
+__device__ __forceinline__ int lo_int(double t) { return __double2loint(t); }
+__device__ __forceinline__ void digits_fast(double u, int (&q)[kS]) {
+    const double w = u * 2097152.0;  // 2^21 u, |w| <= 2^20
+    const double t = w + kMagic;
+    int h = lo_int(t);
+    int l = lo_int((w - (t - kMagic)) * 268435456.0 + kMagic);  // 2^28 remainder, |l| <= 2^27
+    q[0] = (h + (1 << 13)) >> 14;
+    h -= q[0] << 14;
+    q[1] = (h + (1 << 6)) >> 7;
+    q[2] = h - (q[1] << 7);
+    q[3] = (l + (1 << 20)) >> 21;
+    l -= q[3] << 21;
+    q[4] = (l + (1 << 13)) >> 14;
+    l -= q[4] << 14;
+    q[5] = (l + (1 << 6)) >> 7;
+    q[6] = l - (q[5] << 7);
+}
+
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
     return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
            ((uint32_t)(d & 0xFF) << 24);
@@ -229,17 +251,17 @@ __global__ void k_scale_vec(const double2* __restrict__ V, int* __restrict__ mB,
 template <bool ADJ, int NGRP>
 __device__ __forceinline__ void slice_item(uint8_t* bst, int kg, int rr, int quad, const double2 (&xv)[4],
                                            double inv) {
-    double ur[4], ui[4];
+    int qr[4][kS], qi[4][kS];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        ur[u] = xv[u].x * inv;
-        ui[u] = xv[u].y * inv;
+        digits_fast(xv[u].x * inv, qr[u]);
+        digits_fast(xv[u].y * inv, qi[u]);
     }
     uint8_t* cm = bst + (rr >> 2) * 256 + kg * 128 + ((2 * rr) & 7) * 16 + quad * 4;
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
-        int a0 = digit(ur[0]), a1 = digit(ur[1]), a2 = digit(ur[2]), a3 = digit(ur[3]);
-        int b0 = digit(ui[0]), b1 = digit(ui[1]), b2 = digit(ui[2]), b3 = digit(ui[3]);
+        const int a0 = qr[0][s], a1 = qr[1][s], a2 = qr[2][s], a3 = qr[3][s];
+        const int b0 = qi[0][s], b1 = qi[1][s], b2 = qi[2][s], b3 = qi[3][s];
         const uint32_t re = pack4(a0, a1, a2, a3), im = pack4(b0, b1, b2, b3);
         uint32_t* p0 = reinterpret_cast<uint32_t*>(cm + (0 * kS + s) * NGRP * 256);
         uint32_t* p1 = reinterpret_cast<uint32_t*>(cm + (1 * kS + s) * NGRP * 256);
@@ -386,9 +408,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
+        // ===== MMA issuer: the whole warp runs the loop (warp-uniform
+        // descriptors), one elected lane issues the MMAs and commits =====
+        {
             constexpr int kPiece = 256 / NP;  // B slices per MMA (N <= 256)
+            const bool leader = umma::elect_one();
             long long it = 0, chunks = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int ck = 0; ck < nkb; ++ck, ++chunks) {
@@ -403,31 +427,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                         const uint32_t a0 = umma::smem_u32(As + sa * kAStage);
                         const uint32_t b0 = umma::smem_u32(Bs + sb * kBStage);
                         const bool first_step = ks == ck * kStepsPerChunk;
+                        if (leader) {
 #pragma unroll
-                        for (int c = 0; c < 2; ++c)
+                            for (int c = 0; c < 2; ++c)
 #pragma unroll
-                            for (int s = 0; s < kS; ++s) {
-                                const uint64_t ad =
-                                    ADJ ? umma::make_desc(a0 + (s * 2 + c) * kCM, 8 * kPos, kPos)
-                                        : umma::make_desc(a0 + (s * 2 + c) * kCM, kPos, 2 * kPos);
-                                // A slice s against the B slices t = 0 .. S-1-s at once: the
-                                // B planes are stored slice after slice with a uniform 8-row
-                                // stride, so one descriptor spans several slices and the
-                                // products land in consecutive level accumulators (s + t).
+                                for (int s = 0; s < kS; ++s) {
+                                    const uint64_t ad =
+                                        ADJ ? umma::make_desc(a0 + (s * 2 + c) * kCM, 8 * kPos, kPos)
+                                            : umma::make_desc(a0 + (s * 2 + c) * kCM, kPos, 2 * kPos);
+                                    // A slice s against the B slices t = 0 .. S-1-s at once: the
+                                    // B planes are stored slice after slice with a uniform 8-row
+                                    // stride, so one descriptor spans several slices and the
+                                    // products land in consecutive level accumulators (s + t).
 #pragma unroll
-                                for (int t0 = 0; t0 < kS - s; t0 += kPiece) {
-                                    const int ns = (kS - s - t0) < kPiece ? (kS - s - t0) : kPiece;
-                                    const uint64_t bd =
-                                        umma::make_desc(b0 + (c * kS + t0) * NGRP * 256, 128, 256);
-                                    const uint32_t acc = (first_step && c == 0 && s == 0) ? 0u : 1u;
-                                    umma::mma_s8(tmem + (uint32_t)((s + t0) * NP), ad, bd,
-                                                 umma::idesc_s8(kTileM, ns * NP, ADJ, false), acc);
+                                    for (int t0 = 0; t0 < kS - s; t0 += kPiece) {
+                                        const int ns = (kS - s - t0) < kPiece ? (kS - s - t0) : kPiece;
+                                        const uint64_t bd =
+                                            umma::make_desc(b0 + (c * kS + t0) * NGRP * 256, 128, 256);
+                                        const uint32_t acc = (first_step && c == 0 && s == 0) ? 0u : 1u;
+                                        umma::mma_s8(tmem + (uint32_t)((s + t0) * NP), ad, bd,
+                                                     umma::idesc_s8(kTileM, ns * NP, ADJ, false), acc);
+                                    }
                                 }
-                            }
-                        umma::commit(emptyA + sa);
-                        umma::commit(emptyB + sb);
+                            umma::commit(emptyA + sa);
+                            umma::commit(emptyB + sb);
+                        }
+                        __syncwarp();
                     }
-                    umma::commit(acc_full);
+                    if (leader) umma::commit(acc_full);
+                    __syncwarp();
                 }
             }
         }
