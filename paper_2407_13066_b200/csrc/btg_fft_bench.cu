@@ -30,11 +30,21 @@ static double2 root(long long num, long long den) {
     return make_double2((double)cosl(a), (double)(-sinl(a)));
 }
 
+#ifndef BENCH_CPB
+#define BENCH_CPB 0
+#endif
 template <int N>
 struct Run {
     static void go(int C, int reps) {
         using P = fast::FastPlan<N>;
-        constexpr int CPB = P::CPB;
+        constexpr int CPBR = BENCH_CPB ? BENCH_CPB : P::CPB_R2C;
+        constexpr int CPBC = BENCH_CPB ? BENCH_CPB : P::CPB_C2R;
+#ifdef BENCH_PF
+        constexpr bool pf_r = BENCH_PF & 1, pf_c = BENCH_PF & 2;
+#else
+        constexpr bool pf_r = P::PF_R2C, pf_c = P::PF_C2R;
+#endif
+
         const int hi = fast::tw_hi_count<N>();
         std::vector<double2> t(32 + hi + 32 + hi + 1);
         for (int i = 0; i < 32; ++i) t[i] = root(i, N);
@@ -57,18 +67,18 @@ struct Run {
         for (size_t i = 0; i < nx; ++i) hx[i] = (double)rand() / RAND_MAX - 0.5;
         CK(cudaMemcpy(x, hx.data(), nx * 8, cudaMemcpyHostToDevice));
 
-        auto r2c = P::PF_R2C ? fast::k_r2c_pf<N, CPB> : fast::k_r2c_fast<N, CPB>;
-        auto c2r = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
-        constexpr size_t smem = fast::smem_bytes<N, CPB>();
-        CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        auto r2c = pf_r ? fast::k_r2c_pf<N, CPBR> : fast::k_r2c_fast<N, CPBR>;
+        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
+        constexpr size_t smem_r = fast::smem_bytes<N, CPBR>(), smem_c = fast::smem_bytes<N, CPBC>();
+        CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+        CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
         int occ_r = 1, occ_c = 1, sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, r2c, P::TPC * CPB, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c2r, P::TPC * CPB, smem);
-        const int groups = (C + CPB - 1) / CPB;
-        const int grid_r = P::PF_R2C ? std::min(groups, occ_r * sms) : groups;
-        const int grid_c = P::PF_C2R ? std::min(groups, occ_c * sms) : groups;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, r2c, P::TPC * CPBR, smem_r);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c2r, P::TPC * CPBC, smem_c);
+        const int groups_r = (C + CPBR - 1) / CPBR, groups_c = (C + CPBC - 1) / CPBC;
+        const int grid_r = pf_r ? std::min(groups_r, occ_r * sms) : groups_r;
+        const int grid_c = pf_c ? std::min(groups_c, occ_c * sms) : groups_c;
         C2REpilogue epi{};
         cudaEvent_t e0, e1, e2;
         cudaEventCreate(&e0);
@@ -77,9 +87,9 @@ struct Run {
         float tr = 0, tc = 0;
         for (int r = -2; r < reps; ++r) {
             cudaEventRecord(e0);
-            r2c<<<grid_r, P::TPC * CPB, smem>>>(x, N, X, C, C, tabs);
+            r2c<<<grid_r, P::TPC * CPBR, smem_r>>>(x, N, X, C, C, tabs);
             cudaEventRecord(e1);
-            c2r<<<grid_c, P::TPC * CPB, smem>>>(X, C, y, N, C, tabs, epi);
+            c2r<<<grid_c, P::TPC * CPBC, smem_c>>>(X, C, y, N, C, tabs, epi);
             cudaEventRecord(e2);
             CK(cudaEventSynchronize(e2));
             float a, b;
@@ -104,7 +114,7 @@ struct Run {
         std::printf(
             "{\"N_t\": %d, \"channels\": %d, \"cpb\": %d, \"r2c_ms\": %.4f, \"r2c_tbs\": %.3f, \"c2r_ms\": %.4f, "
             "\"c2r_tbs\": %.3f, \"roundtrip_rel_l2\": %.3e}\n",
-            N, C, CPB, tr, bytes / tr / 1e9, tc, bytes / tc / 1e9, std::sqrt(num / den));
+            N, C, CPBR * 100 + CPBC, tr, bytes / tr / 1e9, tc, bytes / tc / 1e9, std::sqrt(num / den));
         cudaFree(x);
         cudaFree(y);
         cudaFree(X);

@@ -39,7 +39,7 @@
 namespace btg {
 namespace fast {
 
-// Plans: TPC threads per channel, default CPB channels per CTA, pass radices
+// Plans: TPC threads per channel, channels per CTA for each direction, pass radices
 // for R2C (small radix last: it runs on butterfly pairs) and C2R (small first),
 // and the resident threads per SM each direction is compiled for (register
 // budget = 64K / RES) and whether the kernel runs persistent with the next
@@ -51,29 +51,30 @@ template <int... Rs>
 struct Radices {};
 template <int N>
 struct FastPlan;
-#define BTG_PLAN(N, tpc, cpb, res_r2c, res_c2r, pf_r2c, pf_c2r, R2CL, C2RL)                    \
+#define BTG_PLAN(N, tpc, cpb_r2c, cpb_c2r, res_r2c, res_c2r, pf_r2c, pf_c2r, R2CL, C2RL)      \
     template <>                                                                                  \
     struct FastPlan<N> {                                                                         \
-        static constexpr int TPC = tpc, CPB = cpb, RES_R2C = res_r2c, RES_C2R = res_c2r;         \
+        static constexpr int TPC = tpc, CPB_R2C = cpb_r2c, CPB_C2R = cpb_c2r;                    \
+        static constexpr int RES_R2C = res_r2c, RES_C2R = res_c2r;                               \
         static constexpr bool PF_R2C = pf_r2c, PF_C2R = pf_c2r;                                  \
         using R2C = R2CL;                                                                        \
         using C2R = C2RL;                                                                        \
     };
 #define BTG_R(...) Radices<__VA_ARGS__>
-//       N      TPC  CPB  RES r2c/c2r  prefetch r2c/c2r
-BTG_PLAN(64,    8,   32, 512,  512,  true,  true,  BTG_R(16, 4),           BTG_R(4, 16))
-BTG_PLAN(128,   16,  16, 1024, 1024, false, false, BTG_R(8, 4, 4),         BTG_R(4, 4, 8))
-BTG_PLAN(256,   16,  16, 512,  256,  true,  true,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
-BTG_PLAN(500,   64,  4,  1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
-BTG_PLAN(512,   64,  4,  256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
-BTG_PLAN(1000,  128, 2,  1024, 1024, false, false, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
-BTG_PLAN(1024,  64,  4,  768,  256,  false, true,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
-BTG_PLAN(2000,  128, 2,  512,  384,  false, false, BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
-BTG_PLAN(2048,  128, 2,  512,  256,  false, false, BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
-BTG_PLAN(4096,  256, 1,  512,  256,  false, false, BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
+//       N      TPC  channels/CTA  RES r2c/c2r  prefetch r2c/c2r
+BTG_PLAN(64,    8,   32, 32,  512,  512,  true,  true,  BTG_R(16, 4),           BTG_R(4, 16))
+BTG_PLAN(128,   16,  16, 16,  1024, 1024, false, false, BTG_R(8, 4, 4),         BTG_R(4, 4, 8))
+BTG_PLAN(256,   16,  16, 16,  512,  256,  true,  true,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
+BTG_PLAN(500,   64,  4,  4,   1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
+BTG_PLAN(512,   64,  4,  4,   256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
+BTG_PLAN(1000,  128, 2,  2,   1024, 1024, false, false, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
+BTG_PLAN(1024,  64,  4,  4,   768,  256,  false, true,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
+BTG_PLAN(2000,  128, 2,  2,   512,  384,  false, false, BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
+BTG_PLAN(2048,  128, 2,  2,   512,  256,  false, false, BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
+BTG_PLAN(4096,  256, 2,  1,   512,  256,  true,  false, BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
 // long horizons: the paper's N_t = 10000 runs and 2^13
-BTG_PLAN(8192,  512, 1,  768,  768,  false, false, BTG_R(16, 16, 8, 4),    BTG_R(4, 8, 16, 16))
-BTG_PLAN(10000, 625, 1,  768,  768,  false, false, BTG_R(16, 5, 5, 5, 5),  BTG_R(5, 5, 5, 5, 16))
+BTG_PLAN(8192,  512, 1,  1,   768,  768,  false, false, BTG_R(16, 16, 8, 4),    BTG_R(4, 8, 16, 16))
+BTG_PLAN(10000, 625, 1,  1,   768,  768,  false, false, BTG_R(16, 5, 5, 5, 5),  BTG_R(5, 5, 5, 5, 16))
 #undef BTG_R
 #undef BTG_PLAN
 

@@ -748,24 +748,24 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
 template <int N>
 cudaError_t r2c_fast_n(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
                        const FastTables& tabs, cudaStream_t stream) {
-    switch (fft_cpb(fast::FastPlan<N>::CPB)) {
+    switch (fft_cpb(fast::FastPlan<N>::CPB_R2C)) {
         case 1: return r2c_fast_nc<N, 1>(in, in_cs, out, out_fs, channels, tabs, stream);
         case 2: return r2c_fast_nc<N, 2>(in, in_cs, out, out_fs, channels, tabs, stream);
         case 4: return r2c_fast_nc<N, 4>(in, in_cs, out, out_fs, channels, tabs, stream);
         case 8: return r2c_fast_nc<N, 8>(in, in_cs, out, out_fs, channels, tabs, stream);
-        default: return r2c_fast_nc<N, fast::FastPlan<N>::CPB>(in, in_cs, out, out_fs, channels, tabs, stream);
+        default: return r2c_fast_nc<N, fast::FastPlan<N>::CPB_R2C>(in, in_cs, out, out_fs, channels, tabs, stream);
     }
 }
 
 template <int N>
 cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
                        const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
-    switch (fft_cpb(fast::FastPlan<N>::CPB)) {
+    switch (fft_cpb(fast::FastPlan<N>::CPB_C2R)) {
         case 1: return c2r_fast_nc<N, 1>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
         case 2: return c2r_fast_nc<N, 2>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
         case 4: return c2r_fast_nc<N, 4>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
         case 8: return c2r_fast_nc<N, 8>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
-        default: return c2r_fast_nc<N, fast::FastPlan<N>::CPB>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        default: return c2r_fast_nc<N, fast::FastPlan<N>::CPB_C2R>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
     }
 }
 
