@@ -50,6 +50,7 @@ typedef enum { BTG_F64 = 64, BTG_F32 = 32 } btg_precision;
 
 /* flags */
 #define BTG_DEVICE_PTRS 0x1u  /* data pointers are device pointers */
+#define BTG_KEEP_CHANNEL_LAYOUT 0x2u  /* btg_setup: SetupOptions::keep_channel_layout (EWP backend) */
 
 /* Hessian options (inverse.hpp:16; Gamma^-1 is the north star's noise weighting) */
 typedef enum { BTG_REG_IDENTITY = 0, BTG_REG_TEMPORAL_LAPLACIAN = 1 } btg_reg_kind;
@@ -164,6 +165,18 @@ btg_status btg_set_timing(btg_op op, int enabled);
  * are built on first use, 14 B per complex entry). The environment variable
  * BTG_TENSOR_I8 selects the latter at creation. */
 typedef enum { BTG_MRHS_DMMA = 0, BTG_MRHS_TENSOR_I8 = 1 } btg_mrhs_engine;
+
+/* EWP backend (the paper's Appendix A; block_operator.cpp:345-421): the
+ * Fourier-space step as element-wise products over the channel-major spectrum
+ * (SpectralP2O::channel_spectra, block_operator.hpp:45). The layout is kept when
+ * the operator is set up with BTG_KEEP_CHANNEL_LAYOUT (or after
+ * btg_set_channel_layout(op, 1)) and built on the device on first use; without
+ * it the EWP calls fail with BTG_EARG like require_channel_layout
+ * (block_operator.cpp:335-341). One right-hand side, SOTI vectors. */
+btg_status btg_set_channel_layout(btg_op op, int keep);
+btg_status btg_has_channel_layout(btg_op op, int* out);
+btg_status btg_forward_ewp(btg_op op, const double* m, size_t m_len, double* d, size_t d_len, unsigned flags);
+btg_status btg_adjoint_ewp(btg_op op, const double* d, size_t d_len, double* m, size_t m_len, unsigned flags);
 btg_status btg_set_multi_rhs_engine(btg_op op, int engine);
 btg_status btg_get_counters(btg_op op, btg_counters* out);
 btg_status btg_reset_counters(btg_op op);

@@ -4,6 +4,7 @@
 // path of /root/reference/proj/include/btoep:
 //   CompactP2O, SpectralP2O, SetupOptions, setup        block_operator.hpp:15-64
 //   apply_forward / apply_adjoint                       block_operator.hpp:71-77
+//   apply_forward_ewp / apply_adjoint_ewp               block_operator.hpp:82-85
 //   SpaceTimeVector, Ordering, tosi_to_soti, ...        space_time.hpp:9-41
 //   PipelineCounters / StageCounters                    counters.hpp:12-45
 //   Regularization, RegKind, HessianOperator            inverse.hpp:16-39
@@ -154,7 +155,7 @@ struct CompactP2O {
 };
 
 struct SetupOptions {
-    bool keep_channel_layout = false;  // EWP backend: out of scope on the GPU
+    bool keep_channel_layout = false;  // EWP backend: keep the channel-major spectrum
     int precision = BTG_F64;           // BTG_F32: complex64 F-hat, FP64 accumulation
     int device = 0;
 };
@@ -188,7 +189,11 @@ public:
 
     std::size_t num_freq() const { return 2 * num_steps; }
     std::size_t block_size() const { return num_sensors * num_sources; }
-    bool has_channel_layout() const { return false; }
+    bool has_channel_layout() const {
+        int v = 0;
+        detail::check(btg_has_channel_layout(h_, &v));
+        return v != 0;
+    }
     btg_op handle() const { return h_; }
 
     // The reference's full 2*num_steps freq_blocks, rebuilt on the host on demand.
@@ -211,7 +216,8 @@ inline SpectralP2O setup(const CompactP2O& compact, const SetupOptions& options 
     compact.validate();
     btg_op h = nullptr;
     detail::check(btg_setup(compact.blocks.data(), compact.num_sensors, compact.num_sources,
-                            compact.num_steps, options.precision, options.device, 0u, &h));
+                            compact.num_steps, options.precision, options.device,
+                            options.keep_channel_layout ? BTG_KEEP_CHANNEL_LAYOUT : 0u, &h));
     return SpectralP2O(h);
 }
 
@@ -266,6 +272,28 @@ inline SpaceTimeVector apply_forward(const SpectralP2O& op, const SpaceTimeVecto
 inline SpaceTimeVector apply_adjoint(const SpectralP2O& op, const SpaceTimeVector& d,
                                      PipelineCounters* counters = nullptr) {
     return detail::apply_dir(op, d, true, counters);
+}
+
+// EWP backend (block_operator.hpp:82-85, block_operator.cpp:345-421): requires
+// setup with keep_channel_layout, else btoep::Error (require_channel_layout).
+namespace detail {
+inline SpaceTimeVector apply_ewp(const SpectralP2O& op, const SpaceTimeVector& x, bool adjoint) {
+    const std::size_t din = adjoint ? op.num_sensors : op.num_sources;
+    const std::size_t dout = adjoint ? op.num_sources : op.num_sensors;
+    check_apply_input(op, x, din, adjoint ? "apply_adjoint_ewp" : "apply_forward_ewp");
+    SpaceTimeVector out = SpaceTimeVector::zeros(dout, op.num_steps, Ordering::SOTI);
+    detail::check(adjoint ? btg_adjoint_ewp(op.handle(), x.values.data(), x.values.size(), out.values.data(),
+                                            out.values.size(), 0u)
+                          : btg_forward_ewp(op.handle(), x.values.data(), x.values.size(), out.values.data(),
+                                            out.values.size(), 0u));
+    return out;
+}
+}  // namespace detail
+inline SpaceTimeVector apply_forward_ewp(const SpectralP2O& op, const SpaceTimeVector& m) {
+    return detail::apply_ewp(op, m, false);
+}
+inline SpaceTimeVector apply_adjoint_ewp(const SpectralP2O& op, const SpaceTimeVector& d) {
+    return detail::apply_ewp(op, d, true);
 }
 
 enum class RegKind { ScaledIdentity, TemporalLaplacian };

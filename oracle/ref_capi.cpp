@@ -104,7 +104,33 @@ void* ref_setup(const double* blocks, std::size_t nd, std::size_t nm, std::size_
     return rc == 0 ? op : nullptr;
 }
 
+// setup with SetupOptions::keep_channel_layout (block_operator.hpp:58-60): the
+// channel-major copy the EWP backend (block_operator.cpp:345-421) streams.
+void* ref_setup_channel_layout(const double* blocks, std::size_t nd, std::size_t nm, std::size_t nt) {
+    SpectralP2O* op = nullptr;
+    const int rc = guarded([&] {
+        SetupOptions o;
+        o.keep_channel_layout = true;
+        op = new SpectralP2O(setup(make_compact(blocks, nd, nm, nt), o));
+    });
+    return rc == 0 ? op : nullptr;
+}
+
 void ref_destroy(void* h) { delete static_cast<SpectralP2O*>(h); }
+
+int ref_forward_ewp(void* h, const double* m, double* d) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        copy_out(apply_forward_ewp(op, make_soti(m, op.num_sources, op.num_steps)), d);
+    });
+}
+
+int ref_adjoint_ewp(void* h, const double* d, double* m) {
+    return guarded([&] {
+        const SpectralP2O& op = *static_cast<SpectralP2O*>(h);
+        copy_out(apply_adjoint_ewp(op, make_soti(d, op.num_sensors, op.num_steps)), m);
+    });
+}
 
 // Full reference spectrum, freq-major (2*nt, nd, nm) complex128 interleaved.
 int ref_spectrum(void* h, double* out_c128) {

@@ -38,6 +38,10 @@ def lib():
         L.ref_setup.argtypes = [_c_double_p, _size_t, _size_t, _size_t]
         L.ref_setup.restype = ctypes.c_void_p
         L.ref_destroy.argtypes = [ctypes.c_void_p]
+        L.ref_setup_channel_layout.argtypes = [_c_double_p, _size_t, _size_t, _size_t]
+        L.ref_setup_channel_layout.restype = ctypes.c_void_p
+        for name in ("ref_forward_ewp", "ref_adjoint_ewp"):
+            getattr(L, name).argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p]
         L.ref_spectrum.argtypes = [ctypes.c_void_p, _c_double_p]
         for name in ("ref_forward", "ref_adjoint"):
             getattr(L, name).argtypes = [ctypes.c_void_p, _c_double_p, _c_double_p, _c_double_p]
@@ -108,11 +112,12 @@ def rng_raw(seed: int, n: int) -> np.ndarray:
 class RefSpectralOperator:
     """btoep::SpectralP2O built by the reference's setup (block_operator.cpp:178-205)."""
 
-    def __init__(self, blocks: np.ndarray):
+    def __init__(self, blocks: np.ndarray, keep_channel_layout: bool = False):
         self.blocks = _f64(blocks)
         nt, nd, nm = self.blocks.shape
         self.num_steps, self.num_sensors, self.num_sources = nt, nd, nm
-        h = lib().ref_setup(_p(self.blocks), nd, nm, nt)
+        setup = lib().ref_setup_channel_layout if keep_channel_layout else lib().ref_setup
+        h = setup(_p(self.blocks), nd, nm, nt)
         if not h:
             raise RefError(lib().ref_last_error().decode())
         self._h = ctypes.c_void_p(h)
@@ -144,6 +149,20 @@ class RefSpectralOperator:
         d = _f64(d)
         m = np.empty((self.num_sources, self.num_steps))
         _check(lib().ref_adjoint(self._h, _p(d), _p(m), None if stage_seconds is None else _p(stage_seconds)))
+        return m
+
+    def apply_forward_ewp(self, m) -> np.ndarray:
+        """apply_forward_ewp (block_operator.cpp:345-382); needs keep_channel_layout."""
+        m = _f64(m)
+        d = np.empty((self.num_sensors, self.num_steps))
+        _check(lib().ref_forward_ewp(self._h, _p(m), _p(d)))
+        return d
+
+    def apply_adjoint_ewp(self, d) -> np.ndarray:
+        """apply_adjoint_ewp (block_operator.cpp:384-421)."""
+        d = _f64(d)
+        m = np.empty((self.num_sources, self.num_steps))
+        _check(lib().ref_adjoint_ewp(self._h, _p(d), _p(m)))
         return m
 
     def hessian_apply(self, v, alpha: float = 0.0, reg_kind: int = 0) -> np.ndarray:

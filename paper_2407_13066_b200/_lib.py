@@ -32,6 +32,10 @@ EXPORTED = (
     "btg_synchronize",
     "btg_set_timing",
     "btg_set_multi_rhs_engine",
+    "btg_set_channel_layout",
+    "btg_has_channel_layout",
+    "btg_forward_ewp",
+    "btg_adjoint_ewp",
     "btg_get_counters",
     "btg_reset_counters",
     "btg_get_dims",
@@ -173,6 +177,10 @@ def load():
     L.btg_synchronize.argtypes = [_vp]
     L.btg_set_timing.argtypes = [_vp, ctypes.c_int]
     L.btg_set_multi_rhs_engine.argtypes = [_vp, ctypes.c_int]
+    L.btg_set_channel_layout.argtypes = [_vp, ctypes.c_int]
+    L.btg_has_channel_layout.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
+    L.btg_forward_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
+    L.btg_adjoint_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
     L.btg_get_counters.argtypes = [_vp, ctypes.POINTER(Counters)]
     L.btg_reset_counters.argtypes = [_vp]
     L.btg_get_dims.argtypes = [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz), ctypes.POINTER(_sz),

@@ -103,6 +103,9 @@ struct btg_op_s {
     uint8_t* oz_B = nullptr;  // adjoint: d-hat slices pre-sliced once per frequency
     size_t oz_B_cap = 0;
     bool oz_valid = false;
+    bool keep_channel = false;  // EWP backend: SetupOptions::keep_channel_layout
+    void* S = nullptr;          // channel-major copy of F-hat [c][f] (built on first EWP use)
+    bool S_valid = false;
     bool legacy_gemv = true;   // register-load GEMV; BTG_GEMV_TMA=1 selects the TMA ring
     int fft_batch = 1;        // channels per CTA for vector transforms
     int fft_batch_setup = 1;  // channels per CTA for the TOSI setup transform
@@ -710,7 +713,8 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
         return fail(BTG_EDIM, "setup rows [%zu, %zu) outside [0, %zu)", i0, i1, op->nd);
     std::lock_guard<std::mutex> lock(op->mu);
     DeviceGuard g(op->device);
-    op->oz_valid = false;  // F-hat changes: int8 slices are stale
+    op->oz_valid = false;  // F-hat changes: int8 slices and the channel layout are stale
+    op->S_valid = false;
     const size_t rows = i1 - i0;
     const size_t slab_channels = rows * op->nm;
     const long long out_fs = (long long)(op->nd * op->nm);
@@ -762,7 +766,8 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
 btg_status btg_setup(const double* blocks, size_t nd, size_t nm, size_t nt, int precision,
                      int device, unsigned flags, btg_op* out) {
     BTG_TRY(btg_create(nd, nm, nt, precision, device, out));
-    btg_status s = btg_setup_rows(*out, blocks, 0, nd, flags);
+    if (flags & BTG_KEEP_CHANNEL_LAYOUT) (*out)->keep_channel = true;
+    btg_status s = btg_setup_rows(*out, blocks, 0, nd, flags & ~BTG_KEEP_CHANNEL_LAYOUT);
     if (s != BTG_OK) {
         const std::string msg = g_err;
         btg_destroy(*out);
@@ -770,6 +775,115 @@ btg_status btg_setup(const double* blocks, size_t nd, size_t nm, size_t nt, int 
         g_err = msg;
     }
     return s;
+}
+
+// ---- EWP backend (block_operator.cpp:345-421) ---------------------------------
+btg_status btg_set_channel_layout(btg_op op, int keep) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    DeviceGuard g(op->device);
+    op->keep_channel = keep != 0;
+    if (!op->keep_channel && op->S) {
+        BTG_CUDA(cudaStreamSynchronize(op->stream));
+        cudaFree(op->S);
+        op->S = nullptr;
+        op->S_valid = false;
+    }
+    return BTG_OK;
+}
+
+btg_status btg_has_channel_layout(btg_op op, int* out) {
+    if (!op || !out) return fail(BTG_EARG, "null argument");
+    *out = op->keep_channel ? 1 : 0;
+    return BTG_OK;
+}
+
+namespace {
+btg_status ewp_dir(btg_op op, bool adjoint, const double* in, size_t in_len, double* out, size_t out_len,
+                   unsigned flags) {
+    BTG_TRY(check_ready(op));
+    const char* what = adjoint ? "apply_adjoint_ewp" : "apply_forward_ewp";
+    if (!in || !out) return fail(BTG_EARG, "null vector pointer");
+    const size_t din = adjoint ? op->nd : op->nm;
+    const size_t dout = adjoint ? op->nm : op->nd;
+    BTG_TRY(check_len(what, in_len, din, op->nt, 1, din));
+    BTG_TRY(check_len(what, out_len, dout, op->nt, 1, dout));
+    if (!op->keep_channel)  // require_channel_layout (block_operator.cpp:335-341)
+        return fail(BTG_EARG,
+                    "%s: spectral operator was built without the channel layout (setup with keep_channel_layout)",
+                    what);
+    DeviceGuard g(op->device);
+    const double* din_p = in;
+    double* dout_p = out;
+    if (!(flags & BTG_DEVICE_PTRS)) {
+        BTG_TRY(host_buffers(op, in_len, out_len));
+        BTG_CUDA(cudaMemcpyAsync(op->hin, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        din_p = op->hin;
+        dout_p = op->hout;
+    }
+    BTG_TRY(ensure_spectral(op, 1));
+    const size_t channels = op->nd * op->nm;
+    if (!op->S) {
+        const size_t bytes = op->nf * channels * op->F_elem;
+        cudaError_t e = cudaMalloc(&op->S, bytes);
+        if (e != cudaSuccess) {
+            op->S = nullptr;
+            return fail(BTG_ENOMEM, "channel layout (%zu bytes): %s", bytes, cudaGetErrorString(e));
+        }
+        op->S_valid = false;
+    }
+    if (!op->S_valid) {
+        BTG_CUDA(op->precision == BTG_F64
+                     ? btg::launch_channel_layout(static_cast<const double2*>(op->F), static_cast<double2*>(op->S),
+                                                  (int)op->nf, (long long)channels, op->stream)
+                     : btg::launch_channel_layout(static_cast<const float2*>(op->F), static_cast<float2*>(op->S),
+                                                  (int)op->nf, (long long)channels, op->stream));
+        op->counters.launches++;
+        op->S_valid = true;
+    }
+    const long long nf = (long long)op->nf;
+    {
+        StageClock clk(op, &op->counters.forward_fft);
+        BTG_CUDA(btg::launch_r2c<double2>(din_p, (long long)op->nt, 1, op->wa, 1, nf, (int)din, (int)op->nt,
+                                          op->plan, op->fft_batch, op->stream, op->gscratch));
+    }
+    {
+        StageClock clk(op, &op->counters.apply);
+        BTG_CUDA(op->precision == BTG_F64
+                     ? btg::launch_ewp(adjoint, static_cast<const double2*>(op->S), op->wa, op->wb, (int)op->nf,
+                                       (int)op->nd, (int)op->nm, op->stream)
+                     : btg::launch_ewp(adjoint, static_cast<const float2*>(op->S), op->wa, op->wb, (int)op->nf,
+                                       (int)op->nd, (int)op->nm, op->stream));
+    }
+    {
+        StageClock clk(op, &op->counters.inverse_fft);
+        BTG_CUDA(btg::launch_c2r(op->wb, 1, nf, dout_p, (long long)op->nt, (int)dout, (int)op->nt, op->plan,
+                                 op->fft_batch, btg::C2REpilogue{}, op->stream, op->gscratch));
+    }
+    op->counters.launches += 3;
+    op->counters.pad.ops += 2.0 * din * op->nt;
+    op->counters.forward_fft.ops += fft_ops(din, op->nt);
+    op->counters.forward_fft.bytes += 8.0 * din * op->nt + 16.0 * op->nf * din;
+    // the reference's EWP op / byte model (block_operator.cpp:371-376) with NF frequencies
+    op->counters.apply.ops += 8.0 * channels * op->nf;
+    op->counters.apply.bytes += 16.0 * op->nf * (3.0 * channels + 2.0 * (op->nd + op->nm));
+    op->counters.inverse_fft.ops += fft_ops(dout, op->nt);
+    op->counters.inverse_fft.bytes += 16.0 * op->nf * dout + 8.0 * dout * op->nt;
+    op->counters.unpad.ops += 2.0 * dout * op->nt;
+    return finish_host(op, out, dout_p, out_len, flags);
+}
+}  // namespace
+
+btg_status btg_forward_ewp(btg_op op, const double* m, size_t m_len, double* d, size_t d_len, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return ewp_dir(op, false, m, m_len, d, d_len, flags);
+}
+
+btg_status btg_adjoint_ewp(btg_op op, const double* d, size_t d_len, double* m, size_t m_len, unsigned flags) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return ewp_dir(op, true, d, d_len, m, m_len, flags);
 }
 
 btg_status btg_forward(btg_op op, const double* m, size_t m_len, double* d, size_t d_len,
@@ -918,6 +1032,7 @@ btg_status btg_internal_upload_spectrum_block(btg_op op, size_t f, const double*
     if (!op || !block || f > op->nt) return fail(BTG_EARG, "bad spectrum block upload");
     std::lock_guard<std::mutex> lock(op->mu);
     op->oz_valid = false;
+    op->S_valid = false;
     DeviceGuard g(op->device);
     const size_t blk = op->nd * op->nm;
     if (op->precision == BTG_F64) {
@@ -1299,6 +1414,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->oz_A);
         cudaFree(op->oz_mA);
         cudaFree(op->oz_B);
+        cudaFree(op->S);
         cudaFree(op->oz_mB);
         cudaFree(op->d_tw);
         cudaFree(op->d_post);

@@ -106,6 +106,13 @@ size_t oz_operator_scales(int nf, int nm);
 size_t oz_vector_scales(int nf, int nrhs, int kdim);
 cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_t* Aq, unsigned long long* mA,
                                  cudaStream_t stream);
+// EWP backend (btg_ewp.cu): channel layout S[c][f] of F-hat, element-wise products.
+template <typename T>
+cudaError_t launch_channel_layout(const T* F, T* S, int nf, long long channels, cudaStream_t stream);
+template <typename T>
+cudaError_t launch_ewp(bool adjoint, const T* S, const double2* in, double2* out, int nf, int nd, int nm,
+                       cudaStream_t stream);
+
 // Bq: workspace of oz_presliced_bytes(nf, nd) for the adjoint's pre-sliced d-hat tiles.
 size_t oz_presliced_bytes(int nf, int nd);
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,

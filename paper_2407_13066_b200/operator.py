@@ -85,6 +85,46 @@ class SpectralOperator:
         fused epilogue adds alpha R reg_v (inverse.cpp:87-89)."""
         return self._apply(d, adjoint=True, reg_v=reg_v, alpha=alpha, reg=reg)
 
+    # -- EWP backend (block_operator.cpp:345-421) ----------------------------------
+    @property
+    def has_channel_layout(self) -> bool:
+        """SpectralP2O::has_channel_layout (block_operator.hpp:49)."""
+        v = ctypes.c_int()
+        check(_lib.load().btg_has_channel_layout(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def apply_forward_ewp(self, m):
+        """apply_forward_ewp: element-wise products over the channel-major
+        spectrum; needs setup(..., keep_channel_layout=True), else Error."""
+        return self._apply_ewp(m, adjoint=False)
+
+    def apply_adjoint_ewp(self, d):
+        """apply_adjoint_ewp (block_operator.cpp:384-421)."""
+        return self._apply_ewp(d, adjoint=True)
+
+    def _apply_ewp(self, x, adjoint: bool):
+        din = self.num_sensors if adjoint else self.num_sources
+        dout = self.num_sources if adjoint else self.num_sensors
+        what = "apply_adjoint_ewp" if adjoint else "apply_forward_ewp"
+        nrhs, shape = self._check_vec(x, din, what)
+        if len(shape) != 2:
+            raise DimensionError(f"{what}: one SOTI vector ({din}, {self.num_steps})")
+        L = _lib.load()
+        fn = L.btg_adjoint_ewp if adjoint else L.btg_forward_ewp
+        if _is_torch(x):
+            import torch
+
+            x = self._prep_torch(x)
+            out = torch.empty((dout, self.num_steps), dtype=torch.float64, device=x.device)
+            self._bind_stream(x)
+            check(fn(self._h, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), BTG_DEVICE_PTRS))
+            return out
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty((dout, self.num_steps), dtype=np.float64)
+        self._bind_stream(None)
+        check(fn(self._h, x.ctypes.data, x.size, out.ctypes.data, out.size, 0))
+        return out
+
     def hessian_apply(self, v, alpha: float = 0.0, reg="identity", gamma_inv=None):
         """F* Gamma^-1 F v + alpha R v (inverse.cpp:78-91 with Gamma^-1 = I)."""
         reg_kind = _REG.get(reg)
@@ -301,8 +341,9 @@ def create(num_sensors: int, num_sources: int, num_steps: int, precision: int = 
 def setup(blocks, keep_channel_layout: bool = False, precision: int = BTG_F64,
           device: Optional[int] = None) -> SpectralOperator:
     """btoep::setup (block_operator.cpp:178-205) from (steps, sensors, sources)
-    blocks (numpy on the host or a CUDA tensor). ``keep_channel_layout`` is
-    accepted for signature parity; the EWP backend it serves is out of scope."""
+    blocks (numpy on the host or a CUDA tensor). ``keep_channel_layout`` keeps
+    the channel-major spectrum the EWP backend streams (SetupOptions,
+    block_operator.hpp:58-60), built on the device on first EWP use."""
     if len(blocks.shape) != 3:
         raise DimensionError("blocks must be (steps, sensors, sources)")
     nt, nd, nm = (int(s) for s in blocks.shape)
@@ -314,6 +355,8 @@ def setup(blocks, keep_channel_layout: bool = False, precision: int = BTG_F64,
             raise DimensionError("compact operator: all dimensions must be positive")
         op = create(nd, nm, nt, precision, 0 if device is None else device)
     op.setup_rows(blocks, 0, nd)
+    if keep_channel_layout:
+        check(_lib.load().btg_set_channel_layout(op._h, 1))
     return op
 
 

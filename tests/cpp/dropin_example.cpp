@@ -48,8 +48,27 @@ int main() {
         for (std::size_t t = 1; t < 6; ++t) CHECK(std::abs(dv.at(s, t) - v.at(s, t - 1)) < 1e-12);
     }
 
-    // typed errors
+    // EWP backend: needs keep_channel_layout, then agrees with the FFT backend
     bool threw = false;
+    CHECK(!sop.has_channel_layout());
+    try {
+        apply_forward_ewp(sop, v);
+    } catch (const Error&) {
+        threw = true;
+    }
+    CHECK(threw);
+    SetupOptions keep;
+    keep.keep_channel_layout = true;
+    SpectralP2O eop = setup(sh, keep);
+    CHECK(eop.has_channel_layout());
+    SpaceTimeVector de = apply_forward_ewp(eop, v);
+    for (std::size_t k = 0; k < de.values.size(); ++k) CHECK(std::abs(de.values[k] - dv.values[k]) < 1e-12);
+    SpaceTimeVector ae = apply_adjoint_ewp(eop, dv);
+    SpaceTimeVector af = apply_adjoint(sop, dv);
+    for (std::size_t k = 0; k < ae.values.size(); ++k) CHECK(std::abs(ae.values[k] - af.values[k]) < 1e-12);
+
+    // typed errors
+    threw = false;
     try {
         apply_forward(op, SpaceTimeVector::zeros(4, 8, Ordering::SOTI));
     } catch (const DimensionError&) {

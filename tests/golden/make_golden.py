@@ -105,7 +105,24 @@ def distributed_case():
     return out
 
 
+def ewp_case():
+    """EWP backend (apply_forward_ewp / apply_adjoint_ewp, block_operator.cpp:345-421)
+    on a reference operator set up with keep_channel_layout: configs[0] with seed
+    1 and a ragged 7 x 45 x 37 case."""
+    out = {}
+    for tag, (seed, nd, nm, nt) in (("a", (1, 8, 256, 64)), ("r", (77, 7, 45, 37))):
+        blocks, m, d = ref_problem(seed, nd, nm, nt)
+        op = refcpu.RefSpectralOperator(blocks, keep_channel_layout=True)
+        out[f"{tag}_seed"] = seed
+        out[f"{tag}_dims"] = np.array([nd, nm, nt])
+        out[f"{tag}_fingerprint"] = fingerprint(blocks, m, d)
+        out[f"{tag}_fwd"] = op.apply_forward_ewp(m)
+        out[f"{tag}_adj"] = op.apply_adjoint_ewp(d)
+    return out
+
+
 def main():
+    np.savez_compressed(OUT / "ewp_case.npz", **ewp_case())
     np.savez_compressed(OUT / "config_a_seed1.npz", **config_a(1, full=True))
     np.savez_compressed(OUT / "config_a_seed20240901.npz", **config_a(20240901, full=False))
     np.savez_compressed(OUT / "small_case.npz", **small_case())
