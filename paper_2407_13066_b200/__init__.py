@@ -8,6 +8,7 @@ Python surface (operator, solver, files) plus the multi-GPU grid
 """
 
 from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
+from .distributed import distributed_adjoint, distributed_forward  # noqa: F401
 from .io import load_operator, peek_operator, read_vector, save_operator, write_vector  # noqa: F401
 from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
 from .planner import comm_cost, modified_cost, parse_grid, plan_grid, select_grid, weak_scaling_shape  # noqa: F401
@@ -23,6 +24,8 @@ __all__ = [
     "HessianOperator",
     "SpectralOperator",
     "cg_solve",
+    "distributed_adjoint",
+    "distributed_forward",
     "comm_cost",
     "modified_cost",
     "parse_grid",

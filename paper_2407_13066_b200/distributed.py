@@ -29,7 +29,8 @@ from typing import List, Optional, Tuple
 
 from ._lib import GridError
 
-__all__ = ["Shard", "CommEvent", "partition_bounds", "GridEngine", "synthetic_shard_operator"]
+__all__ = ["Shard", "CommEvent", "partition_bounds", "GridEngine", "synthetic_shard_operator", "distributed_forward",
+           "distributed_adjoint"]
 
 
 @dataclass(frozen=True)
@@ -331,3 +332,83 @@ class GridEngine:
         if self.local_op is not None and hasattr(self.local_op, "close"):
             self.local_op.close()
         self.local_op = None
+
+
+# ---------------------------------------------------------------------------
+# Single-process logical grid: the reference module's distributed_forward /
+# distributed_adjoint (python/src/bindings.cpp:148-172 over distributed.cpp:
+# 312-392). Every grid cell's shard is set up as its own device operator —
+# spread round-robin over the visible GPUs — and the partial results are summed
+# with the reference's fixed binary tree (tree_reduce, distributed.cpp:36-47),
+# on the host, in the same order.
+# ---------------------------------------------------------------------------
+def _tree_reduce(partials):
+    """((v0 + v1) + (v2 + v3)) + ...: tree_reduce (distributed.cpp:36-47)."""
+    parts = [p.copy() for p in partials]
+    step = 1
+    while step < len(parts):
+        for i in range(0, len(parts) - step, 2 * step):
+            parts[i] += parts[i + step]
+        step *= 2
+    return parts[0]
+
+
+def _grid_apply(blocks, x, grid: str, backend: str, adjoint: bool, devices=None):
+    import numpy as np
+
+    from ._lib import DimensionError, Error
+    from .operator import setup
+    from .planner import parse_grid
+
+    if backend not in ("fft", "ewp"):
+        raise Error(f"backend '{backend}': the GPU path provides 'fft' and 'ewp' (the 'naive' "
+                    "direct sum is the reference's test oracle)")
+    blocks = np.ascontiguousarray(blocks, dtype=np.float64)
+    if blocks.ndim != 3:
+        raise DimensionError("blocks must be (steps, sensors, sources)")
+    nt, nd, nm = blocks.shape
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    din, dout = (nd, nm) if adjoint else (nm, nd)
+    if x.shape != (din, nt):
+        raise DimensionError(f"distributed_{'adjoint' if adjoint else 'forward'}: vector is {x.shape}, "
+                             f"expected ({din}, {nt})")
+    rows, cols = parse_grid(grid)
+    shards = partition_bounds(nd, nm, rows, cols)
+    if devices is None:
+        import torch
+
+        devices = list(range(max(1, torch.cuda.device_count())))
+    out = np.zeros((dout, nt))
+    # F: row i sums its cells' partial d over j; F*: column j sums over i
+    groups = ([[s for s in shards if s.grid_row == i] for i in range(rows)] if not adjoint
+              else [[s for s in shards if s.grid_col == j] for j in range(cols)])
+    for cells in groups:
+        partials = []
+        for s in cells:
+            n_out = s.local_sources if adjoint else s.local_sensors
+            if s.empty:
+                partials.append(np.zeros((n_out, nt)))
+                continue
+            dev = devices[(s.grid_row * cols + s.grid_col) % len(devices)]
+            local = blocks[:, s.sensor_begin:s.sensor_end, s.source_begin:s.source_end]
+            with setup(local, keep_channel_layout=backend == "ewp", device=dev) as op:
+                xs = x[s.sensor_begin:s.sensor_end] if adjoint else x[s.source_begin:s.source_end]
+                if backend == "ewp":
+                    partials.append(op.apply_adjoint_ewp(xs) if adjoint else op.apply_forward_ewp(xs))
+                else:
+                    partials.append(op.apply_adjoint(xs) if adjoint else op.apply_forward(xs))
+        s0 = cells[0]
+        lo, hi = (s0.source_begin, s0.source_end) if adjoint else (s0.sensor_begin, s0.sensor_end)
+        if hi > lo:
+            out[lo:hi] = _tree_reduce(partials)
+    return out
+
+
+def distributed_forward(blocks, m, grid: str = "1x1", backend: str = "fft", devices=None):
+    """The reference module's distributed_forward(blocks, m, grid, backend)."""
+    return _grid_apply(blocks, m, grid, backend, adjoint=False, devices=devices)
+
+
+def distributed_adjoint(blocks, d, grid: str = "1x1", backend: str = "fft", devices=None):
+    """The reference module's distributed_adjoint(blocks, d, grid, backend)."""
+    return _grid_apply(blocks, d, grid, backend, adjoint=True, devices=devices)

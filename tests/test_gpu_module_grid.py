@@ -1,0 +1,38 @@
+"""The reference module's single-process grid entry points,
+distributed_forward / distributed_adjoint(blocks, m, grid, backend)
+(python/src/bindings.cpp:148-172), on the GPU: against the reference's own
+distributed results (tests/golden/distributed_case.npz, test_smoke.py:68-78
+grids), with both backends."""
+
+import numpy as np
+import pytest
+
+from oracle import restate as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def btg():
+    import paper_2407_13066_b200 as m
+
+    return m
+
+
+@pytest.mark.parametrize("grid", ["1x4", "2x2", "4x1", "2x3"])
+@pytest.mark.parametrize("backend", ["fft", "ewp"])
+def test_module_grid_matches_reference(btg, golden_dir, grid, backend):
+    g = np.load(golden_dir / "distributed_case.npz")
+    blocks, m, d = R.random_problem(5, 5, 7, 12)
+    assert R.rel_l2(btg.distributed_forward(blocks, m, grid, backend), g[f"fwd_{grid}"]) <= 1e-12
+    assert R.rel_l2(btg.distributed_adjoint(blocks, d, grid, backend), g[f"adj_{grid}"]) <= 1e-12
+
+
+def test_module_grid_errors(btg):
+    blocks, m, _ = R.random_problem(5, 5, 7, 12)
+    with pytest.raises(ValueError):  # GridError: more rows than sensors (distributed.cpp:147-152)
+        btg.distributed_forward(blocks, m, "6x1")
+    with pytest.raises(RuntimeError):
+        btg.distributed_forward(blocks, m, "1x1", backend="naive")
+    with pytest.raises(ValueError):
+        btg.distributed_forward(blocks, m[:3], "1x2")
