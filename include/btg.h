@@ -174,6 +174,15 @@ typedef enum { BTG_MRHS_DMMA = 0, BTG_MRHS_TENSOR_I8 = 1 } btg_mrhs_engine;
  * it the EWP calls fail with BTG_EARG like require_channel_layout
  * (block_operator.cpp:335-341). One right-hand side, SOTI vectors. */
 btg_status btg_set_channel_layout(btg_op op, int keep);
+
+/* Naive backend (naive_apply_forward / naive_apply_adjoint,
+ * block_operator.cpp:423-482): the direct O(N_t^2 N_d N_m) triangular sum on the
+ * compact TOSI blocks (N_t x N_d x N_m) with SOTI vectors, in the reference's
+ * summation order; stateless (no handle). */
+btg_status btg_naive_forward(const double* blocks, size_t num_sensors, size_t num_sources, size_t num_steps,
+                             const double* m, double* d, int device, unsigned flags);
+btg_status btg_naive_adjoint(const double* blocks, size_t num_sensors, size_t num_sources, size_t num_steps,
+                             const double* d, double* m, int device, unsigned flags);
 btg_status btg_has_channel_layout(btg_op op, int* out);
 btg_status btg_forward_ewp(btg_op op, const double* m, size_t m_len, double* d, size_t d_len, unsigned flags);
 btg_status btg_adjoint_ewp(btg_op op, const double* d, size_t d_len, double* m, size_t m_len, unsigned flags);

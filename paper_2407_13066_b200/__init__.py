@@ -10,7 +10,8 @@ Python surface (operator, solver, files) plus the multi-GPU grid
 from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
 from .distributed import distributed_adjoint, distributed_forward  # noqa: F401
 from .io import load_operator, peek_operator, read_vector, save_operator, write_vector  # noqa: F401
-from .operator import HessianOperator, SpectralOperator, create, fill_uniform, setup  # noqa: F401
+from .operator import (HessianOperator, SpectralOperator, create, fill_uniform, naive_apply_adjoint,  # noqa: F401
+                       naive_apply_forward, setup)
 from .planner import comm_cost, modified_cost, parse_grid, plan_grid, select_grid, weak_scaling_shape  # noqa: F401
 from .solver import cg_solve, cg_solve_op, objective_eval  # noqa: F401
 
@@ -36,6 +37,8 @@ __all__ = [
     "create",
     "fill_uniform",
     "load_operator",
+    "naive_apply_adjoint",
+    "naive_apply_forward",
     "objective_eval",
     "peek_operator",
     "read_vector",

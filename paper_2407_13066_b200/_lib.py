@@ -35,6 +35,8 @@ EXPORTED = (
     "btg_set_channel_layout",
     "btg_has_channel_layout",
     "btg_forward_ewp",
+    "btg_naive_forward",
+    "btg_naive_adjoint",
     "btg_adjoint_ewp",
     "btg_get_counters",
     "btg_reset_counters",
@@ -180,6 +182,8 @@ def load():
     L.btg_set_channel_layout.argtypes = [_vp, ctypes.c_int]
     L.btg_has_channel_layout.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
     L.btg_forward_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
+    for name in ("btg_naive_forward", "btg_naive_adjoint"):
+        getattr(L, name).argtypes = [_dp, _sz, _sz, _sz, _dp, _dp, ctypes.c_int, ctypes.c_uint]
     L.btg_adjoint_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
     L.btg_get_counters.argtypes = [_vp, ctypes.POINTER(Counters)]
     L.btg_reset_counters.argtypes = [_vp]

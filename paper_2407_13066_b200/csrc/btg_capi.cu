@@ -874,6 +874,52 @@ btg_status ewp_dir(btg_op op, bool adjoint, const double* in, size_t in_len, dou
 }
 }  // namespace
 
+namespace {
+btg_status naive_dir(bool adjoint, const double* blocks, size_t nd, size_t nm, size_t nt, const double* in,
+                     double* out, int device, unsigned flags) {
+    if (!blocks || !in || !out) return fail(BTG_EARG, "null pointer");
+    if (nd == 0 || nm == 0 || nt == 0) return fail(BTG_EDIM, "compact operator: all dimensions must be positive");
+    if (nd > INT32_MAX || nm > INT32_MAX || nt > INT32_MAX) return fail(BTG_EDIM, "naive backend: dimension too large");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count)
+        return fail(BTG_ECUDA, "no CUDA device %d", device);
+    DeviceGuard g(device);
+    const size_t nb = nt * nd * nm, nin = (adjoint ? nd : nm) * nt, nout = (adjoint ? nm : nd) * nt;
+    const double *b_d = blocks, *in_d = in;
+    double* out_d = out;
+    double* tmp = nullptr;
+    const bool host = !(flags & BTG_DEVICE_PTRS);
+    if (host) {
+        BTG_CUDA(cudaMalloc(&tmp, (nb + nin + nout) * sizeof(double)));
+        cudaError_t e = cudaMemcpy(tmp, blocks, nb * sizeof(double), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(tmp + nb, in, nin * sizeof(double), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(tmp);
+            return fail(BTG_ECUDA, "naive backend upload: %s", cudaGetErrorString(e));
+        }
+        b_d = tmp;
+        in_d = tmp + nb;
+        out_d = tmp + nb + nin;
+    }
+    cudaError_t e = btg::launch_naive(adjoint, b_d, in_d, out_d, (int)nd, (int)nm, (int)nt, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && host) e = cudaMemcpy(out, out_d, nout * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(BTG_ECUDA, "naive backend: %s", cudaGetErrorString(e));
+    return BTG_OK;
+}
+}  // namespace
+
+btg_status btg_naive_forward(const double* blocks, size_t nd, size_t nm, size_t nt, const double* m, double* d,
+                             int device, unsigned flags) {
+    return naive_dir(false, blocks, nd, nm, nt, m, d, device, flags);
+}
+
+btg_status btg_naive_adjoint(const double* blocks, size_t nd, size_t nm, size_t nt, const double* d, double* m,
+                             int device, unsigned flags) {
+    return naive_dir(true, blocks, nd, nm, nt, d, m, device, flags);
+}
+
 btg_status btg_forward_ewp(btg_op op, const double* m, size_t m_len, double* d, size_t d_len, unsigned flags) {
     if (!op) return fail(BTG_EARG, "null operator handle");
     std::lock_guard<std::mutex> lock(op->mu);

@@ -113,6 +113,10 @@ template <typename T>
 cudaError_t launch_ewp(bool adjoint, const T* S, const double2* in, double2* out, int nf, int nd, int nm,
                        cudaStream_t stream);
 
+// Naive backend (btg_naive.cu): direct triangular sum on the compact operator.
+cudaError_t launch_naive(bool adjoint, const double* blocks, const double* in, double* out, int nd, int nm, int nt,
+                         cudaStream_t stream);
+
 // Bq: workspace of oz_presliced_bytes(nf, nd) for the adjoint's pre-sliced d-hat tiles.
 size_t oz_presliced_bytes(int nf, int nd);
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,

@@ -357,12 +357,11 @@ def _grid_apply(blocks, x, grid: str, backend: str, adjoint: bool, devices=None)
     import numpy as np
 
     from ._lib import DimensionError, Error
-    from .operator import setup
+    from .operator import naive_apply_adjoint, naive_apply_forward, setup
     from .planner import parse_grid
 
-    if backend not in ("fft", "ewp"):
-        raise Error(f"backend '{backend}': the GPU path provides 'fft' and 'ewp' (the 'naive' "
-                    "direct sum is the reference's test oracle)")
+    if backend not in ("fft", "ewp", "naive"):
+        raise Error(f"unknown backend '{backend}' (expected fft, ewp or naive)")  # parse_backend
     blocks = np.ascontiguousarray(blocks, dtype=np.float64)
     if blocks.ndim != 3:
         raise DimensionError("blocks must be (steps, sensors, sources)")
@@ -391,6 +390,10 @@ def _grid_apply(blocks, x, grid: str, backend: str, adjoint: bool, devices=None)
                 continue
             dev = devices[(s.grid_row * cols + s.grid_col) % len(devices)]
             local = blocks[:, s.sensor_begin:s.sensor_end, s.source_begin:s.source_end]
+            if backend == "naive":
+                xs = x[s.sensor_begin:s.sensor_end] if adjoint else x[s.source_begin:s.source_end]
+                partials.append(naive_apply_adjoint(local, xs, dev) if adjoint else naive_apply_forward(local, xs, dev))
+                continue
             with setup(local, keep_channel_layout=backend == "ewp", device=dev) as op:
                 xs = x[s.sensor_begin:s.sensor_end] if adjoint else x[s.source_begin:s.source_end]
                 if backend == "ewp":

@@ -377,3 +377,31 @@ def fill_uniform(tensor, seed: int, offset: int = 0, lo: float = -1.0, hi: float
         a, b, c = tensor.shape
         check(L.btg_fill_uniform_3d(tensor.data_ptr(), a, b, c, seed & (2**64 - 1), offset, strides[0], strides[1],
                                     lo, hi, stream))
+
+
+def _naive(blocks, x, adjoint: bool, device: Optional[int]):
+    blocks = np.ascontiguousarray(blocks, dtype=np.float64)
+    if blocks.ndim != 3:
+        raise DimensionError("blocks must be (steps, sensors, sources)")
+    nt, nd, nm = blocks.shape
+    what = "naive_apply_adjoint" if adjoint else "naive_apply_forward"
+    din, dout = (nd, nm) if adjoint else (nm, nd)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.shape != (din, nt):
+        raise DimensionError(f"{what}: input does not match operator")
+    out = np.empty((dout, nt))
+    fn = _lib.load().btg_naive_adjoint if adjoint else _lib.load().btg_naive_forward
+    check(fn(blocks.ctypes.data, nd, nm, nt, x.ctypes.data, out.ctypes.data, 0 if device is None else device, 0))
+    return out
+
+
+def naive_apply_forward(blocks, m, device: Optional[int] = None):
+    """The reference module's naive_apply_forward(blocks, m) (block_operator.cpp:423-450):
+    direct triangular sum on the GPU; SOTI vectors."""
+    return _naive(blocks, m, False, device)
+
+
+def naive_apply_adjoint(blocks, d, device: Optional[int] = None):
+    """naive_apply_adjoint (block_operator.cpp:452-482)."""
+    return _naive(blocks, d, True, device)
+

@@ -20,7 +20,7 @@ def btg():
 
 
 @pytest.mark.parametrize("grid", ["1x4", "2x2", "4x1", "2x3"])
-@pytest.mark.parametrize("backend", ["fft", "ewp"])
+@pytest.mark.parametrize("backend", ["fft", "ewp", "naive"])
 def test_module_grid_matches_reference(btg, golden_dir, grid, backend):
     g = np.load(golden_dir / "distributed_case.npz")
     blocks, m, d = R.random_problem(5, 5, 7, 12)
@@ -33,6 +33,18 @@ def test_module_grid_errors(btg):
     with pytest.raises(ValueError):  # GridError: more rows than sensors (distributed.cpp:147-152)
         btg.distributed_forward(blocks, m, "6x1")
     with pytest.raises(RuntimeError):
-        btg.distributed_forward(blocks, m, "1x1", backend="naive")
+        btg.distributed_forward(blocks, m, "1x1", backend="blas")
     with pytest.raises(ValueError):
         btg.distributed_forward(blocks, m[:3], "1x2")
+
+
+def test_naive_backend_matches_reference_naive(btg, golden_dir):
+    """naive_apply_forward at configs[0] against the reference's own naive
+    result, and the naive adjoint against the FFT adjoint."""
+    g = np.load(golden_dir / "config_a_seed1.npz")
+    nd, nm, nt = (int(x) for x in g["dims"])
+    blocks, m, d = R.random_problem(int(g["seed"]), nd, nm, nt)
+    assert R.rel_l2(btg.naive_apply_forward(blocks, m), g["naive_fwd"]) <= 1e-13
+    assert R.rel_l2(btg.naive_apply_adjoint(blocks, d), g["adj"]) <= 1e-12
+    with pytest.raises(ValueError):
+        btg.naive_apply_forward(blocks, m[:, :5])
