@@ -220,6 +220,13 @@ btg_status btg_load_operator(const char* path, int precision, int device, btg_op
  * block, no re-setup (partition_operator(SpectralP2O), distributed.cpp:198-218). */
 btg_status btg_load_operator_rect(const char* path, size_t i0, size_t i1, size_t j0, size_t j1,
                                   int precision, int device, btg_op* out);
+/* io::write_operator(CompactP2O) / io::read_compact_operator (io.cpp:97-111,159-180):
+ * time-domain TOSI files of the first block column (N_t x N_d x N_m). read:
+ * blocks == NULL queries the dimensions only. */
+btg_status btg_write_compact(const char* path, const double* blocks, size_t num_sensors, size_t num_sources,
+                             size_t num_steps);
+btg_status btg_read_compact(const char* path, double* blocks, size_t capacity, size_t* num_sensors,
+                            size_t* num_sources, size_t* num_steps);
 /* io::write_operator(SpectralP2O): the reference's 2 N_t frequency-domain file. */
 btg_status btg_save_operator(btg_op op, const char* path);
 btg_status btg_write_vector(const char* path, const double* values, size_t spatial_dim,
@@ -247,6 +254,15 @@ btg_status btg_weak_scaling_shape(double local_ratio, size_t workers, int* indif
 btg_status btg_modified_cost(double rows, size_t workers, double log_dim_ratio, double* out);
 btg_status btg_comm_cost(size_t rows, size_t cols, size_t num_sources, size_t num_sensors, size_t num_steps,
                          double latency, double bandwidth, double* out);
+/* CostEstimate / conventional_cost_estimate (grid_planner.hpp:84-97) and
+ * apply_arithmetic_intensity (grid_planner.hpp:100). */
+typedef struct {
+    double per_solve_flops, effective_rank, conventional_total_flops, fft_setup_flops, fft_matvec_flops,
+        fft_total_flops, ratio;
+} btg_cost_estimate;
+btg_status btg_conventional_cost_estimate(double grid_points, double num_steps, double num_sensors,
+                                          double rank_fraction, btg_cost_estimate* out);
+double btg_apply_arithmetic_intensity(double local_sensors, double local_sources);
 
 /* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */
 btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes);

@@ -9,10 +9,12 @@ Python surface (operator, solver, files) plus the multi-GPU grid
 
 from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
 from .distributed import distributed_adjoint, distributed_forward  # noqa: F401
-from .io import load_operator, peek_operator, read_vector, save_operator, write_vector  # noqa: F401
+from .io import (load_operator, peek_operator, read_operator, read_vector, save_operator,  # noqa: F401
+                 write_operator, write_vector)
 from .operator import (HessianOperator, SpectralOperator, create, fill_uniform, naive_apply_adjoint,  # noqa: F401
                        naive_apply_forward, setup)
-from .planner import comm_cost, modified_cost, parse_grid, plan_grid, select_grid, weak_scaling_shape  # noqa: F401
+from .planner import (apply_arithmetic_intensity, comm_cost, conventional_cost_estimate, modified_cost,  # noqa: F401
+                      parse_grid, plan_grid, select_grid, weak_scaling_shape)
 from .solver import cg_solve, cg_solve_op, objective_eval  # noqa: F401
 
 __all__ = [
@@ -24,7 +26,9 @@ __all__ = [
     "SolverError",
     "HessianOperator",
     "SpectralOperator",
+    "apply_arithmetic_intensity",
     "cg_solve",
+    "conventional_cost_estimate",
     "distributed_adjoint",
     "distributed_forward",
     "comm_cost",
@@ -41,8 +45,10 @@ __all__ = [
     "naive_apply_forward",
     "objective_eval",
     "peek_operator",
+    "read_operator",
     "read_vector",
     "save_operator",
     "setup",
+    "write_operator",
     "write_vector",
 ]

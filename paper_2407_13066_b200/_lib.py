@@ -36,6 +36,10 @@ EXPORTED = (
     "btg_has_channel_layout",
     "btg_forward_ewp",
     "btg_naive_forward",
+    "btg_write_compact",
+    "btg_read_compact",
+    "btg_conventional_cost_estimate",
+    "btg_apply_arithmetic_intensity",
     "btg_naive_adjoint",
     "btg_adjoint_ewp",
     "btg_get_counters",
@@ -182,6 +186,12 @@ def load():
     L.btg_set_channel_layout.argtypes = [_vp, ctypes.c_int]
     L.btg_has_channel_layout.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
     L.btg_forward_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
+    L.btg_conventional_cost_estimate.argtypes = [ctypes.c_double] * 4 + [ctypes.POINTER(ctypes.c_double * 7)]
+    L.btg_apply_arithmetic_intensity.argtypes = [ctypes.c_double, ctypes.c_double]
+    L.btg_apply_arithmetic_intensity.restype = ctypes.c_double
+    L.btg_write_compact.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, _sz]
+    L.btg_read_compact.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_sz),
+                                   ctypes.POINTER(_sz)]
     for name in ("btg_naive_forward", "btg_naive_adjoint"):
         getattr(L, name).argtypes = [_dp, _sz, _sz, _sz, _dp, _dp, ctypes.c_int, ctypes.c_uint]
     L.btg_adjoint_ewp.argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
@@ -220,7 +230,7 @@ def load():
     L.btg_comm_cost.argtypes = [_sz, _sz, _sz, _sz, _sz, ctypes.c_double, ctypes.c_double,
                                 ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTED:
-        if name not in ("btg_last_error", "btg_abi_version", "btg_destroy"):
+        if name not in ("btg_last_error", "btg_abi_version", "btg_destroy", "btg_apply_arithmetic_intensity"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

@@ -88,6 +88,32 @@ btg_status btg_comm_cost(size_t rows, size_t cols, size_t num_sources, size_t nu
     return BTG_OK;
 }
 
+// conventional_cost_estimate (grid_planner.cpp:282-299): conventional
+// (solve-based) vs FFT-based Hessian cost model of the paper's Table 1.
+btg_status btg_conventional_cost_estimate(double grid_points, double num_steps, double num_sensors,
+                                          double rank_fraction, btg_cost_estimate* out) {
+    if (!out) return btg_internal_fail(BTG_EARG, "null output");
+    if (grid_points <= 0.0 || num_steps <= 0.0 || num_sensors <= 0.0 || rank_fraction <= 0.0)
+        return btg_internal_fail(BTG_EARG, "cost estimate: all inputs must be positive");
+    const double state_dim = 3.0 * grid_points;  // 3 values per grid point
+    out->per_solve_flops = 324.0 * state_dim * num_steps;
+    out->effective_rank = num_sensors * num_steps * rank_fraction;
+    out->conventional_total_flops = 2.0 * out->effective_rank * out->per_solve_flops;
+    const double num_sources = std::pow(grid_points, 2.0 / 3.0);  // surface field
+    out->fft_setup_flops = num_sensors * out->per_solve_flops;
+    out->fft_matvec_flops = 2.0 * out->effective_rank * 8.0 * num_sources * num_sensors * num_steps;
+    out->fft_total_flops = out->fft_setup_flops + out->fft_matvec_flops;
+    out->ratio = out->conventional_total_flops / out->fft_total_flops;
+    return BTG_OK;
+}
+
+// apply_arithmetic_intensity (grid_planner.cpp:301-304): flop/byte of the
+// Fourier-space step on an n_d x n_m shard.
+double btg_apply_arithmetic_intensity(double local_sensors, double local_sources) {
+    const double prod = local_sensors * local_sources;
+    return prod / (2.0 * (prod + local_sources + local_sensors));
+}
+
 btg_status btg_select_grid(size_t workers, double log_dim_ratio, unsigned gpus_per_node, size_t* rows,
                            size_t* cols) {
     if (!rows || !cols) return btg_internal_fail(BTG_EARG, "null output");

@@ -206,6 +206,51 @@ btg_status btg_save_operator(btg_op op, const char* path) {
     return BTG_OK;
 }
 
+// io::write_operator(CompactP2O) (io.cpp:97-111): time-domain TOSI file.
+btg_status btg_write_compact(const char* path, const double* blocks, size_t nd, size_t nm, size_t nt) {
+    if (!path || !blocks) return btg_internal_fail(BTG_EARG, "null argument");
+    if (nd == 0 || nm == 0 || nt == 0)
+        return btg_internal_fail(BTG_EDIM, "compact operator: all dimensions must be positive");
+    File fh;
+    fh.f = std::fopen(path, "wb");
+    if (!fh.f) return ferr(std::string("cannot open '") + path + "' for writing");
+    unsigned char h[kHeader] = {};
+    std::memcpy(h, "BTOP", 4);
+    put_u32(h + 4, kVersion);
+    put_u32(h + 8, 0);   // TOSI
+    put_u32(h + 12, 0);  // time domain
+    put_u64(h + 16, nd);
+    put_u64(h + 24, nm);
+    put_u64(h + 32, nt);
+    put_u32(h + 40, 0);  // real
+    if (std::fwrite(h, 1, kHeader, fh.f) != kHeader) return ferr("failed writing the header");
+    const size_t n = nt * nd * nm;
+    if (std::fwrite(blocks, sizeof(double), n, fh.f) != n) return ferr("failed writing the payload");
+    return BTG_OK;
+}
+
+// io::read_compact_operator (io.cpp:159-180); blocks == NULL queries the dimensions.
+btg_status btg_read_compact(const char* path, double* blocks, size_t capacity, size_t* nd, size_t* nm,
+                            size_t* nt) {
+    btg_file_header h{};
+    btg_status s = btg_peek_operator(path, &h);
+    if (s != BTG_OK) return s;
+    if (h.domain != 0 || h.complex_scalar)
+        return ferr(std::string("'") + path +
+                    "' holds a frequency-domain operator; a time-domain compact operator was expected");
+    if (h.ordering != 0) return ferr(std::string("'") + path + "': compact operators must be TOSI-ordered");
+    if (nd) *nd = h.num_sensors;
+    if (nm) *nm = h.num_sources;
+    if (nt) *nt = h.num_steps;
+    if (!blocks) return BTG_OK;
+    const size_t n = h.num_steps * h.num_sensors * h.num_sources;
+    if (capacity < n) return btg_internal_fail(BTG_EDIM, "read_compact: destination too small");
+    File fh;
+    fh.f = std::fopen(path, "rb");
+    if (!fh.f || !read_at(fh.f, kHeader, blocks, n * sizeof(double))) return ferr("file truncated");
+    return BTG_OK;
+}
+
 btg_status btg_write_vector(const char* path, const double* values, size_t spatial_dim, size_t num_steps,
                             int ordering) {
     if (!path || (!values && spatial_dim * num_steps != 0)) return btg_internal_fail(BTG_EARG, "null argument");

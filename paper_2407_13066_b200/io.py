@@ -19,7 +19,8 @@ from . import _lib
 from ._lib import check
 from .operator import SpectralOperator
 
-__all__ = ["peek_operator", "load_operator", "load_operator_rect", "save_operator", "read_vector", "write_vector"]
+__all__ = ["peek_operator", "load_operator", "load_operator_rect", "save_operator", "read_vector", "write_vector",
+           "read_operator", "write_operator"]
 
 
 def peek_operator(path) -> dict:
@@ -84,3 +85,27 @@ def read_vector(path) -> np.ndarray:
     if o.value == 1:
         return flat.reshape(sp.value, st.value)
     return np.ascontiguousarray(flat.reshape(st.value, sp.value).T)
+
+
+def write_operator(path, blocks) -> None:
+    """The reference module's write_operator(path, blocks) (bindings.cpp:306-310,
+    io.cpp:97-111): a time-domain TOSI file of (steps, sensors, sources) blocks."""
+    b = np.ascontiguousarray(blocks, dtype=np.float64)
+    if b.ndim != 3:
+        raise _lib.DimensionError("blocks must be (steps, sensors, sources)")
+    nt, nd, nm = b.shape
+    check(_lib.load().btg_write_compact(str(Path(path)).encode(), b.ctypes.data, nd, nm, nt))
+
+
+def read_operator(path) -> np.ndarray:
+    """read_operator(path) (bindings.cpp:311-315, io.cpp:159-180): the compact
+    (steps, sensors, sources) blocks of a time-domain file; FormatError for a
+    frequency-domain one."""
+    L = _lib.load()
+    p = str(Path(path)).encode()
+    nd, nm, nt = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    check(L.btg_read_compact(p, None, 0, ctypes.byref(nd), ctypes.byref(nm), ctypes.byref(nt)))
+    out = np.empty((nt.value, nd.value, nm.value), dtype=np.float64)
+    check(L.btg_read_compact(p, out.ctypes.data, out.size, None, None, None))
+    return out
+

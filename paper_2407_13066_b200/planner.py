@@ -69,3 +69,20 @@ def parse_grid(text: str) -> Tuple[int, int]:
     if r <= 0 or c <= 0:
         raise _lib.Error("grid shape: rows and cols must be positive")
     return r, c
+
+
+def conventional_cost_estimate(grid_points: float, num_steps: float, num_sensors: float,
+                               rank_fraction: float = 0.1) -> dict:
+    """conventional_cost_estimate (grid_planner.cpp:282-299), as the reference module's dict."""
+    v = (ctypes.c_double * 7)()
+    check(_lib.load().btg_conventional_cost_estimate(float(grid_points), float(num_steps), float(num_sensors),
+                                                     float(rank_fraction), ctypes.byref(v)))
+    keys = ("per_solve_flops", "effective_rank", "conventional_total_flops", "fft_setup_flops",
+            "fft_matvec_flops", "fft_total_flops", "ratio")
+    return dict(zip(keys, list(v)))
+
+
+def apply_arithmetic_intensity(local_sensors: float, local_sources: float) -> float:
+    """apply_arithmetic_intensity (grid_planner.cpp:301-304)."""
+    return float(_lib.load().btg_apply_arithmetic_intensity(float(local_sensors), float(local_sources)))
+

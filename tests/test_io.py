@@ -65,3 +65,40 @@ def test_operator_files_round_trip_through_the_reference(tmp_path):
         assert R.rel_l2(op3.apply_adjoint(d), ref.apply_adjoint(d)) <= 1e-12
     with bio.load_operator(tmp_path / "ref_freq.btop", precision=32) as op4:
         assert R.rel_l2(op4.apply_forward(m), ref.apply_forward(m)) <= 1e-5
+
+
+@needs_ref
+def test_compact_operator_files_byte_identical_with_reference(tmp_path):
+    """The module's write_operator / read_operator (bindings.cpp:306-315): our
+    time-domain file is byte-identical to the reference's io::write_operator,
+    and each side reads the other's file back exactly."""
+    import paper_2407_13066_b200 as btg
+
+    blocks, _, _ = R.random_problem(62, 3, 5, 7)
+    btg.write_operator(tmp_path / "ours.btop", blocks)
+    refcpu.write_compact(tmp_path / "ref.btop", blocks)
+    assert (tmp_path / "ours.btop").read_bytes() == (tmp_path / "ref.btop").read_bytes()
+    np.testing.assert_array_equal(btg.read_operator(tmp_path / "ref.btop"), blocks)
+    # a frequency-domain file is not a compact operator (io.cpp:161-163)
+    (tmp_path / "freq.btop").write_bytes(b"BTOP" + (1).to_bytes(4, "little") + (0).to_bytes(4, "little")
+                                         + (1).to_bytes(4, "little") + (1).to_bytes(8, "little") * 3
+                                         + (1).to_bytes(4, "little") + bytes(20) + bytes(32))
+    with pytest.raises(btg.FormatError):
+        btg.read_operator(tmp_path / "freq.btop")
+
+
+def test_planner_cost_helpers_match_reference_formulas():
+    """conventional_cost_estimate / apply_arithmetic_intensity (grid_planner.cpp:282-304)."""
+    import paper_2407_13066_b200 as btg
+
+    est = btg.conventional_cost_estimate(1e6, 1000, 100, 0.1)
+    per = 324.0 * 3e6 * 1000
+    assert est["per_solve_flops"] == per
+    assert est["effective_rank"] == 100 * 1000 * 0.1
+    assert est["conventional_total_flops"] == 2.0 * 1e4 * per
+    fft = 100 * per + 2.0 * 1e4 * 8.0 * (1e6 ** (2.0 / 3.0)) * 100 * 1000
+    assert est["fft_total_flops"] == pytest.approx(fft, rel=1e-15)
+    assert est["ratio"] == pytest.approx(2.0 * 1e4 * per / fft, rel=1e-15)
+    with pytest.raises(RuntimeError):
+        btg.conventional_cost_estimate(0, 1, 1)
+    assert btg.apply_arithmetic_intensity(100, 32768) == pytest.approx(100 * 32768 / (2.0 * (100 * 32768 + 32868)))
