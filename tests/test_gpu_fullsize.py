@@ -79,3 +79,40 @@ def test_full_size_slices_and_pairing(dims):
         assert torch.equal(fsd, op.apply_adjoint(df))
     finally:
         op.close()
+
+
+@pytest.mark.parametrize("engine", ["dmma", "tensor_i8"])
+def test_configs3_multi_rhs_full_size(engine):
+    """configs[3] at full size (N_t=1024, N_d=128, N_m=16384, 32 right-hand
+    sides) on both multi-RHS engines: per-RHS column-slice parity (forward on
+    inputs supported on J, adjoint restricted to J) and the adjoint pairing
+    over every right-hand side."""
+    import torch
+
+    nt, nd, nm, nrhs = 1024, 128, 16384, 32
+    op = _build(nt, nd, nm)
+    try:
+        op.set_multi_rhs_engine(engine)
+        rng = np.random.default_rng(3)
+        J = np.sort(rng.choice(nm, size=16, replace=False))
+        spec_J = R.setup_full(R.synthetic_blocks_slice(SEED, nd, nm, nt, np.arange(nd), J))
+        MJ = rng.uniform(-1, 1, size=(nrhs, len(J), nt))
+        M = torch.zeros((nrhs, nm, nt), dtype=torch.float64, device="cuda:0")
+        M[:, torch.from_numpy(J).cuda()] = torch.from_numpy(MJ).cuda()
+        Dv = rng.uniform(-1, 1, size=(nrhs, nd, nt))
+        Fd = op.apply_forward(M).cpu().numpy()
+        A = op.apply_adjoint(torch.from_numpy(Dv).cuda()).cpu().numpy()
+        for r in range(nrhs):
+            assert R.rel_l2(Fd[r], R.apply_forward(spec_J, MJ[r])) <= 1e-12
+            assert R.rel_l2(A[r][J], R.apply_adjoint(spec_J, Dv[r])) <= 1e-12
+        from paper_2407_13066_b200 import fill_uniform
+
+        Mf = torch.empty((nrhs, nm, nt), dtype=torch.float64, device="cuda:0")
+        fill_uniform(Mf, 21)
+        Df = torch.from_numpy(Dv).cuda()
+        lhs = torch.sum(op.apply_forward(Mf) * Df, dim=(1, 2))
+        rhs = torch.sum(Mf * op.apply_adjoint(Df), dim=(1, 2))
+        assert float(torch.max(torch.abs(lhs - rhs) / torch.abs(lhs))) <= 1e-11
+    finally:
+        op.close()
+        torch.cuda.empty_cache()
