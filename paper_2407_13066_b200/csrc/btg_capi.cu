@@ -101,6 +101,8 @@ struct btg_op_s {
     int* oz_mB = nullptr;
     size_t oz_mB_cap = 0;
     uint8_t* oz_B = nullptr;  // adjoint: d-hat slices pre-sliced once per frequency
+    int16_t* oz_vexp = nullptr;  // forward: x-hat block exponents per channel group, from the R2C
+    size_t oz_vexp_cap = 0;
     size_t oz_B_cap = 0;
     bool oz_valid = false;
     bool keep_channel = false;  // EWP backend: SetupOptions::keep_channel_layout
@@ -245,12 +247,15 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // R2C of `channels` SOTI rows into a frequency-major array whose frequency
 // stride is `fs` (default: channels; a column chunk of a wider array otherwise).
-btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out, size_t fs = 0) {
+btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out, size_t fs = 0,
+                       const btg::R2CBlockMax* bm = nullptr) {
     StageClock clk(op, &op->counters.forward_fft);
     if (!fs) fs = channels;
     if (op->fast_ok && aligned16(v) && aligned16(out))
         BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, (long long)fs,
-                                          (int)channels, op->fast, op->stream));
+                                          (int)channels, op->fast, op->stream, bm ? *bm : btg::R2CBlockMax{}));
+    else if (bm)
+        return fail(BTG_EARG, "internal: block maxima need the fast R2C");
     else
         BTG_CUDA(btg::launch_r2c<double2>(v, (long long)op->nt, 1, out, (long long)fs, 1,
                                           (int)channels, (int)op->nt, op->plan, op->fft_batch, op->stream,
@@ -315,7 +320,8 @@ btg_status ensure_oz(btg_op op, size_t nrhs) {
     return BTG_OK;
 }
 
-btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, size_t nrhs) {
+btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, size_t nrhs,
+                     const int16_t* vexp = nullptr, int vexp_cpb = 1) {
     StageClock clk(op, &op->counters.apply);
     const size_t nin = adjoint ? op->nd : op->nm;
     const size_t nout = adjoint ? op->nm : op->nd;
@@ -326,7 +332,7 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
         BTG_TRY(ensure_oz(op, nrhs));
         e = btg::oz_apply(adjoint, op->oz_A, op->oz_mA, in, out, nf, nd, nm, (int)nrhs, op->oz_mB, op->oz_B,
-                          op->stream);
+                          op->stream, vexp, vexp_cpb);
     } else if (nrhs > 1) {
         // ZGEMM on the FP64 tensor cores (btg_zgemm.cu); FP64 F-hat only.
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
@@ -364,6 +370,20 @@ btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size
     const size_t cout = adjoint ? op->nm : op->nd;
     if (nrhs > 1 && op->precision == BTG_F64 && !op->no_dmma) {
         BTG_TRY(ensure_spectral(op, nrhs));
+        // int8 engine, forward: the x-hat block maxima come out of the R2C
+        const int cpb = btg::fast_r2c_cpb((int)op->nt);
+        if (op->tensor_i8 && !adjoint && nrhs <= 32 && op->fast_ok && cpb > 0 && cin % cpb == 0 &&
+            aligned16(in) && aligned16(op->wa) && !std::getenv("BTG_OZ_SCALE_PASS")) {
+            btg::R2CBlockMax bm;
+            bm.nf = (int)op->nf;
+            const size_t n = (nrhs * cin / cpb) * op->nf;
+            BTG_TRY(grow(op->oz_vexp, op->oz_vexp_cap, n));
+            bm.pexp = op->oz_vexp;
+            BTG_TRY(run_r2c_vec(op, in, nrhs * cin, op->wa, 0, &bm));
+            BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, nrhs, op->oz_vexp, cpb));
+            BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi));
+            return BTG_OK;
+        }
         BTG_TRY(run_r2c_vec(op, in, nrhs * cin, op->wa));
         BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, nrhs));
         BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi));
@@ -1461,6 +1481,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->oz_mA);
         cudaFree(op->oz_B);
         cudaFree(op->S);
+        cudaFree(op->oz_vexp);
         cudaFree(op->oz_mB);
         cudaFree(op->d_tw);
         cudaFree(op->d_post);

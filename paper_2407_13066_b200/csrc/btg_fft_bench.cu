@@ -87,7 +87,7 @@ struct Run {
         float tr = 0, tc = 0;
         for (int r = -2; r < reps; ++r) {
             cudaEventRecord(e0);
-            r2c<<<grid_r, P::TPC * CPBR, smem_r>>>(x, N, X, C, C, tabs);
+            r2c<<<grid_r, P::TPC * CPBR, smem_r>>>(x, N, X, C, C, tabs, R2CBlockMax{});
             cudaEventRecord(e1);
             c2r<<<grid_c, P::TPC * CPBC, smem_c>>>(X, C, y, N, C, tabs, epi);
             cudaEventRecord(e2);

@@ -273,13 +273,41 @@ __device__ __forceinline__ void presplit_pair(double2 xk, double2 xn, double2 w,
     zn = make_double2(inv_len * (ax + c.y), inv_len * (-ay + c.x));
 }
 
+// Optional R2C epilogue for the tcgen05 int8 multi-RHS engine (R2CBlockMax,
+// btg_kernels.cuh): the CPB lanes of a channel group reduce max |re|, |im| of X_k
+// by shuffles and one lane stores its block exponent — so the engine's separate
+// block-max pass over x-hat reduces to a max over 256 int16 per block.
+template <int CPB>
+__device__ __forceinline__ void block_max(const R2CBlockMax& bm, int c0, int b, int k, double2 x) {
+    // block exponent e + 1 of m = max |re|, |im| with m < 2^e (btg_ozaki.cu scale_exp):
+    // for normal m that is the biased exponent field - 1021; zero -> INT16_MIN
+    const double m = fmax(fabs(x.x), fabs(x.y));
+    const int E = (int)((unsigned long long)__double_as_longlong(m) >> 52);
+    int e = E - 1021;
+    if (E == 0) {
+        e = -32768;
+        if (m > 0.0) {  // subnormal
+            frexp(m, &e);
+            e += 1;
+        }
+    }
+    static_assert(CPB <= 32, "channel group wider than a warp");
+    if constexpr (CPB > 1) {
+        const int lane = threadIdx.x & 31;
+        const unsigned mask = (CPB == 32 ? 0xffffffffu : ((1u << CPB) - 1u)) << (lane & ~(CPB - 1) & 31);
+#pragma unroll
+        for (int o = 1; o < CPB; o <<= 1) e = max(e, __shfl_xor_sync(mask, e, o));
+    }
+    if (b == 0) bm.pexp[(size_t)(c0 / CPB) * bm.nf + k] = (int16_t)e;
+}
+
 // ---------------------------------------------------------------------------
 // r2c: SOTI rows (time contiguous) -> frequency-major out[k*out_fs + c]
 // ---------------------------------------------------------------------------
 template <int N, int CPB>
 __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     k_r2c_fast(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
-               int channels, FastTables tabs) {
+               int channels, FastTables tabs, R2CBlockMax bm) {
     using P = FastPlan<N>;
     using RL = typename P::R2C;
     constexpr int TPC = P::TPC, CS = chan_stride(N);
@@ -362,6 +390,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 split_pair(va[q], vb[R - 1 - q], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
                 orow[(long long)(N - k) * out_fs] = xn;
+                if (bm.pexp) {
+                    block_max<CPB>(bm, c - b, b, k, xk);
+                    block_max<CPB>(bm, c - b, b, N - k, xn);
+                }
             }
         } else {
             // butterfly 0: positions q NB pair with ((R - q) % R) NB; q = 0 gives X_0 and X_N
@@ -375,6 +407,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 split_pair(va[q], va[qp], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
                 if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                if (bm.pexp) {
+                    block_max<CPB>(bm, c - b, b, k, xk);
+                    if (q != qp || q == 0) block_max<CPB>(bm, c - b, b, N - k, xn);
+                }
             }
             // butterfly NB/2: positions NB/2 + q NB pair with index R-1-q
 #pragma unroll
@@ -387,6 +423,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 split_pair(vb[q], vb[qp], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
                 if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                if (bm.pexp) {
+                    block_max<CPB>(bm, c - b, b, k, xk);
+                    if (q != qp) block_max<CPB>(bm, c - b, b, N - k, xn);
+                }
             }
         }
     }
@@ -547,7 +587,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
 template <int N, int CPB>
 __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     k_r2c_pf(const double* __restrict__ in, long long in_cs, double2* __restrict__ out, long long out_fs,
-               int channels, FastTables tabs) {
+               int channels, FastTables tabs, R2CBlockMax bm) {
     using P = FastPlan<N>;
     using RL = typename P::R2C;
     constexpr int TPC = P::TPC, CS = chan_stride(N);
@@ -644,6 +684,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         split_pair(va[q], vb[R - 1 - q], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
                         orow[(long long)(N - k) * out_fs] = xn;
+                        if (bm.pexp) {
+                            block_max<CPB>(bm, c - b, b, k, xk);
+                            block_max<CPB>(bm, c - b, b, N - k, xn);
+                        }
                     }
                 } else {
                     // butterfly 0: positions q NB pair with ((R - q) % R) NB; q = 0 gives X_0 and X_N
@@ -657,6 +701,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         split_pair(va[q], va[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
                         if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                        if (bm.pexp) {
+                            block_max<CPB>(bm, c - b, b, k, xk);
+                            if (q != qp || q == 0) block_max<CPB>(bm, c - b, b, N - k, xn);
+                        }
                     }
                     // butterfly NB/2: positions NB/2 + q NB pair with index R-1-q
 #pragma unroll
@@ -669,6 +717,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         split_pair(vb[q], vb[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
                         if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                        if (bm.pexp) {
+                            block_max<CPB>(bm, c - b, b, k, xk);
+                            if (q != qp) block_max<CPB>(bm, c - b, b, N - k, xn);
+                        }
                     }
                 }
             }

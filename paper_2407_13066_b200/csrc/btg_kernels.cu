@@ -711,7 +711,7 @@ int persistent_grid(K kern, int threads, size_t smem, int groups) {
 
 template <int N, int CPB>
 cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
-                        const FastTables& tabs, cudaStream_t stream) {
+                        const FastTables& tabs, cudaStream_t stream, const R2CBlockMax& bm) {
     using P = fast::FastPlan<N>;
     if constexpr (P::TPC * CPB > 1024 || fast::smem_bytes<N, CPB>() > 227 * 1024) {
         return cudaErrorNotSupported;
@@ -722,7 +722,8 @@ cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long lo
         if (e != cudaSuccess) return e;
         const int groups = (channels + CPB - 1) / CPB;
         const int grid = P::PF_R2C ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
-        kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs);
+        if (bm.pexp && channels % CPB != 0) return cudaErrorInvalidValue;
+        kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_cs, out, out_fs, channels, tabs, bm);
         return cudaGetLastError();
     }
 }
@@ -747,13 +748,14 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
 
 template <int N>
 cudaError_t r2c_fast_n(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
-                       const FastTables& tabs, cudaStream_t stream) {
+                       const FastTables& tabs, cudaStream_t stream, const R2CBlockMax& bm) {
     switch (fft_cpb(fast::FastPlan<N>::CPB_R2C)) {
-        case 1: return r2c_fast_nc<N, 1>(in, in_cs, out, out_fs, channels, tabs, stream);
-        case 2: return r2c_fast_nc<N, 2>(in, in_cs, out, out_fs, channels, tabs, stream);
-        case 4: return r2c_fast_nc<N, 4>(in, in_cs, out, out_fs, channels, tabs, stream);
-        case 8: return r2c_fast_nc<N, 8>(in, in_cs, out, out_fs, channels, tabs, stream);
-        default: return r2c_fast_nc<N, fast::FastPlan<N>::CPB_R2C>(in, in_cs, out, out_fs, channels, tabs, stream);
+        case 1: return r2c_fast_nc<N, 1>(in, in_cs, out, out_fs, channels, tabs, stream, bm);
+        case 2: return r2c_fast_nc<N, 2>(in, in_cs, out, out_fs, channels, tabs, stream, bm);
+        case 4: return r2c_fast_nc<N, 4>(in, in_cs, out, out_fs, channels, tabs, stream, bm);
+        case 8: return r2c_fast_nc<N, 8>(in, in_cs, out, out_fs, channels, tabs, stream, bm);
+        default: return r2c_fast_nc<N, fast::FastPlan<N>::CPB_R2C>(in, in_cs, out, out_fs, channels, tabs, stream,
+                                                                   bm);
     }
 }
 
@@ -773,6 +775,14 @@ cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long lon
 
 }  // namespace
 
+int fast_r2c_cpb(int n) {
+#define BTG_CASE(N) \
+    if (n == N) return fft_cpb(fast::FastPlan<N>::CPB_R2C);
+    BTG_FAST_SIZES(BTG_CASE)
+#undef BTG_CASE
+    return 0;
+}
+
 bool fast_fft_supported(int n) {
 #define BTG_CASE(N) \
     if (n == N) return true;
@@ -784,10 +794,10 @@ bool fast_fft_supported(int n) {
 int fast_fft_hi_count(int n) { return (n + fast::kTwLo - 1) / fast::kTwLo + 1; }
 
 cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double2* out, long long out_fs,
-                                int channels, const FastTables& tabs, cudaStream_t stream) {
+                                int channels, const FastTables& tabs, cudaStream_t stream, const R2CBlockMax& bm) {
     if (channels <= 0) return cudaSuccess;
 #define BTG_CASE(N) \
-    if (n == N) return r2c_fast_n<N>(in, in_cs, out, out_fs, channels, tabs, stream);
+    if (n == N) return r2c_fast_n<N>(in, in_cs, out, out_fs, channels, tabs, stream, bm);
     BTG_FAST_SIZES(BTG_CASE)
 #undef BTG_CASE
     return cudaErrorNotSupported;

@@ -22,6 +22,16 @@ struct C2REpilogue {
 
 // Split twiddle tables of the compile-time-N vector FFTs (btg_fft_fast.cuh):
 // lo[i] = W_N^i (i < 32), hi[h] = W_N^{32h}; post_* the same for W_{2N}.
+// R2C epilogue of the int8 multi-RHS engine (btg_fft_fast.cuh block_max): per
+// channel group (the CTA's CPB channels) and frequency, the block exponent of
+// max |re|, |im| (scale_exp, INT16_MIN for zero) — pexp[group][k], plain stores;
+// oz_exponents_from_groups() takes the max over each 1024-channel block. The
+// exponent is monotonic in the value, so this is the exponent of the exact max.
+struct R2CBlockMax {
+    int16_t* pexp = nullptr;
+    int nf = 0;  // frequencies (row length of pexp)
+};
+
 struct FastTables {
     const double2* lo = nullptr;
     const double2* hi = nullptr;
@@ -31,12 +41,15 @@ struct FastTables {
 
 // Lengths N = N_t with a register-resident compile-time plan.
 bool fast_fft_supported(int n);
+// Channels per CTA of the fast R2C for length n (0 if no fast plan).
+int fast_r2c_cpb(int n);
 int fast_fft_hi_count(int n);  // entries of hi (post_hi has one more)
 
 // SOTI rows (16-byte aligned) -> frequency-major; returns cudaErrorNotSupported
 // when N has no compile-time plan.
 cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double2* out, long long out_fs,
-                                int channels, const FastTables& tabs, cudaStream_t stream);
+                                int channels, const FastTables& tabs, cudaStream_t stream,
+                                const R2CBlockMax& bm = R2CBlockMax{});
 cudaError_t launch_c2r_vec_fast(int n, const double2* in, long long in_fs, double* out, long long out_cs,
                                 int channels, const FastTables& tabs, const C2REpilogue& epi,
                                 cudaStream_t stream);
@@ -119,8 +132,11 @@ cudaError_t launch_naive(bool adjoint, const double* blocks, const double* in, d
 
 // Bq: workspace of oz_presliced_bytes(nf, nd) for the adjoint's pre-sliced d-hat tiles.
 size_t oz_presliced_bytes(int nf, int nd);
+// vexp: optional per-group exponents of V from the R2C epilogue (R2CBlockMax,
+// forward, nrhs <= 32; groups of vexp_cpb channels).
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
-                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream);
+                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream,
+                     const int16_t* vexp = nullptr, int vexp_cpb = 1);
 
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream);

@@ -690,12 +690,34 @@ cudaError_t oz_quantize_operator(const double2* F, int nf, int nd, int nm, int8_
     return cudaGetLastError();
 }
 
+namespace oz {
+// Block exponents from the R2C's per-group exponents (R2CBlockMax): the max over
+// the channel groups of each 1024-channel block; thread per (f, r, kb), f fastest
+// along the (coalesced) pexp rows. The R2C-fused alternative to k_scale_vec.
+__global__ void k_exponents(const int16_t* __restrict__ pexp, int* __restrict__ mB, int nf, int nrhs, int nm,
+                            int cpb) {
+    const int nkb = (nm + kChunk - 1) / kChunk;
+    const long long n = (long long)nf * nrhs * nkb;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int f = (int)(i % nf);
+        const long long rk = i / nf;
+        const int kb = (int)(rk % nkb), r = (int)(rk / nkb);
+        const long long g0 = ((long long)r * nm + (long long)kb * kChunk) / cpb;
+        const long long g1 = ((long long)r * nm + min(nm, (kb + 1) * kChunk) + cpb - 1) / cpb;
+        int e = -32768;
+        for (long long g = g0; g < g1; ++g) e = max(e, (int)pexp[g * nf + f]);
+        mB[((size_t)f * nrhs + r) * nkb + kb] = e == -32768 ? 0 : e;
+    }
+}
+}  // namespace oz
+
 size_t oz_presliced_bytes(int nf, int nd) {  // adjoint B tiles, up to 32 RHS per pass
     return (size_t)nf * ((nd + 31) / 32) * oz::BTileBytes<4>();
 }
 
 cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* mA, const double2* V, double2* Y,
-                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream) {
+                     int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream,
+                     const int16_t* vexp, int vexp_cpb) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int K = adjoint ? nd : nm;
@@ -718,7 +740,10 @@ cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* m
         const int nr = std::min(32, nrhs - r0);
         a.r0 = r0;
         a.nr = nr;
-        oz::k_scale_vec<<<sms * 8, 256, 0, stream>>>(V, mB, nf, nrhs, r0, nr, K, nkb);
+        if (vexp && nrhs <= 32 && !adjoint)  // block exponents folded into the R2C (R2CBlockMax)
+            oz::k_exponents<<<sms * 8, 256, 0, stream>>>(vexp, mB, nf, nrhs, nm, vexp_cpb);
+        else
+            oz::k_scale_vec<<<sms * 8, 256, 0, stream>>>(V, mB, nf, nrhs, r0, nr, K, nkb);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         const int ng = (nr + 7) / 8;  // N' = 16 ng columns

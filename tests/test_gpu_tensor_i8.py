@@ -80,3 +80,23 @@ def test_engine_switch_on_one_handle(btg):
         assert R.rel_l2(F_dmma[r], want) <= TOL64
         assert R.rel_l2(F_i8[r], want) <= TOL64
         assert R.rel_l2(A_i8[r], A_dmma[r]) <= TOL64
+
+
+@pytest.mark.parametrize("dims", [(130, 2048, 64, 9), (40, 1104, 256, 32), (12, 3076, 1024, 5)])
+def test_fused_block_max_matches_scale_pass(btg, dims, monkeypatch):
+    """Lengths with a fast R2C plan: the x-hat block maxima come out of the R2C
+    epilogue (R2CBlockMax) instead of a separate pass; the exponents are the same
+    exact maxima, so the results are bit-identical to the scale pass and meet the
+    FP64 bar against the oracle."""
+    nd, nm, nt, nrhs = dims
+    blocks, _, _ = R.random_problem(1200 + nt, nd, nm, nt)
+    spec = R.setup_full(blocks)
+    M = R.Mt19937_64(1300 + nt).uniform(nrhs * nm * nt, -1, 1).reshape(nrhs, nm, nt)
+    with btg.setup(blocks) as op:
+        op.set_multi_rhs_engine("tensor_i8")
+        fused = op.apply_forward(M)
+        monkeypatch.setenv("BTG_OZ_SCALE_PASS", "1")
+        separate = op.apply_forward(M)
+    assert np.array_equal(fused, separate)
+    for r in range(nrhs):
+        assert R.rel_l2(fused[r], R.apply_forward(spec, M[r])) <= TOL64
