@@ -148,6 +148,12 @@ __device__ __forceinline__ void digits_fast(double u, int (&q)[kS]) {
     q[6] = l - (q[5] << 7);
 }
 
+// Exact int32 -> FP64 on the FP64 pipe (one DADD instead of an I2F.F64): the
+// bit pattern 0x43300000:(x ^ 2^31) is 2^52 + 2^31 + x.
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+    return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
     return (uint32_t)(a & 0xFF) | ((uint32_t)(b & 0xFF) << 8) | ((uint32_t)(c & 0xFF) << 16) |
            ((uint32_t)(d & 0xFF) << 24);
@@ -477,32 +483,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
         int ck_of_drain = 0;
         auto drain = [&]() {
             const int f = (int)(tile_of_drain / mtiles), mt = (int)(tile_of_drain % mtiles);
-            umma::mbar_wait(acc_full, (uint32_t)(drained & 1));
-            umma::fence_after_sync();
             const int ck = ck_of_drain;
+            // the block exponents are global loads: issue them before the wait
             const int ebA = ADJ ? scale_exp(g.mA[(size_t)f * g.nkbA + (mt * kTileM) / kChunk])
                                 : scale_exp(g.mA[(size_t)f * g.nkbA + ck]);
             int ebB[NP / 2];
 #pragma unroll
             for (int rr = 0; rr < NP / 2; ++rr)
                 ebB[rr] = rr < g.nr ? g.mB[((size_t)f * g.nr + rr) * nkb + ck] : 0;
+            umma::mbar_wait(acc_full, (uint32_t)(drained & 1));
+            umma::fence_after_sync();
+            // 8 columns at a time: all 7 level loads in flight before one wait
 #pragma unroll
-            for (int cg = 0; cg < NP / 16; ++cg) {
-                double v[16];
+            for (int cg = 0; cg < NP / 8; ++cg) {
+                uint32_t r[kLevels][8];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = 0.0;
+                for (int L = 0; L < kLevels; ++L)
+                    umma::ld_32x32b_x8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(L * NP + cg * 8), r[L]);
+                umma::ld_wait();
+                double v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = 0.0;
 #pragma unroll
                 for (int L = 0; L < kLevels; ++L) {
-                    uint32_t r[16];
-                    umma::ld_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(L * NP + cg * 16), r);
-                    umma::ld_wait();
                     const double w = pow2(-7 * (L + 2));
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) v[q] = fma((double)(int)r[q], w, v[q]);
+                    for (int q = 0; q < 8; ++q) v[q] = fma(i32_to_f64(r[L][q]), w, v[q]);
                 }
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int col = cg * 16 + q, rr = col >> 1;
+                for (int q = 0; q < 8; ++q) {
+                    const int col = cg * 8 + q, rr = col >> 1;
                     if (rr < g.nr) acc[col] = fma(v[q], pow2(ebA + ebB[rr]), acc[col]);
                 }
             }
