@@ -377,7 +377,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
         // ===== TMA producer: F-hat slice tiles =====
         if (lane == 0) {
             const uint64_t pol = umma::policy_evict_first();
-            const uint64_t pol_b = umma::policy_evict_last();  // B tiles are reused by every row tile of f
             long long it = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 const int f = (int)(tile / mtiles), mt = (int)(tile % mtiles);
@@ -403,12 +402,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_oz_gemm(GemmArgs g) {
                             umma::bulk_load(dst + (ig - ig0) * 8 * kPos, base + ((size_t)ig * g.JG + jg0) * kPos,
                                             bytes, fullA + st, pol);
                     }
-                    if constexpr (BPRE) {
+                }
+            }
+        }
+        if constexpr (BPRE) {
+            if (lane == 1) {
+                // pre-sliced B tiles on their own thread, so a full B ring never
+                // holds back the A prefetch
+                const uint64_t pol_b = umma::policy_evict_last();  // reused by every row tile of f
+                long long it = 0;
+                for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                    const int f = (int)(tile / mtiles);
+                    for (int ks = 0; ks < nks; ++ks, ++it) {
                         const int sb = (int)(it % kBStages);
                         if (it >= kBStages) umma::mbar_wait(emptyB + sb, (uint32_t)(((it / kBStages) - 1) & 1));
                         umma::mbar_expect_tx(fullB + sb, (uint32_t)kBStage);
-                        umma::bulk_load(Bs + sb * kBStage, g.Bq + ((size_t)f * nks + ks) * kBStage, (uint32_t)kBStage,
-                                        fullB + sb, pol_b);
+                        umma::bulk_load(Bs + sb * kBStage, g.Bq + ((size_t)f * nks + ks) * kBStage,
+                                        (uint32_t)kBStage, fullB + sb, pol_b);
                     }
                 }
             }
