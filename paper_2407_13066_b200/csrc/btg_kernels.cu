@@ -443,14 +443,25 @@ __global__ void __launch_bounds__(kThreads, 2)
                     for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[u][q][v], w);
             }
         }
-        for (; i < nd; ++i) {
-            const double2 w = dsrc[i];
+        if (i < nd) {
+            // remainder rows (< UNR): one batch of predicated loads, all in flight
+            // together, then the same i-ascending accumulation
+            double2 fv[UNR][JPT][VEC];
 #pragma unroll
-            for (int q = 0; q < JPT; ++q) {
-                double2 fv[VEC];
-                FLoad<TF, VEC>::load(ff + (size_t)i * ld + jb + q * kStep, pol, fv);
+            for (int u = 0; u < UNR; ++u)
+                if (i + u < nd)
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[v], w);
+                    for (int q = 0; q < JPT; ++q)
+                        FLoad<TF, VEC>::load(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                if (i + u < nd) {
+                    const double2 w = dsrc[i + u];
+#pragma unroll
+                    for (int q = 0; q < JPT; ++q)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[u][q][v], w);
+                }
             }
         }
 #pragma unroll
