@@ -264,6 +264,30 @@ btg_status btg_conventional_cost_estimate(double grid_points, double num_steps, 
                                           double rank_fraction, btg_cost_estimate* out);
 double btg_apply_arithmetic_intensity(double local_sensors, double local_sources);
 
+/* ---- single-process partition (distributed.hpp:43-121) ------------------------
+ * partition_operator / distributed_forward / distributed_adjoint: one device
+ * handle per non-empty cell of a rows x cols grid (the ceiling partition,
+ * distributed.cpp:145-175; BTG_EGRID for grids wider than the operator), placed
+ * round-robin on `devices` (NULL: device 0). The partial data / parameter slices
+ * are summed on the host with the reference's fixed tree (tree_reduce,
+ * distributed.cpp:36-47), so `parallel` (one host thread per cell, the
+ * reference's ExecutionPolicy::Parallel) gives bit-identical results. Host SOTI
+ * vectors. backend: 0 fft, 1 ewp (needs BTG_KEEP_CHANNEL_LAYOUT), 2 naive
+ * (partitions of compact operators only, as in the reference). */
+typedef struct btg_partition_s* btg_partition;
+btg_status btg_partition_create(const double* blocks, size_t num_sensors, size_t num_sources, size_t num_steps,
+                                size_t rows, size_t cols, const int* devices, size_t num_devices, int precision,
+                                unsigned flags, btg_partition* out);      /* partition_operator(CompactP2O) */
+btg_status btg_partition_from_operator(btg_op op, size_t rows, size_t cols, const int* devices,
+                                       size_t num_devices, btg_partition* out);  /* partition_operator(SpectralP2O) */
+/* bounds[4] = sensor_begin, sensor_end, source_begin, source_end; *op NULL for an empty cell */
+btg_status btg_partition_shard(btg_partition p, size_t row, size_t col, size_t* bounds, btg_op* op);
+btg_status btg_partition_forward(btg_partition p, const double* m, size_t m_len, double* d, size_t d_len,
+                                 int backend, int parallel);
+btg_status btg_partition_adjoint(btg_partition p, const double* d, size_t d_len, double* m, size_t m_len,
+                                 int backend, int parallel);
+void btg_partition_destroy(btg_partition p);
+
 /* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */
 btg_status btg_spectrum_device(btg_op op, void** ptr, size_t* elem_bytes);
 

@@ -9,12 +9,14 @@
 //   PipelineCounters / StageCounters                    counters.hpp:12-45
 //   Regularization, RegKind, HessianOperator            inverse.hpp:16-39
 //   Error, DimensionError, OrderingError, GridError     errors.hpp:8-36
+//   Partition, partition_operator, distributed_forward/adjoint   distributed.hpp:14-121
 // A caller that compiled against the reference relinks against libbtg.so and
 // includes this header instead; F-hat then lives in HBM (SpectralP2O is a
 // move-only device handle; freq_blocks is materialized only on request).
 // Header-only: every numeric step runs in the CUDA library.
 #pragma once
 
+#include <array>
 #include <complex>
 #include <cstddef>
 #include <cstdint>
@@ -413,6 +415,108 @@ inline SpectralP2O slice(const SpectralP2O& op, std::size_t i0, std::size_t i1, 
     btg_op h = nullptr;
     detail::check(btg_slice_operator(op.handle(), i0, i1, j0, j1, device, &h));
     return SpectralP2O(h);
+}
+
+// ---- single-process partition (distributed.hpp:14-121) -----------------------
+enum class Backend { Fft, Ewp, Naive };
+inline Backend parse_backend(const std::string& name) {
+    if (name == "fft") return Backend::Fft;
+    if (name == "ewp") return Backend::Ewp;
+    if (name == "naive") return Backend::Naive;
+    throw Error("unknown backend '" + name + "' (expected fft, ewp or naive)");
+}
+enum class ExecutionPolicy { Serial, Parallel };
+struct EngineOptions {
+    Backend backend = Backend::Fft;
+    ExecutionPolicy policy = ExecutionPolicy::Serial;
+};
+
+// Partition: a grid of device handles (round-robin over `devices`, default
+// device 0), shards as in the reference (row-major, ceiling cuts).
+class Partition {
+public:
+    GridShape grid;
+    std::size_t num_sensors = 0, num_sources = 0, num_steps = 0;
+
+    Partition() = default;
+    Partition(btg_partition h, GridShape g, std::size_t nd, std::size_t nm, std::size_t nt)
+        : grid(g), num_sensors(nd), num_sources(nm), num_steps(nt), h_(h) {}
+    Partition(const Partition&) = delete;
+    Partition& operator=(const Partition&) = delete;
+    Partition(Partition&& o) noexcept { *this = std::move(o); }
+    Partition& operator=(Partition&& o) noexcept {
+        if (this != &o) {
+            if (h_) btg_partition_destroy(h_);
+            h_ = std::exchange(o.h_, nullptr);
+            grid = o.grid;
+            num_sensors = o.num_sensors;
+            num_sources = o.num_sources;
+            num_steps = o.num_steps;
+        }
+        return *this;
+    }
+    ~Partition() {
+        if (h_) btg_partition_destroy(h_);
+    }
+    btg_partition handle() const { return h_; }
+    // WorkerShard bounds (distributed.hpp:27-40): sensor_begin, sensor_end, source_begin, source_end
+    std::array<std::size_t, 4> shard_bounds(std::size_t row, std::size_t col) const {
+        std::array<std::size_t, 4> b{};
+        detail::check(btg_partition_shard(h_, row, col, b.data(), nullptr));
+        return b;
+    }
+
+private:
+    btg_partition h_ = nullptr;
+};
+
+inline Partition partition_operator(const CompactP2O& op, const GridShape& grid, const SetupOptions& options = {},
+                                    const std::vector<int>& devices = {}) {
+    op.validate();
+    btg_partition h = nullptr;
+    detail::check(btg_partition_create(op.blocks.data(), op.num_sensors, op.num_sources, op.num_steps, grid.rows,
+                                       grid.cols, devices.empty() ? nullptr : devices.data(), devices.size(),
+                                       options.precision,
+                                       options.keep_channel_layout ? BTG_KEEP_CHANNEL_LAYOUT : 0u, &h));
+    return Partition(h, grid, op.num_sensors, op.num_sources, op.num_steps);
+}
+inline Partition partition_operator(const SpectralP2O& op, const GridShape& grid, const SetupOptions& = {},
+                                    const std::vector<int>& devices = {}) {
+    op.validate();
+    btg_partition h = nullptr;
+    detail::check(btg_partition_from_operator(op.handle(), grid.rows, grid.cols,
+                                              devices.empty() ? nullptr : devices.data(), devices.size(), &h));
+    return Partition(h, grid, op.num_sensors, op.num_sources, op.num_steps);
+}
+
+namespace detail {
+inline SpaceTimeVector distributed_apply(const Partition& p, const SpaceTimeVector& x, bool adjoint,
+                                         const EngineOptions& options) {
+    x.validate();
+    x.require_ordering(Ordering::SOTI);
+    const std::size_t din = adjoint ? p.num_sensors : p.num_sources;
+    const std::size_t dout = adjoint ? p.num_sources : p.num_sensors;
+    if (x.spatial_dim != din || x.num_steps != p.num_steps)
+        throw DimensionError(std::string(adjoint ? "distributed_adjoint" : "distributed_forward") +
+                             ": vector does not match the partition");
+    SpaceTimeVector out = SpaceTimeVector::zeros(dout, p.num_steps, Ordering::SOTI);
+    const int backend = static_cast<int>(options.backend);
+    const int parallel = options.policy == ExecutionPolicy::Parallel ? 1 : 0;
+    detail::check(adjoint ? btg_partition_adjoint(p.handle(), x.values.data(), x.values.size(), out.values.data(),
+                                                  out.values.size(), backend, parallel)
+                          : btg_partition_forward(p.handle(), x.values.data(), x.values.size(), out.values.data(),
+                                                  out.values.size(), backend, parallel));
+    return out;
+}
+}  // namespace detail
+
+inline SpaceTimeVector distributed_forward(const Partition& partition, const SpaceTimeVector& m,
+                                           const EngineOptions& options = {}) {
+    return detail::distributed_apply(partition, m, false, options);
+}
+inline SpaceTimeVector distributed_adjoint(const Partition& partition, const SpaceTimeVector& d,
+                                           const EngineOptions& options = {}) {
+    return detail::distributed_apply(partition, d, true, options);
 }
 
 }  // namespace btoep

@@ -14,6 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
 BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER, BTG_EFORMAT = range(9)
 BTG_F64, BTG_F32 = 64, 32
 BTG_DEVICE_PTRS = 0x1
+BTG_KEEP_CHANNEL_LAYOUT = 0x2
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's stream 0)
 BTG_REG_IDENTITY, BTG_REG_TEMPORAL_LAPLACIAN = 0, 1
 BTG_GAMMA_NONE, BTG_GAMMA_PER_SENSOR, BTG_GAMMA_PER_SAMPLE = 0, 1, 2
@@ -37,6 +38,12 @@ EXPORTED = (
     "btg_forward_ewp",
     "btg_naive_forward",
     "btg_write_compact",
+    "btg_partition_create",
+    "btg_partition_from_operator",
+    "btg_partition_shard",
+    "btg_partition_forward",
+    "btg_partition_adjoint",
+    "btg_partition_destroy",
     "btg_read_compact",
     "btg_conventional_cost_estimate",
     "btg_apply_arithmetic_intensity",
@@ -189,6 +196,14 @@ def load():
     L.btg_conventional_cost_estimate.argtypes = [ctypes.c_double] * 4 + [ctypes.POINTER(ctypes.c_double * 7)]
     L.btg_apply_arithmetic_intensity.argtypes = [ctypes.c_double, ctypes.c_double]
     L.btg_apply_arithmetic_intensity.restype = ctypes.c_double
+    L.btg_partition_create.argtypes = [_dp, _sz, _sz, _sz, _sz, _sz, ctypes.POINTER(ctypes.c_int), _sz,
+                                       ctypes.c_int, ctypes.c_uint, ctypes.POINTER(_vp)]
+    L.btg_partition_from_operator.argtypes = [_vp, _sz, _sz, ctypes.POINTER(ctypes.c_int), _sz, ctypes.POINTER(_vp)]
+    L.btg_partition_shard.argtypes = [_vp, _sz, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_vp)]
+    for name in ("btg_partition_forward", "btg_partition_adjoint"):
+        getattr(L, name).argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_int, ctypes.c_int]
+    L.btg_partition_destroy.argtypes = [_vp]
+    L.btg_partition_destroy.restype = None
     L.btg_write_compact.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, _sz]
     L.btg_read_compact.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_sz),
                                    ctypes.POINTER(_sz)]
@@ -230,7 +245,8 @@ def load():
     L.btg_comm_cost.argtypes = [_sz, _sz, _sz, _sz, _sz, ctypes.c_double, ctypes.c_double,
                                 ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTED:
-        if name not in ("btg_last_error", "btg_abi_version", "btg_destroy", "btg_apply_arithmetic_intensity"):
+        if name not in ("btg_last_error", "btg_abi_version", "btg_destroy", "btg_apply_arithmetic_intensity",
+                        "btg_partition_destroy"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

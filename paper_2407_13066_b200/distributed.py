@@ -29,8 +29,8 @@ from typing import List, Optional, Tuple
 
 from ._lib import GridError
 
-__all__ = ["Shard", "CommEvent", "partition_bounds", "GridEngine", "synthetic_shard_operator", "distributed_forward",
-           "distributed_adjoint"]
+__all__ = ["Shard", "CommEvent", "partition_bounds", "GridEngine", "synthetic_shard_operator", "Partition",
+           "partition_operator", "distributed_forward", "distributed_adjoint"]
 
 
 @dataclass(frozen=True)
@@ -335,83 +335,132 @@ class GridEngine:
 
 
 # ---------------------------------------------------------------------------
-# Single-process logical grid: the reference module's distributed_forward /
-# distributed_adjoint (python/src/bindings.cpp:148-172 over distributed.cpp:
-# 312-392). Every grid cell's shard is set up as its own device operator —
-# spread round-robin over the visible GPUs — and the partial results are summed
-# with the reference's fixed binary tree (tree_reduce, distributed.cpp:36-47),
-# on the host, in the same order.
+# Single-process partition over the visible GPUs: the reference's Partition /
+# distributed_forward / distributed_adjoint (distributed.hpp:43-121) and the
+# module functions of the same names (python/src/bindings.cpp:148-172), over
+# libbtg's btg_partition_* (one device handle per grid cell, placed round-robin
+# on the device list; partial slices summed with the reference's fixed tree).
 # ---------------------------------------------------------------------------
-def _tree_reduce(partials):
-    """((v0 + v1) + (v2 + v3)) + ...: tree_reduce (distributed.cpp:36-47)."""
-    parts = [p.copy() for p in partials]
-    step = 1
-    while step < len(parts):
-        for i in range(0, len(parts) - step, 2 * step):
-            parts[i] += parts[i + step]
-        step *= 2
-    return parts[0]
+_BACKENDS = {"fft": 0, "ewp": 1, "naive": 2}
 
 
-def _grid_apply(blocks, x, grid: str, backend: str, adjoint: bool, devices=None):
-    import numpy as np
+def _parse_backend(name: str) -> int:
+    """parse_backend (distributed.cpp): "fft" | "ewp" | "naive"."""
+    from ._lib import Error
 
-    from ._lib import DimensionError, Error
-    from .operator import naive_apply_adjoint, naive_apply_forward, setup
-    from .planner import parse_grid
+    if name not in _BACKENDS:
+        raise Error(f"unknown backend '{name}' (expected fft, ewp or naive)")
+    return _BACKENDS[name]
 
-    if backend not in ("fft", "ewp", "naive"):
-        raise Error(f"unknown backend '{backend}' (expected fft, ewp or naive)")  # parse_backend
-    blocks = np.ascontiguousarray(blocks, dtype=np.float64)
-    if blocks.ndim != 3:
-        raise DimensionError("blocks must be (steps, sensors, sources)")
-    nt, nd, nm = blocks.shape
-    x = np.ascontiguousarray(x, dtype=np.float64)
-    din, dout = (nd, nm) if adjoint else (nm, nd)
-    if x.shape != (din, nt):
-        raise DimensionError(f"distributed_{'adjoint' if adjoint else 'forward'}: vector is {x.shape}, "
-                             f"expected ({din}, {nt})")
-    rows, cols = parse_grid(grid)
-    shards = partition_bounds(nd, nm, rows, cols)
-    if devices is None:
-        import torch
 
-        devices = list(range(max(1, torch.cuda.device_count())))
-    out = np.zeros((dout, nt))
-    # F: row i sums its cells' partial d over j; F*: column j sums over i
-    groups = ([[s for s in shards if s.grid_row == i] for i in range(rows)] if not adjoint
-              else [[s for s in shards if s.grid_col == j] for j in range(cols)])
-    for cells in groups:
-        partials = []
-        for s in cells:
-            n_out = s.local_sources if adjoint else s.local_sensors
-            if s.empty:
-                partials.append(np.zeros((n_out, nt)))
-                continue
-            dev = devices[(s.grid_row * cols + s.grid_col) % len(devices)]
-            local = blocks[:, s.sensor_begin:s.sensor_end, s.source_begin:s.source_end]
-            if backend == "naive":
-                xs = x[s.sensor_begin:s.sensor_end] if adjoint else x[s.source_begin:s.source_end]
-                partials.append(naive_apply_adjoint(local, xs, dev) if adjoint else naive_apply_forward(local, xs, dev))
-                continue
-            with setup(local, keep_channel_layout=backend == "ewp", device=dev) as op:
-                xs = x[s.sensor_begin:s.sensor_end] if adjoint else x[s.source_begin:s.source_end]
-                if backend == "ewp":
-                    partials.append(op.apply_adjoint_ewp(xs) if adjoint else op.apply_forward_ewp(xs))
-                else:
-                    partials.append(op.apply_adjoint(xs) if adjoint else op.apply_forward(xs))
-        s0 = cells[0]
-        lo, hi = (s0.source_begin, s0.source_end) if adjoint else (s0.sensor_begin, s0.sensor_end)
-        if hi > lo:
-            out[lo:hi] = _tree_reduce(partials)
-    return out
+class Partition:
+    """partition_operator(CompactP2O | SpectralP2O, GridShape) (distributed.cpp:179-218)."""
+
+    def __init__(self, source, grid, keep_channel_layout: bool = False, precision: int = 64, devices=None):
+        import ctypes
+
+        import numpy as np
+
+        from . import _lib
+        from .operator import SpectralOperator
+        from .planner import parse_grid
+
+        rows, cols = parse_grid(grid) if isinstance(grid, str) else (int(grid[0]), int(grid[1]))
+        if devices is None:
+            import torch
+
+            devices = list(range(max(1, torch.cuda.device_count())))
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        L = _lib.load()
+        if isinstance(source, SpectralOperator):
+            _lib.check(L.btg_partition_from_operator(source._h, rows, cols, devs, len(devices), ctypes.byref(h)))
+            self.num_sensors, self.num_sources, self.num_steps = (source.num_sensors, source.num_sources,
+                                                                  source.num_steps)
+        else:
+            b = np.ascontiguousarray(source, dtype=np.float64)
+            if b.ndim != 3:
+                raise _lib.DimensionError("blocks must be (steps, sensors, sources)")
+            nt, nd, nm = b.shape
+            flags = _lib.BTG_KEEP_CHANNEL_LAYOUT if keep_channel_layout else 0
+            _lib.check(L.btg_partition_create(b.ctypes.data, nd, nm, nt, rows, cols, devs, len(devices),
+                                              int(precision), flags, ctypes.byref(h)))
+            self.num_sensors, self.num_sources, self.num_steps = nd, nm, nt
+        self._h = h
+        self.rows, self.cols = rows, cols
+
+    def bounds(self):
+        """(sensor_begin, sensor_end, source_begin, source_end) per shard, row-major."""
+        import ctypes
+
+        from . import _lib
+
+        out = []
+        for i in range(self.rows):
+            for j in range(self.cols):
+                b = (ctypes.c_size_t * 4)()
+                _lib.check(_lib.load().btg_partition_shard(self._h, i, j, b, None))
+                out.append(tuple(int(x) for x in b))
+        return out
+
+    def _apply(self, x, adjoint: bool, backend: str, parallel: bool):
+        import numpy as np
+
+        from . import _lib
+
+        din, dout = (self.num_sensors, self.num_sources) if adjoint else (self.num_sources, self.num_sensors)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (din, self.num_steps):
+            raise _lib.DimensionError(f"distributed_{'adjoint' if adjoint else 'forward'}: vector is {x.shape}, "
+                                      f"expected ({din}, {self.num_steps})")
+        out = np.empty((dout, self.num_steps))
+        fn = _lib.load().btg_partition_adjoint if adjoint else _lib.load().btg_partition_forward
+        _lib.check(fn(self._h, x.ctypes.data, x.size, out.ctypes.data, out.size, _parse_backend(backend),
+                      int(bool(parallel))))
+        return out
+
+    def forward(self, m, backend: str = "fft", parallel: bool = False):
+        """distributed_forward (distributed.cpp:312-351)."""
+        return self._apply(m, False, backend, parallel)
+
+    def adjoint(self, d, backend: str = "fft", parallel: bool = False):
+        """distributed_adjoint (distributed.cpp:353-392)."""
+        return self._apply(d, True, backend, parallel)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            from . import _lib
+
+            _lib.load().btg_partition_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def partition_operator(source, grid, keep_channel_layout: bool = False, precision: int = 64, devices=None):
+    """partition_operator (distributed.hpp:57-66)."""
+    return Partition(source, grid, keep_channel_layout, precision, devices)
 
 
 def distributed_forward(blocks, m, grid: str = "1x1", backend: str = "fft", devices=None):
     """The reference module's distributed_forward(blocks, m, grid, backend)."""
-    return _grid_apply(blocks, m, grid, backend, adjoint=False, devices=devices)
+    _parse_backend(backend)
+    with Partition(blocks, grid, keep_channel_layout=backend == "ewp", devices=devices) as p:
+        return p.forward(m, backend)
 
 
 def distributed_adjoint(blocks, d, grid: str = "1x1", backend: str = "fft", devices=None):
     """The reference module's distributed_adjoint(blocks, d, grid, backend)."""
-    return _grid_apply(blocks, d, grid, backend, adjoint=True, devices=devices)
+    _parse_backend(backend)
+    with Partition(blocks, grid, keep_channel_layout=backend == "ewp", devices=devices) as p:
+        return p.adjoint(d, backend)

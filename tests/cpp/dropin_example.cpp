@@ -111,6 +111,21 @@ int main() {
         CHECK(std::abs(d2.at(1, t)) < 1e-12);
     }
 
+    // single-process partition (distributed.hpp): 2 x 1 grid of the shift operator
+    {
+        GridShape g2;
+        g2.rows = 2;
+        Partition pp = partition_operator(sh, g2);
+        SpaceTimeVector dp = distributed_forward(pp, v);
+        for (std::size_t k = 0; k < dp.values.size(); ++k) CHECK(std::abs(dp.values[k] - dv.values[k]) < 1e-12);
+        EngineOptions par;
+        par.policy = ExecutionPolicy::Parallel;
+        SpaceTimeVector ap = distributed_adjoint(pp, dv, par);
+        SpaceTimeVector af2 = apply_adjoint(sop, dv);
+        for (std::size_t k = 0; k < ap.values.size(); ++k) CHECK(std::abs(ap.values[k] - af2.values[k]) < 1e-12);
+        CHECK(pp.shard_bounds(1, 0)[0] == 1);
+    }
+
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
