@@ -298,6 +298,22 @@ inline SpaceTimeVector apply_adjoint_ewp(const SpectralP2O& op, const SpaceTimeV
     return detail::apply_ewp(op, d, true);
 }
 
+// ---- distributed engine options (distributed.hpp:14-21,104-107) -----------------
+enum class Backend { Fft, Ewp, Naive };
+inline Backend parse_backend(const std::string& name) {
+    if (name == "fft") return Backend::Fft;
+    if (name == "ewp") return Backend::Ewp;
+    if (name == "naive") return Backend::Naive;
+    throw Error("unknown backend '" + name + "' (expected fft, ewp or naive)");
+}
+enum class ExecutionPolicy { Serial, Parallel };
+struct EngineOptions {
+    Backend backend = Backend::Fft;
+    ExecutionPolicy policy = ExecutionPolicy::Serial;
+};
+
+class Partition;
+
 enum class RegKind { ScaledIdentity, TemporalLaplacian };
 struct Regularization {
     RegKind kind = RegKind::ScaledIdentity;
@@ -311,22 +327,10 @@ struct HessianOperator {
     Regularization reg;
     std::vector<double> gamma_inv;
 
-    SpaceTimeVector apply(const SpaceTimeVector& v) const {
-        if (!op) throw Error("hessian: no operator attached");
-        detail::check_apply_input(*op, v, op->num_sources, "hessian");
-        int gk = BTG_GAMMA_NONE;
-        if (gamma_inv.size() == op->num_sensors) gk = BTG_GAMMA_PER_SENSOR;
-        else if (gamma_inv.size() == op->num_sensors * op->num_steps) gk = BTG_GAMMA_PER_SAMPLE;
-        else if (!gamma_inv.empty()) throw DimensionError("hessian: gamma_inv has the wrong length");
-        SpaceTimeVector out = SpaceTimeVector::zeros(v.spatial_dim, v.num_steps, Ordering::SOTI);
-        detail::check(btg_hessian(op->handle(), v.values.data(), v.values.size(), out.values.data(),
-                                  out.values.size(), 1, gamma_inv.empty() ? nullptr : gamma_inv.data(), gk,
-                                  reg.alpha,
-                                  reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN
-                                                                         : BTG_REG_IDENTITY,
-                                  0u));
-        return out;
-    }
+    const Partition* partition = nullptr;  // set: F and F* run on the partition (inverse.cpp:80-85)
+    EngineOptions engine;
+
+    SpaceTimeVector apply(const SpaceTimeVector& v) const;
 };
 
 // btoep::CGResult / cg_solve (inverse.hpp:44-53): the whole iteration runs in HBM.
@@ -418,19 +422,6 @@ inline SpectralP2O slice(const SpectralP2O& op, std::size_t i0, std::size_t i1, 
 }
 
 // ---- single-process partition (distributed.hpp:14-121) -----------------------
-enum class Backend { Fft, Ewp, Naive };
-inline Backend parse_backend(const std::string& name) {
-    if (name == "fft") return Backend::Fft;
-    if (name == "ewp") return Backend::Ewp;
-    if (name == "naive") return Backend::Naive;
-    throw Error("unknown backend '" + name + "' (expected fft, ewp or naive)");
-}
-enum class ExecutionPolicy { Serial, Parallel };
-struct EngineOptions {
-    Backend backend = Backend::Fft;
-    ExecutionPolicy policy = ExecutionPolicy::Serial;
-};
-
 // Partition: a grid of device handles (round-robin over `devices`, default
 // device 0), shards as in the reference (row-major, ceiling cuts).
 class Partition {
@@ -517,6 +508,52 @@ inline SpaceTimeVector distributed_forward(const Partition& partition, const Spa
 inline SpaceTimeVector distributed_adjoint(const Partition& partition, const SpaceTimeVector& d,
                                            const EngineOptions& options = {}) {
     return detail::distributed_apply(partition, d, true, options);
+}
+
+// HessianOperator::apply (inverse.cpp:78-91): on the partition when one is set
+// (distributed_forward, Gamma^-1, distributed_adjoint, + alpha R v on the host),
+// else the fused single-device btg_hessian.
+inline SpaceTimeVector HessianOperator::apply(const SpaceTimeVector& v) const {
+    if (!op) throw Error("hessian: no operator attached");
+    if (!partition) {
+        detail::check_apply_input(*op, v, op->num_sources, "hessian");
+        int gk = BTG_GAMMA_NONE;
+        if (gamma_inv.size() == op->num_sensors) gk = BTG_GAMMA_PER_SENSOR;
+        else if (gamma_inv.size() == op->num_sensors * op->num_steps) gk = BTG_GAMMA_PER_SAMPLE;
+        else if (!gamma_inv.empty()) throw DimensionError("hessian: gamma_inv has the wrong length");
+        SpaceTimeVector out = SpaceTimeVector::zeros(v.spatial_dim, v.num_steps, Ordering::SOTI);
+        detail::check(btg_hessian(op->handle(), v.values.data(), v.values.size(), out.values.data(),
+                                  out.values.size(), 1, gamma_inv.empty() ? nullptr : gamma_inv.data(), gk,
+                                  reg.alpha,
+                                  reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN
+                                                                         : BTG_REG_IDENTITY,
+                                  0u));
+        return out;
+    }
+    SpaceTimeVector d = distributed_forward(*partition, v, engine);
+    if (!gamma_inv.empty()) {
+        const std::size_t nd = d.spatial_dim, nt = d.num_steps;
+        if (gamma_inv.size() != nd && gamma_inv.size() != nd * nt)
+            throw DimensionError("hessian: gamma_inv has the wrong length");
+        for (std::size_t i = 0; i < nd; ++i)
+            for (std::size_t t = 0; t < nt; ++t)
+                d.values[i * nt + t] *= gamma_inv.size() == nd ? gamma_inv[i] : gamma_inv[i * nt + t];
+    }
+    SpaceTimeVector out = distributed_adjoint(*partition, d, engine);
+    if (reg.alpha != 0.0) {  // Regularization::apply (inverse.cpp:32-49)
+        const std::size_t nt = v.num_steps;
+        for (std::size_t s = 0; s < v.spatial_dim; ++s) {
+            const double* x = v.values.data() + s * nt;
+            double* y = out.values.data() + s * nt;
+            for (std::size_t t = 0; t < nt; ++t) {
+                double r = x[t];
+                if (reg.kind == RegKind::TemporalLaplacian)
+                    r = 2.0 * x[t] - (t > 0 ? x[t - 1] : 0.0) - (t + 1 < nt ? x[t + 1] : 0.0);
+                y[t] += reg.alpha * r;
+            }
+        }
+    }
+    return out;
 }
 
 }  // namespace btoep

@@ -124,6 +124,12 @@ int main() {
         SpaceTimeVector af2 = apply_adjoint(sop, dv);
         for (std::size_t k = 0; k < ap.values.size(); ++k) CHECK(std::abs(ap.values[k] - af2.values[k]) < 1e-12);
         CHECK(pp.shard_bounds(1, 0)[0] == 1);
+        // HessianOperator on the partition (inverse.cpp:80-85) equals the fused device Hessian
+        HessianOperator hp{&sop, {RegKind::TemporalLaplacian, 0.3}};
+        HessianOperator hd = hp;
+        hp.partition = &pp;
+        SpaceTimeVector x1 = hp.apply(v), x2 = hd.apply(v);
+        for (std::size_t k = 0; k < x1.values.size(); ++k) CHECK(std::abs(x1.values[k] - x2.values[k]) < 1e-12);
     }
 
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
