@@ -415,6 +415,25 @@ def run_ours(args):
                     "per_unit": "8 FLOP per complex MAC x (N_t+1) x N_d x N_m x nrhs"}
         roof.update({"bytes_per_launch": gemv_bytes, "flops_per_launch": fl["gemv"], "ms_per_launch": dur,
                      "stage_ms": kernels, "probe": probe})
+        # per-phase HBM rates (north star: FFT and GEMV phases against the peak);
+        # algorithmic bytes of SURVEY §8d: R2C 8 C N_t + 16 NF C, C2R the mirror
+        nf_ = nt + 1
+
+        def fft_bytes(ch):
+            return 8.0 * ch * nt + 16.0 * nf_ * ch
+
+        phases = {}
+        for name, key, ch in (("fwd", "forward_fft", nm * nrhs), ("fwd", "inverse_fft", nd * nrhs),
+                              ("adj", "forward_fft", nd * nrhs), ("adj", "inverse_fft", nm * nrhs)):
+            ms_ = kernels[name][key]
+            if ms_ > 0:
+                phases[f"{name}.{key}"] = {"ms": ms_, "GB/s": fft_bytes(ch) / (ms_ * 1e-3) / 1e9,
+                                           "frac": fft_bytes(ch) / (ms_ * 1e-3) / 1e9 / peak}
+        for name in ("fwd", "adj"):
+            ms_ = kernels[name]["apply"]
+            phases[f"{name}.apply"] = {"ms": ms_, "GB/s": gemv_bytes / (ms_ * 1e-3) / 1e9,
+                                       "frac": gemv_bytes / (ms_ * 1e-3) / 1e9 / peak}
+        roof["phases"] = phases
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
             try:
