@@ -480,9 +480,51 @@ inline Partition partition_operator(const SpectralP2O& op, const GridShape& grid
     return Partition(h, grid, op.num_sensors, op.num_sources, op.num_steps);
 }
 
+// CommLog (distributed.hpp:77-92): the collectives the partition's data flow
+// implies, with the reference's byte model (record_collective, distributed.cpp:23-34).
+struct CommEvent {
+    std::string phase;  // "broadcast" | "reduce"
+    std::size_t participants = 0;
+    std::size_t messages = 0;
+    std::uint64_t link_bytes = 0;
+    std::uint64_t total_bytes = 0;
+    std::size_t tree_depth = 0;
+};
+struct CommLog {
+    std::string mode = "tree";
+    std::vector<CommEvent> events;
+    std::uint64_t total_bytes() const {
+        std::uint64_t s = 0;
+        for (const auto& e : events) s += e.total_bytes;
+        return s;
+    }
+    std::size_t total_messages() const {
+        std::size_t s = 0;
+        for (const auto& e : events) s += e.messages;
+        return s;
+    }
+};
+
 namespace detail {
+inline void record_collective(CommLog* log, const char* phase, std::size_t participants, std::uint64_t link_bytes) {
+    if (!log) return;
+    CommEvent e;
+    e.phase = phase;
+    e.participants = participants;
+    e.messages = participants == 0 ? 0 : participants - 1;
+    e.link_bytes = link_bytes;
+    e.total_bytes = static_cast<std::uint64_t>(e.messages) * link_bytes;
+    std::size_t depth = 0, reach = 1;
+    while (reach < participants) {
+        reach *= 2;
+        ++depth;
+    }
+    e.tree_depth = depth;
+    log->events.push_back(std::move(e));
+}
+
 inline SpaceTimeVector distributed_apply(const Partition& p, const SpaceTimeVector& x, bool adjoint,
-                                         const EngineOptions& options) {
+                                         const EngineOptions& options, CommLog* log) {
     x.validate();
     x.require_ordering(Ordering::SOTI);
     const std::size_t din = adjoint ? p.num_sensors : p.num_sources;
@@ -490,6 +532,14 @@ inline SpaceTimeVector distributed_apply(const Partition& p, const SpaceTimeVect
     if (x.spatial_dim != din || x.num_steps != p.num_steps)
         throw DimensionError(std::string(adjoint ? "distributed_adjoint" : "distributed_forward") +
                              ": vector does not match the partition");
+    // F: column broadcasts of the parameter slices, row reduces of the data slices
+    // (distributed.cpp:320-349); F*: row broadcasts, column reduces (:360-390)
+    const std::size_t nb = adjoint ? p.grid.rows : p.grid.cols, nr = adjoint ? p.grid.cols : p.grid.rows;
+    for (std::size_t k = 0; k < nb; ++k) {
+        const auto b = adjoint ? p.shard_bounds(k, 0) : p.shard_bounds(0, k);
+        const std::size_t dim = adjoint ? b[1] - b[0] : b[3] - b[2];
+        record_collective(log, "broadcast", adjoint ? p.grid.cols : p.grid.rows, 8ull * p.num_steps * dim);
+    }
     SpaceTimeVector out = SpaceTimeVector::zeros(dout, p.num_steps, Ordering::SOTI);
     const int backend = static_cast<int>(options.backend);
     const int parallel = options.policy == ExecutionPolicy::Parallel ? 1 : 0;
@@ -497,17 +547,22 @@ inline SpaceTimeVector distributed_apply(const Partition& p, const SpaceTimeVect
                                                   out.values.size(), backend, parallel)
                           : btg_partition_forward(p.handle(), x.values.data(), x.values.size(), out.values.data(),
                                                   out.values.size(), backend, parallel));
+    for (std::size_t k = 0; k < nr; ++k) {
+        const auto b = adjoint ? p.shard_bounds(0, k) : p.shard_bounds(k, 0);
+        const std::size_t dim = adjoint ? b[3] - b[2] : b[1] - b[0];
+        record_collective(log, "reduce", adjoint ? p.grid.rows : p.grid.cols, 8ull * p.num_steps * dim);
+    }
     return out;
 }
 }  // namespace detail
 
 inline SpaceTimeVector distributed_forward(const Partition& partition, const SpaceTimeVector& m,
-                                           const EngineOptions& options = {}) {
-    return detail::distributed_apply(partition, m, false, options);
+                                           const EngineOptions& options = {}, CommLog* log = nullptr) {
+    return detail::distributed_apply(partition, m, false, options, log);
 }
 inline SpaceTimeVector distributed_adjoint(const Partition& partition, const SpaceTimeVector& d,
-                                           const EngineOptions& options = {}) {
-    return detail::distributed_apply(partition, d, true, options);
+                                           const EngineOptions& options = {}, CommLog* log = nullptr) {
+    return detail::distributed_apply(partition, d, true, options, log);
 }
 
 // HessianOperator::apply (inverse.cpp:78-91): on the partition when one is set

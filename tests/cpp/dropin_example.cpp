@@ -131,6 +131,36 @@ int main() {
         SpaceTimeVector x1 = hp.apply(v), x2 = hd.apply(v);
         for (std::size_t k = 0; k < x1.values.size(); ++k) CHECK(std::abs(x1.values[k] - x2.values[k]) < 1e-12);
     }
+    // CommLog byte model (test_distributed.cpp:139-186)
+    {
+        const std::size_t steps = 16;
+        auto rnd_op = [&](std::size_t nd_, std::size_t nm_) {
+            CompactP2O c = CompactP2O::zeros(nd_, nm_, steps);
+            for (std::size_t k = 0; k < c.blocks.size(); ++k) c.blocks[k] = std::sin(0.7 * k);
+            return c;
+        };
+        CommLog l1;
+        Partition p11 = partition_operator(rnd_op(3, 4), GridShape{1, 1});
+        distributed_forward(p11, SpaceTimeVector::zeros(4, steps, Ordering::SOTI), {}, &l1);
+        CHECK(l1.total_bytes() == 0 && l1.total_messages() == 0);
+        CommLog l2;
+        Partition p14 = partition_operator(rnd_op(3, 8), GridShape{1, 4});
+        distributed_forward(p14, SpaceTimeVector::zeros(8, steps, Ordering::SOTI), {}, &l2);
+        std::uint64_t rb = 0;
+        std::size_t rm = 0;
+        for (const CommEvent& e : l2.events) {
+            if (e.phase == "broadcast") CHECK(e.total_bytes == 0);
+            if (e.phase != "reduce") continue;
+            CHECK(e.link_bytes == 8 * steps * 3);
+            rb += e.total_bytes;
+            rm += e.messages;
+        }
+        CHECK(rm == 3 && rb == 3 * 8 * steps * 3);
+        CommLog l3;
+        Partition p22 = partition_operator(rnd_op(4, 6), GridShape{2, 2});
+        distributed_forward(p22, SpaceTimeVector::zeros(6, steps, Ordering::SOTI), {}, &l3);
+        CHECK(l3.total_bytes() == 2 * 1 * 8 * steps * 3 + 2 * 1 * 8 * steps * 2);
+    }
 
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
