@@ -43,6 +43,14 @@ struct FLoad;
 
 template <>
 struct FLoad<double2, 1> {
+    // raw (unconverted) register form of one load, converted at the FMA
+    using Raw = double2;
+    __device__ __forceinline__ static void load_raw(const double2* p, uint64_t pol, Raw& r) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+            : "=d"(r.x), "=d"(r.y)
+            : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double2 get(const Raw& r, int) { return r; }
     __device__ __forceinline__ static void load(const double2* p, uint64_t pol, double2* out) {
         double2 r;
         asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
@@ -55,6 +63,13 @@ struct FLoad<double2, 1> {
 
 template <>
 struct FLoad<float2, 1> {
+    using Raw = float2;
+    __device__ __forceinline__ static void load_raw(const float2* p, uint64_t pol, Raw& r) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+            : "=f"(r.x), "=f"(r.y)
+            : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double2 get(const Raw& r, int) { return make_double2(r.x, r.y); }
     __device__ __forceinline__ static void load(const float2* p, uint64_t pol, double2* out) {
         float x, y;
         asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
@@ -70,6 +85,15 @@ struct FLoad<float2, 1> {
 
 template <>
 struct FLoad<float2, 2> {
+    using Raw = float4;
+    __device__ __forceinline__ static void load_raw(const float2* p, uint64_t pol, Raw& r) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+            : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double2 get(const Raw& r, int v) {
+        return v == 0 ? make_double2(r.x, r.y) : make_double2(r.z, r.w);
+    }
     __device__ __forceinline__ static void load(const float2* p, uint64_t pol, double2* out) {
         float a, b, c, d;
         asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
@@ -251,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     int j = threadIdx.x * VEC;
     for (; j + (UNR - 1) * kStep + VEC <= nm; j += UNR * kStep) {
         double2 xv[UNR][VEC];
-        double2 fv[UNR][ROWS][VEC];
+        typename FLoad<TF, VEC>::Raw fv[UNR][ROWS];  // unconverted: FP32 stays 4 B / value in registers
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -261,10 +285,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
                 if (r < nr) {
-                    FLoad<TF, VEC>::load(fb + (size_t)r * ld + j + u * kStep, pol, fv[u][r]);
+                    FLoad<TF, VEC>::load_raw(fb + (size_t)r * ld + j + u * kStep, pol, fv[u][r]);
                 } else {
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) fv[u][r][v] = make_double2(0.0, 0.0);
+                    fv[u][r] = {};
                 }
             }
 #pragma unroll
@@ -272,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], fv[u][r][v], xv[u][v]);
+                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], FLoad<TF, VEC>::get(fv[u][r], v), xv[u][v]);
     }
     for (; j < nm; j += kStep) {
 #pragma unroll
@@ -428,31 +451,31 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (jb + (JPT - 1) * kStep + VEC <= nm) {
         int i = 0;
         for (; i + UNR <= nd; i += UNR) {
-            double2 fv[UNR][JPT][VEC];
+            typename FLoad<TF, VEC>::Raw fv[UNR][JPT];
 #pragma unroll
             for (int u = 0; u < UNR; ++u)
 #pragma unroll
                 for (int q = 0; q < JPT; ++q)
-                    FLoad<TF, VEC>::load(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
+                    FLoad<TF, VEC>::load_raw(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const double2 w = dsrc[i + u];
 #pragma unroll
                 for (int q = 0; q < JPT; ++q)
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[u][q][v], w);
+                    for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], FLoad<TF, VEC>::get(fv[u][q], v), w);
             }
         }
         if (i < nd) {
             // remainder rows (< UNR): one batch of predicated loads, all in flight
             // together, then the same i-ascending accumulation
-            double2 fv[UNR][JPT][VEC];
+            typename FLoad<TF, VEC>::Raw fv[UNR][JPT];
 #pragma unroll
             for (int u = 0; u < UNR; ++u)
                 if (i + u < nd)
 #pragma unroll
                     for (int q = 0; q < JPT; ++q)
-                        FLoad<TF, VEC>::load(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
+                        FLoad<TF, VEC>::load_raw(ff + (size_t)(i + u) * ld + jb + q * kStep, pol, fv[u][q]);
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 if (i + u < nd) {
@@ -460,7 +483,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int q = 0; q < JPT; ++q)
 #pragma unroll
-                        for (int v = 0; v < VEC; ++v) cmac_conj(ar[q][v], ai[q][v], fv[u][q][v], w);
+                        for (int v = 0; v < VEC; ++v)
+                            cmac_conj(ar[q][v], ai[q][v], FLoad<TF, VEC>::get(fv[u][q], v), w);
                 }
             }
         }
@@ -611,7 +635,10 @@ cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int
         dim3 grid((nd + kRows - 1) / kRows, nb);
         if constexpr (sizeof(TF) == 8) {
             if ((nm & 1) == 0 && (j0 & 1) == 0) {
-                k_gemv_fwd<TF, 2, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+                // FP32 pairs: 16-byte loads of two complex, 4 rows x 2 unrolled steps per
+                // thread (8 rows x 2 spills; measured 3.99 vs 9.98 ms at configs[1])
+                dim3 g4((nd + 3) / 4, nb);
+                k_gemv_fwd<TF, 2, 4, 2><<<g4, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
                 continue;
             }
         }
