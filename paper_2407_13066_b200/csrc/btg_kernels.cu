@@ -372,12 +372,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     constexpr int kStep = 32 * VEC;
     int j = lane * VEC;
     for (; j + (UNR - 1) * kStep + VEC <= nm; j += UNR * kStep) {
-        double2 fv[UNR][RPW][VEC], xv[UNR][RPW][VEC];
+        typename FLoad<TF, VEC>::Raw fv[UNR][RPW];
+        double2 xv[UNR][RPW][VEC];
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
-                FLoad<TF, VEC>::load(fr[r] + j + u * kStep, pol, fv[u][r]);
+                FLoad<TF, VEC>::load_raw(fr[r] + j + u * kStep, pol, fv[u][r]);
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) xv[u][r][v] = __ldg(xr[r] + j + u * kStep + v);
             }
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int r = 0; r < RPW; ++r)
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], fv[u][r][v], xv[u][r][v]);
+                for (int v = 0; v < VEC; ++v) cmac(ar[r], ai[r], FLoad<TF, VEC>::get(fv[u][r], v), xv[u][r][v]);
     }
     for (; j < nm; j += kStep) {
 #pragma unroll
