@@ -106,6 +106,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.file = None
+        self.skip = 0
 
     def __enter__(self):
         try:
@@ -113,6 +114,13 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a moment to emit its first row: wait for it (<= 3 s)
+            # so a short timed region still gets samples; rows already written
+            # before the timed region are skipped in summary()
+            t_end = time.time() + 3.0
+            while time.time() < t_end and Path(self.file.name).stat().st_size == 0:
+                time.sleep(0.02)
+            self.skip = len(Path(self.file.name).read_text().strip().splitlines())
         except Exception:
             self.proc = None
         return self
@@ -129,8 +137,10 @@ class ClockSampler:
         if not self.file:
             return None
         try:
-            rows = [ln.split(",") for ln in Path(self.file.name).read_text().strip().splitlines() if ln.strip()]
+            lines = [ln for ln in Path(self.file.name).read_text().strip().splitlines() if ln.strip()]
             os.unlink(self.file.name)
+            # rows from inside the timed region; the last pre-region row if it was too short for one
+            rows = [ln.split(",") for ln in (lines[self.skip:] or lines[-1:])]
         except Exception:
             return None
         sm, mx, reasons = [], [], set()

@@ -513,9 +513,17 @@ btg_status host_forward_stage(btg_op op, const double* m_host) {
         const auto [j0, nc] = plan[c];
         BTG_CUDA(cudaMemcpyAsync(op->hin + j0 * nt, m_host + j0 * nt, nc * nt * sizeof(double),
                                  cudaMemcpyHostToDevice, op->copy_stream));
+        // the chunk's R2C runs on the copy stream behind its H2D, so it overlaps the
+        // previous chunk's GEMV instead of sitting between GEMVs on the compute stream
+        {
+            cudaStream_t main = op->stream;
+            op->stream = op->copy_stream;
+            const btg_status st = run_r2c_vec(op, op->hin + j0 * nt, nc, op->wa + j0, op->nm);
+            op->stream = main;
+            BTG_TRY(st);
+        }
         BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
         BTG_CUDA(cudaStreamWaitEvent(op->stream, op->ev[c], 0));
-        BTG_TRY(run_r2c_vec(op, op->hin + j0 * nt, nc, op->wa + j0, op->nm));
         BTG_TRY(gemv_range(op, false, op->wa, op->wb, j0, nc, c > 0));
     }
     count_apply(op);
