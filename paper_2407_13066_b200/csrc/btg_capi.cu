@@ -448,7 +448,7 @@ std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
     const size_t big = std::max<size_t>(512, (op->nm / 8 + 511) / 512 * 512);
     std::vector<size_t> sizes;
     size_t left = op->nm;
-    for (size_t w = 1024; w < big && left > 0; w *= 2) {
+    for (size_t w = 512; w < big && left > 0; w *= 2) {
         sizes.push_back(std::min(w, left));
         left -= sizes.back();
     }
