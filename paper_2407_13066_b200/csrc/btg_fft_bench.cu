@@ -67,9 +67,15 @@ struct Run {
         for (size_t i = 0; i < nx; ++i) hx[i] = (double)rand() / RAND_MAX - 0.5;
         CK(cudaMemcpy(x, hx.data(), nx * 8, cudaMemcpyHostToDevice));
 
-        auto r2c = pf_r ? fast::k_r2c_pf<N, CPBR> : fast::k_r2c_fast<N, CPBR>;
+#ifdef BENCH_NO_TMA
+        constexpr bool tma_r = false;
+#else
+        constexpr bool tma_r = fast::UseTmaR2C<N>::value;
+#endif
+        auto r2c = tma_r ? fast::k_r2c_tma<N, CPBR> : pf_r ? fast::k_r2c_pf<N, CPBR> : fast::k_r2c_fast<N, CPBR>;
         auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
-        constexpr size_t smem_r = fast::smem_bytes<N, CPBR>(), smem_c = fast::smem_bytes<N, CPBC>();
+        constexpr size_t smem_r = tma_r ? fast::smem_bytes_tma<N, CPBR>() : fast::smem_bytes<N, CPBR>();
+        constexpr size_t smem_c = fast::smem_bytes<N, CPBC>();
         CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
         CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
         int occ_r = 1, occ_c = 1, sms = 148;
@@ -77,7 +83,7 @@ struct Run {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, r2c, P::TPC * CPBR, smem_r);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c2r, P::TPC * CPBC, smem_c);
         const int groups_r = (C + CPBR - 1) / CPBR, groups_c = (C + CPBC - 1) / CPBC;
-        const int grid_r = pf_r ? std::min(groups_r, occ_r * sms) : groups_r;
+        const int grid_r = (pf_r || tma_r) ? std::min(groups_r, occ_r * sms) : groups_r;
         const int grid_c = pf_c ? std::min(groups_c, occ_c * sms) : groups_c;
         C2REpilogue epi{};
         cudaEvent_t e0, e1, e2;

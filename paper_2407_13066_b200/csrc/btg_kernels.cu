@@ -756,6 +756,18 @@ cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long lo
         return cudaErrorNotSupported;
     } else {
         constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        if constexpr (fast::UseTmaR2C<N>::value && CPB == P::CPB_R2C) {
+            if (channels <= fast::UseTmaR2C<N>::max_channels) {
+                constexpr size_t smem_t = fast::smem_bytes_tma<N, CPB>();
+                auto kt = fast::k_r2c_tma<N, CPB>;
+                cudaError_t e = set_smem(kt, smem_t);
+                if (e != cudaSuccess) return e;
+                if (bm.pexp && channels % CPB != 0) return cudaErrorInvalidValue;
+                const int grid = persistent_grid(kt, P::TPC * CPB, smem_t, (channels + CPB - 1) / CPB);
+                kt<<<grid, P::TPC * CPB, smem_t, stream>>>(in, in_cs, out, out_fs, channels, tabs, bm);
+                return cudaGetLastError();
+            }
+        }
         auto kern = P::PF_R2C ? fast::k_r2c_pf<N, CPB> : fast::k_r2c_fast<N, CPB>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
