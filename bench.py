@@ -541,6 +541,26 @@ def run_ours(args):
                "ops_ms": {k: statistics.median(v) for k, v in e_ops.items()},
                "path": "btg_forward/btg_adjoint/btg_hessian with pinned host buffers (H2D + compute + D2H per call)"}
 
+    # The Hessian's consumer (row f1): device-resident CG, fixed iteration count
+    # (tol 0), CUDA events on the handle's stream; one Hessian per iteration.
+    solver = None
+    if engine is None and nrhs == 1 and rank == 0:
+        try:
+            iters = 20
+            btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=1)  # warm
+            torch.cuda.synchronize(device)
+            c0, c1 = ev(), ev()
+            c0.record(stream)
+            _, it_done, _, _ = btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=iters)
+            c1.record(stream)
+            torch.cuda.synchronize(device)
+            ms_it = c0.elapsed_time(c1) / max(1, it_done)
+            solver = {"iterations": it_done, "ms_per_iteration": ms_it,
+                      "TB/s": b["H"] / (ms_it * 1e-3) / 1e12,
+                      "path": "btg_cg_solve (inverse.cpp:105-156 on the device): one F* F + alpha I per iteration"}
+        except Exception as exc:
+            solver = {"error": str(exc)}
+
     # Multi-RHS: the alternative engine of the Fourier step measured on the same
     # operator — exact-integer Ozaki splitting on the tcgen05 int8 tensor cores.
     alt = None
@@ -611,6 +631,8 @@ def run_ours(args):
         }
         if alt:
             line["alt_engines"] = alt
+        if solver:
+            line["solver"] = solver
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

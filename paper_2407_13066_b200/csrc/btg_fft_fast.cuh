@@ -539,33 +539,45 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     for (int bf = 0; bf < BF; ++bf) {
         const int j = tc + bf * TPC;
         if (NB % TPC == 0 || j < NB) {
+            // epilogue operands first (16-byte loads), so their latency overlaps the pass
+            constexpr int NQ = (R + 1) / 2;
+            double2 er[NQ], eg[NQ];
+            double el[NQ], eh[NQ];
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int p = j + q * NB;
+                const bool ok = p < N / 2;
+                const int t0 = 2 * p;
+                er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
+                el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
+                eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
+                eg[q] = (epi.gamma_mode == 2 && ok)
+                            ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
+                            : make_double2(1.0, 1.0);
+            }
             double2 v[R];
-#pragma unroll
+            #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
             twiddle_inputs<N, R, NS, +1>(v, j, lo, hi);
             dft<R, +1>(v);
-#pragma unroll
-            for (int q = 0; q < (R + 1) / 2; ++q) {  // keep p = j + q*NB < N/2 (unpad)
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q) {  // keep p = j + q*NB < N/2 (unpad)
                 const int p = j + q * NB;
                 if ((R % 2 == 1) && q == R / 2 && p >= N / 2) break;
                 double y0 = v[q].x, y1 = v[q].y;
-                const int t0 = 2 * p;
                 if (epi.gamma_mode == 1) {
                     const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
                     y0 *= g;
                     y1 *= g;
                 } else if (epi.gamma_mode == 2) {
-                    const double* gr = epi.gamma + (long long)(c % epi.gamma_dim) * N;
-                    y0 *= __ldg(gr + t0);
-                    y1 *= __ldg(gr + t0 + 1);
+                    y0 *= eg[q].x;
+                    y1 *= eg[q].y;
                 }
                 if (vrow) {
-                    double r0 = __ldg(vrow + t0), r1 = __ldg(vrow + t0 + 1);
+                    double r0 = er[q].x, r1 = er[q].y;
                     if (epi.reg_kind == 1) {
-                        const double l = t0 > 0 ? __ldg(vrow + t0 - 1) : 0.0;
-                        const double h = t0 + 2 < N ? __ldg(vrow + t0 + 2) : 0.0;
-                        const double a0 = 2.0 * r0 - l - r1;  // reference order: 2x - x[t-1] - x[t+1]
-                        const double a1 = 2.0 * r1 - r0 - h;
+                        const double a0 = 2.0 * r0 - el[q] - r1;  // reference order: 2x - x[t-1] - x[t+1]
+                        const double a1 = 2.0 * r1 - r0 - eh[q];
                         r0 = a0;
                         r1 = a1;
                     }
@@ -864,33 +876,45 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
             for (int bf = 0; bf < BF; ++bf) {
                 const int j = tc + bf * TPC;
                 if (NB % TPC == 0 || j < NB) {
+                    // epilogue operands first (16-byte loads), so their latency overlaps the pass
+                    constexpr int NQ = (R + 1) / 2;
+                    double2 er[NQ], eg[NQ];
+                    double el[NQ], eh[NQ];
+                    #pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int p = j + q * NB;
+                        const bool ok = p < N / 2;
+                        const int t0 = 2 * p;
+                        er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
+                        el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
+                        eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
+                        eg[q] = (epi.gamma_mode == 2 && ok)
+                                    ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
+                                    : make_double2(1.0, 1.0);
+                    }
                     double2 v[R];
-#pragma unroll
+                    #pragma unroll
                     for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
                     twiddle_inputs<N, R, NS, +1>(v, j, lo, hi);
                     dft<R, +1>(v);
-#pragma unroll
-                    for (int q = 0; q < (R + 1) / 2; ++q) {  // keep p = j + q*NB < N/2 (unpad)
+                    #pragma unroll
+                    for (int q = 0; q < NQ; ++q) {  // keep p = j + q*NB < N/2 (unpad)
                         const int p = j + q * NB;
                         if ((R % 2 == 1) && q == R / 2 && p >= N / 2) break;
                         double y0 = v[q].x, y1 = v[q].y;
-                        const int t0 = 2 * p;
                         if (epi.gamma_mode == 1) {
-                            const double gm = __ldg(epi.gamma + (c % epi.gamma_dim));
-                            y0 *= gm;
-                            y1 *= gm;
+                            const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
+                            y0 *= g;
+                            y1 *= g;
                         } else if (epi.gamma_mode == 2) {
-                            const double* gr = epi.gamma + (long long)(c % epi.gamma_dim) * N;
-                            y0 *= __ldg(gr + t0);
-                            y1 *= __ldg(gr + t0 + 1);
+                            y0 *= eg[q].x;
+                            y1 *= eg[q].y;
                         }
                         if (vrow) {
-                            double r0 = __ldg(vrow + t0), r1 = __ldg(vrow + t0 + 1);
+                            double r0 = er[q].x, r1 = er[q].y;
                             if (epi.reg_kind == 1) {
-                                const double l = t0 > 0 ? __ldg(vrow + t0 - 1) : 0.0;
-                                const double h = t0 + 2 < N ? __ldg(vrow + t0 + 2) : 0.0;
-                                const double a0 = 2.0 * r0 - l - r1;  // reference order: 2x - x[t-1] - x[t+1]
-                                const double a1 = 2.0 * r1 - r0 - h;
+                                const double a0 = 2.0 * r0 - el[q] - r1;  // reference order: 2x - x[t-1] - x[t+1]
+                                const double a1 = 2.0 * r1 - r0 - eh[q];
                                 r0 = a0;
                                 r1 = a1;
                             }
