@@ -8,7 +8,7 @@ Python surface (operator, solver, files) plus the multi-GPU grid
 """
 
 from ._lib import DimensionError, Error, FormatError, GridError, OrderingError, SolverError  # noqa: F401
-from .distributed import distributed_adjoint, distributed_forward  # noqa: F401
+from .distributed import Partition, distributed_adjoint, distributed_forward, partition_operator  # noqa: F401
 from .io import (load_operator, peek_operator, read_operator, read_vector, save_operator,  # noqa: F401
                  write_operator, write_vector)
 from .operator import (HessianOperator, SpectralOperator, create, fill_uniform, naive_apply_adjoint,  # noqa: F401
@@ -23,6 +23,7 @@ __all__ = [
     "FormatError",
     "GridError",
     "OrderingError",
+    "Partition",
     "SolverError",
     "HessianOperator",
     "SpectralOperator",
@@ -44,6 +45,7 @@ __all__ = [
     "naive_apply_adjoint",
     "naive_apply_forward",
     "objective_eval",
+    "partition_operator",
     "peek_operator",
     "read_operator",
     "read_vector",
