@@ -945,8 +945,9 @@ __host__ __device__ constexpr size_t smem_bytes_tma() {
     return smem_bytes<N, CPB>() + sizeof(double) * CPB * stage_stride<N>() + 16;
 }
 // Plans that have the TMA-staged R2C, and the largest channel count it is used for:
-// measured on B200 at N_t = 1024 it wins at 32768 channels (0.194 vs 0.220 ms) and
-// loses at 524288 (3.8 vs 3.5 ms: 16 resident warps per SM instead of 24).
+// measured on B200 at N_t = 1024 it wins up to ~2e5 channels (32768: 0.194 vs 0.220 ms;
+// 196608: 1.276 vs 1.309 ms) and loses beyond (262144: 1.82 vs 1.77; 524288: 3.8 vs
+// 3.5 ms — 16 resident warps per SM instead of 24).
 template <int N>
 struct UseTmaR2C {
     static constexpr bool value = false;
@@ -955,7 +956,7 @@ struct UseTmaR2C {
 template <>
 struct UseTmaR2C<1024> {
     static constexpr bool value = true;
-    static constexpr int max_channels = 65536;
+    static constexpr int max_channels = 196608;
 };
 
 template <int N, int CPB>
