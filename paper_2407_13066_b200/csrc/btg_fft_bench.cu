@@ -69,6 +69,8 @@ struct Run {
 
 #ifdef BENCH_NO_TMA
         constexpr bool tma_r = false;
+#elif defined(BENCH_FORCE_TMA)
+        constexpr bool tma_r = true;
 #else
         constexpr bool tma_r = fast::UseTmaR2C<N>::value;
 #endif
