@@ -23,7 +23,11 @@
 //   The same bytes are the K-major A operand of the forward (rows i, K = j) and
 //   the MN-major A operand of the adjoint (rows j, K = i).
 //   Block scales  mA[f][jb] (max |F| over all i and the 1024-column block jb)
-//   Vector scales mB[f][r][kb] (max over a 1024-entry block of x-hat_f[r] / d-hat_f[r])
+//   Vector scales mB[f][r][kb] (max over a 1024-entry block of x-hat_f[r] / d-hat_f[r]);
+//   for the forward they come from the R2C epilogue (per-group exponents,
+//   k_exponents), else from k_scale_vec
+//   Adjoint B tiles Bq[f][ks][tile]: d-hat_f sliced once per frequency (k_slice_vec)
+//   and TMA-fed, since every row tile of f multiplies the same d-hat_f
 // The complex product uses plane-separated K: K' = (c, k); the B operand rows
 // n' = 2r+q carry (xr, xi) against the real plane and (-xi, xr) against the
 // imaginary plane (adjoint: (dr, di) and (di, -dr)), so one real GEMM yields
@@ -36,6 +40,7 @@
 //              slices t = 0..S-1-s in ONE descriptor window (N = NP (S-s), split
 //              at 256) whose products land in the consecutive level accumulators
 //              s + t: 20 MMAs per 32-wide K step at N = 64 (instead of 56 small ones).
+//   warp 0 lane 1 (adjoint) TMA producer of the pre-sliced B tiles
 //   warps 2-5  prefetch the FP64 vector block of step it+2 (cp.async into a
 //              thread-private ring), slice step it into the B tile (shared
 //              memory), and drain the TMEM level accumulators into FP64
