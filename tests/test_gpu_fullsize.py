@@ -1,5 +1,5 @@
-"""Parity at BASELINE.json's full sizes (configs[1] and configs[2]) through
-size-independent properties, without 100+ GB of host memory:
+"""Parity at BASELINE.json's full sizes (configs[1], configs[2], a configs[4] 1x8 shard,
+and configs[3] on both multi-RHS engines) through size-independent properties, without 100+ GB of host memory:
 
 * F* column slices: output column j of F* d depends only on column j of F, so a
   slice J of m is checked against the oracle on host-regenerated blocks[:, :, J];
@@ -29,7 +29,8 @@ def _build(nt, nd, nm):
     return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), SEED, 0)
 
 
-@pytest.mark.parametrize("dims", [(1024, 100, 32768), (1000, 600, 8192)], ids=["configs1", "configs2"])
+@pytest.mark.parametrize("dims", [(1024, 100, 32768), (1000, 600, 8192), (4096, 256, 8192)],
+                         ids=["configs1", "configs2", "configs4_1x8_shard"])
 def test_full_size_slices_and_pairing(dims):
     import torch
 
