@@ -20,13 +20,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 SEED = 4242
 
 
-def _build(nt, nd, nm):
+def _build(nt, nd, nm, precision=64):
     import torch
 
     from paper_2407_13066_b200.distributed import Shard, synthetic_shard_operator
 
     torch.cuda.empty_cache()
-    return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), SEED, 0)
+    return synthetic_shard_operator(nd, nm, nt, Shard(0, 0, 0, nd, 0, nm), SEED, 0, precision=precision)
 
 
 @pytest.mark.parametrize("dims", [(1024, 100, 32768), (1000, 600, 8192), (4096, 256, 8192)],
@@ -114,6 +114,30 @@ def test_configs3_multi_rhs_full_size(engine):
         lhs = torch.sum(op.apply_forward(Mf) * Df, dim=(1, 2))
         rhs = torch.sum(Mf * op.apply_adjoint(Df), dim=(1, 2))
         assert float(torch.max(torch.abs(lhs - rhs) / torch.abs(lhs))) <= 1e-11
+    finally:
+        op.close()
+        torch.cuda.empty_cache()
+
+
+def test_configs4_fp32_shard_full_size():
+    """configs[4]'s FP32 F-hat variant at a 1x4 shard (N_t=4096, N_d=256,
+    N_m=16384, 137 GB of complex64 F-hat): column-slice parity at the FP32 bar
+    (relative L2 <= 1e-5, north star) against the FP64 oracle."""
+    import torch
+
+    nt, nd, nm = 4096, 256, 16384
+    op = _build(nt, nd, nm, precision=32)
+    try:
+        rng = np.random.default_rng(9)
+        J = np.sort(rng.choice(nm, size=12, replace=False))
+        spec_J = R.setup_full(R.synthetic_blocks_slice(SEED, nd, nm, nt, np.arange(nd), J))
+        mJ = rng.uniform(-1, 1, size=(len(J), nt))
+        m = torch.zeros((nm, nt), dtype=torch.float64, device="cuda:0")
+        m[torch.from_numpy(J).cuda()] = torch.from_numpy(mJ).cuda()
+        assert R.rel_l2(op.apply_forward(m).cpu().numpy(), R.apply_forward(spec_J, mJ)) <= 1e-5
+        d = rng.uniform(-1, 1, size=(nd, nt))
+        a = op.apply_adjoint(torch.from_numpy(d).cuda()).cpu().numpy()
+        assert R.rel_l2(a[J], R.apply_adjoint(spec_J, d)) <= 1e-5
     finally:
         op.close()
         torch.cuda.empty_cache()
