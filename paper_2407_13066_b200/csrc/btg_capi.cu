@@ -441,14 +441,27 @@ bool host_pipelined(btg_op op, size_t nrhs) {
     return !off && nrhs == 1 && op->legacy_gemv && op->nm >= 4096;
 }
 
-// Column chunks (multiples of 512 columns): N_m/8-wide, except a geometric
-// ramp of small chunks where the pipeline fills (first H2D) or drains (last
-// D2H) — the only transfers left exposed. At most kHostChunks chunks.
+// Column chunks (multiples of 256 columns): a geometric ramp from 512 columns,
+// x1.5 per chunk, capped at N_m/2. The first H2D (last D2H) is the only
+// transfer left exposed; x1.5 keeps each next chunk's PCIe copy (8 N_t B per
+// column at ~55 GB/s) shorter than the current chunk's GEMV (16 N_d (N_t+1) B
+// per column at ~7 TB/s), so the GEMVs never wait — a x2 ramp did (CUPTI
+// timeline, profiles/tools/host_timeline.py; 33.5 -> 33.2 ms per configs[1]
+// e2e step). At most kHostChunks chunks. BTG_HOST_RAMP (percent) and
+// BTG_HOST_BIG_DIV are tuning knobs.
 std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
-    const size_t big = std::max<size_t>(512, (op->nm / 8 + 511) / 512 * 512);
+    static const size_t growth = [] {
+        const char* s = std::getenv("BTG_HOST_RAMP");
+        return s ? std::max<size_t>(110, std::strtoul(s, nullptr, 10)) : 150;
+    }();
+    static const size_t div = [] {
+        const char* s = std::getenv("BTG_HOST_BIG_DIV");
+        return s ? std::max<size_t>(1, std::strtoul(s, nullptr, 10)) : 2;
+    }();
+    const size_t big = std::max<size_t>(512, (op->nm / div + 511) / 512 * 512);
     std::vector<size_t> sizes;
     size_t left = op->nm;
-    for (size_t w = 512; w < big && left > 0; w *= 2) {
+    for (size_t w = 512; w < big && left > 0; w = (w * growth / 100 + 255) / 256 * 256) {
         sizes.push_back(std::min(w, left));
         left -= sizes.back();
     }
