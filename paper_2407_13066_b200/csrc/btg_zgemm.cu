@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "btg_kernels.cuh"
 
@@ -273,6 +274,249 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 }
 
+// ---------------------------------------------------------------------------
+// 3M variants (default): three real products per complex product instead of the
+// four the embedding above performs, so each DMMA carries 4/3 as many complex
+// MACs (6 real flops per complex MAC instead of 8):
+//   forward  P1 = Fr Xr, P2 = Fi Xi, P3 = (Fr + Fi)(Xr + Xi);  D = (P1 - P2, P3 - P1 - P2)
+//   adjoint  P1 = Fr Dr, P2 = Fi Di, P3 = (Fr - Fi)(Dr + Di);  G = (P1 + P2, P3 - P1 + P2)
+// K runs over complex indices; one 16-byte shared load yields both parts of an
+// operand, and the operand sums are formed in registers. The same 128 x 32-complex
+// CTA tile; each warp owns 32 rows x 16 complex RHS (2 x 2 m16n8k4 tiles per
+// product). Padded strides keep every fragment load conflict-free (16-byte
+// slots: row stride = 16 banks mod 32 for the forward A / both B, 8 for the
+// adjoint A). Normwise the 3M error bound is a small constant times the 4M one
+// (the parity bar is relative L2 over the output); the fixed K order keeps results
+// deterministic.
+// ---------------------------------------------------------------------------
+constexpr int kF3AStride = 2 * kFwdKc + 8;  // doubles per A row
+constexpr int kM3BStride = kFwdKc + 4;      // complex per B row (both directions)
+constexpr size_t kF3StageDoubles = (size_t)kTileM * kF3AStride + 2 * (size_t)kTileR * kM3BStride;
+constexpr int kA3AStride = kTileM + 2;      // complex per adjoint A row (i)
+constexpr size_t kA3StageDoubles = 2 * ((size_t)kAdjKc * kA3AStride + (size_t)kTileR * kM3BStride);
+
+template <bool kAdj>
+__device__ __forceinline__ void mma3(double (&p1)[2][2][4], double (&p2)[2][2][4], double (&p3)[2][2][4],
+                                     const double2 (&a)[2][2], const double2 (&b)[2]) {
+    double as[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) as[mt][h] = kAdj ? a[mt][h].x - a[mt][h].y : a[mt][h].x + a[mt][h].y;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        const double bs = b[nt].x + b[nt].y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            dmma(p1[mt][nt], a[mt][0].x, a[mt][1].x, b[nt].x);
+            dmma(p2[mt][nt], a[mt][0].y, a[mt][1].y, b[nt].y);
+            dmma(p3[mt][nt], as[mt][0], as[mt][1], bs);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_zgemm3m_fwd(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
+                  int nm, int nrhs) {
+    extern __shared__ __align__(16) double sm[];
+    const int f = blockIdx.y;
+    const int m0 = blockIdx.x * kTileM;
+    const int r0 = blockIdx.z * kTileR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const double2* Ff = F + (size_t)f * nd * nm;
+    const double2* Xf = X + (size_t)f * nrhs * nm;
+
+    auto stage_a = [&](int st) { return sm + (size_t)st * kF3StageDoubles; };
+    auto stage_b = [&](int st) {
+        return reinterpret_cast<double2*>(sm + (size_t)st * kF3StageDoubles + (size_t)kTileM * kF3AStride);
+    };
+    auto load_stage = [&](int st, int kc) {
+        double* As = stage_a(st);
+        double2* Bs = stage_b(st);
+#pragma unroll
+        for (int q = 0; q < (kTileM * kFwdKc) / kThreads; ++q) {
+            const int idx = threadIdx.x + q * kThreads;
+            const int row = idx / kFwdKc, col = idx % kFwdKc;
+            const int gi = m0 + row, gj = kc + col;
+            const bool ok = gi < nd && gj < nm;
+            cp_async16(As + row * kF3AStride + 2 * col, Ff + (size_t)(ok ? gi : 0) * nm + (ok ? gj : 0), ok);
+        }
+#pragma unroll
+        for (int q = 0; q < (kTileR * kFwdKc) / kThreads; ++q) {
+            const int idx = threadIdx.x + q * kThreads;
+            const int r = idx / kFwdKc, col = idx % kFwdKc;
+            const int gr = r0 + r, gj = kc + col;
+            const bool ok = gr < nrhs && gj < nm;
+            cp_async16(Bs + r * kM3BStride + col, Xf + (size_t)(ok ? gr : 0) * nm + (ok ? gj : 0), ok);
+        }
+    };
+
+    double p1[2][2][4], p2[2][2][4], p3[2][2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) p1[a][b][c] = p2[a][b][c] = p3[a][b][c] = 0.0;
+
+    const int nk = (nm + kFwdKc - 1) / kFwdKc;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) load_stage(s, s * kFwdKc);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        {
+            const int nxt = kt + kStages - 1;
+            if (nxt < nk) load_stage(nxt % kStages, nxt * kFwdKc);
+            cp_async_commit();
+        }
+        const double* As = stage_a(kt % kStages);
+        const double2* Bs = stage_b(kt % kStages);
+#pragma unroll
+        for (int ks = 0; ks < kFwdKc / 4; ++ks) {
+            const int kk = ks * 4 + tig;  // complex k of this lane's A column / B row
+            double2 a[2][2], b[2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    a[mt][h] = *reinterpret_cast<const double2*>(As + (wm * 32 + mt * 16 + h * 8 + g) * kF3AStride +
+                                                                 2 * kk);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[(wn * 16 + nt * 8 + g) * kM3BStride + kk];
+            mma3<false>(p1, p2, p3, a, b);
+        }
+    }
+    cp_async_wait<0>();
+
+    // lane holds C[g (+8)][2 tig + q]: rows (i) x complex RHS
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int r = r0 + wn * 16 + nt * 8 + 2 * tig + q;
+                if (r >= nrhs) continue;
+                double2* yr = Y + ((size_t)f * nrhs + r) * nd;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int row = m0 + wm * 32 + mt * 16 + h * 8 + g;
+                    const int c = 2 * h + q;
+                    if (row < nd)
+                        yr[row] = make_double2(p1[mt][nt][c] - p2[mt][nt][c],
+                                               p3[mt][nt][c] - p1[mt][nt][c] - p2[mt][nt][c]);
+                }
+            }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_zgemm3m_adj(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
+                  int nm, int nrhs) {
+    extern __shared__ __align__(16) double sm[];
+    const int f = blockIdx.y;
+    const int j0 = blockIdx.x * kTileM;
+    const int r0 = blockIdx.z * kTileR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const double2* Ff = F + (size_t)f * nd * nm;
+    const double2* Xf = X + (size_t)f * nrhs * nd;
+
+    auto stage_a = [&](int st) { return reinterpret_cast<double2*>(sm + (size_t)st * kA3StageDoubles); };
+    auto stage_b = [&](int st) {
+        return reinterpret_cast<double2*>(sm + (size_t)st * kA3StageDoubles + 2 * (size_t)kAdjKc * kA3AStride);
+    };
+    auto load_stage = [&](int st, int kc) {
+        double2* As = stage_a(st);
+        double2* Bs = stage_b(st);
+#pragma unroll
+        for (int q = 0; q < (kAdjKc * kTileM) / kThreads; ++q) {
+            const int idx = threadIdx.x + q * kThreads;
+            const int ii = idx / kTileM, jj = idx % kTileM;
+            const int gi = kc + ii, gj = j0 + jj;
+            const bool ok = gi < nd && gj < nm;
+            cp_async16(As + ii * kA3AStride + jj, Ff + (size_t)(ok ? gi : 0) * nm + (ok ? gj : 0), ok);
+        }
+#pragma unroll
+        for (int q = 0; q < (kTileR * kAdjKc) / kThreads; ++q) {
+            const int idx = threadIdx.x + q * kThreads;
+            const int r = idx / kAdjKc, ii = idx % kAdjKc;
+            const int gr = r0 + r, gi = kc + ii;
+            const bool ok = gr < nrhs && gi < nd;
+            cp_async16(Bs + r * kM3BStride + ii, Xf + (size_t)(ok ? gr : 0) * nd + (ok ? gi : 0), ok);
+        }
+    };
+
+    double p1[2][2][4], p2[2][2][4], p3[2][2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) p1[a][b][c] = p2[a][b][c] = p3[a][b][c] = 0.0;
+
+    const int nk = (nd + kAdjKc - 1) / kAdjKc;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) load_stage(s, s * kAdjKc);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        {
+            const int nxt = kt + kStages - 1;
+            if (nxt < nk) load_stage(nxt % kStages, nxt * kAdjKc);
+            cp_async_commit();
+        }
+        const double2* As = stage_a(kt % kStages);
+        const double2* Bs = stage_b(kt % kStages);
+#pragma unroll
+        for (int ks = 0; ks < kAdjKc / 4; ++ks) {
+            const int kk = ks * 4 + tig;  // complex i of this lane's A column / B row
+            double2 a[2][2], b[2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) a[mt][h] = As[kk * kA3AStride + wm * 32 + mt * 16 + h * 8 + g];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[(wn * 16 + nt * 8 + g) * kM3BStride + kk];
+            mma3<true>(p1, p2, p3, a, b);
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int r = r0 + wn * 16 + nt * 8 + 2 * tig + q;
+                if (r >= nrhs) continue;
+                double2* yr = Y + ((size_t)f * nrhs + r) * nm;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int jj = j0 + wm * 32 + mt * 16 + h * 8 + g;
+                    const int c = 2 * h + q;
+                    if (jj < nm)
+                        yr[jj] = make_double2(p1[mt][nt][c] + p2[mt][nt][c],
+                                              p3[mt][nt][c] - p1[mt][nt][c] + p2[mt][nt][c]);
+                }
+            }
+}
+
+bool use_4m() {
+    static const bool v = std::getenv("BTG_ZGEMM_4M") != nullptr;
+    return v;
+}
+
 constexpr int kMaxGridY = 65535;
 
 template <typename K>
@@ -284,28 +528,32 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream) {
-    const size_t smem = kStages * kFwdStageDoubles * sizeof(double);
-    cudaError_t e = set_smem(k_zgemm_fwd, smem);
+    const bool m4 = use_4m();
+    const auto kern = m4 ? k_zgemm_fwd : k_zgemm3m_fwd;
+    const size_t smem = kStages * (m4 ? kFwdStageDoubles : kF3StageDoubles) * sizeof(double);
+    cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
         const int nb = std::min(kMaxGridY, nf - f0);
         dim3 grid((nd + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
-        k_zgemm_fwd<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nm,
-                                                      Y + (size_t)f0 * nrhs * nd, nd, nm, nrhs);
+        kern<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nm,
+                                               Y + (size_t)f0 * nrhs * nd, nd, nm, nrhs);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream) {
-    const size_t smem = kStages * kAdjStageDoubles * sizeof(double);
-    cudaError_t e = set_smem(k_zgemm_adj, smem);
+    const bool m4 = use_4m();
+    const auto kern = m4 ? k_zgemm_adj : k_zgemm3m_adj;
+    const size_t smem = kStages * (m4 ? kAdjStageDoubles : kA3StageDoubles) * sizeof(double);
+    cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {
         const int nb = std::min(kMaxGridY, nf - f0);
         dim3 grid((nm + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
-        k_zgemm_adj<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nd,
-                                                      Y + (size_t)f0 * nrhs * nm, nd, nm, nrhs);
+        kern<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nd,
+                                               Y + (size_t)f0 * nrhs * nm, nd, nm, nrhs);
     }
     return cudaGetLastError();
 }
