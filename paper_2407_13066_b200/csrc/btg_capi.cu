@@ -441,38 +441,49 @@ bool host_pipelined(btg_op op, size_t nrhs) {
     return !off && nrhs == 1 && op->legacy_gemv && op->nm >= 4096;
 }
 
-// Column chunks (multiples of 256 columns): a geometric ramp from 512 columns,
-// x1.5 per chunk, capped at N_m/2. The first H2D (last D2H) is the only
-// transfer left exposed; x1.5 keeps each next chunk's PCIe copy (8 N_t B per
-// column at ~55 GB/s) shorter than the current chunk's GEMV (16 N_d (N_t+1) B
-// per column at ~7 TB/s), so the GEMVs never wait — a x2 ramp did (CUPTI
-// timeline, profiles/tools/host_timeline.py; 33.5 -> 33.2 ms per configs[1]
-// e2e step). At most kHostChunks chunks. BTG_HOST_RAMP (percent) and
-// BTG_HOST_BIG_DIV are tuning knobs.
+// Column chunks (multiples of 256 columns): a geometric ramp x1.5 per chunk from
+// ~512 columns, scaled so the series ends exactly at N_m (no small leftover
+// chunk: a GEMV over a few thousand columns runs at ~6 TB/s, not ~7.2). The first
+// H2D (last D2H) is the only transfer left exposed; x1.5 keeps each next chunk's
+// PCIe copy (8 N_t B per column at ~55 GB/s) shorter than the current chunk's
+// GEMV (16 N_d (N_t+1) B per column at ~7 TB/s), so the GEMVs never wait — a x2
+// ramp did (CUPTI timeline, profiles/tools/host_timeline.py; 33.5 -> 33.2 ms per
+// configs[1] e2e step). At most kHostChunks chunks (wider N_m: the ramp, then
+// equal chunks). BTG_HOST_RAMP (percent) is a tuning knob.
 std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
-    static const size_t growth = [] {
+    static const double growth = [] {
         const char* s = std::getenv("BTG_HOST_RAMP");
-        return s ? std::max<size_t>(110, std::strtoul(s, nullptr, 10)) : 150;
+        return s ? std::max(1.1, std::strtod(s, nullptr) / 100.0) : 1.5;
     }();
-    static const size_t div = [] {
-        const char* s = std::getenv("BTG_HOST_BIG_DIV");
-        return s ? std::max<size_t>(1, std::strtoul(s, nullptr, 10)) : 2;
-    }();
-    const size_t big = std::max<size_t>(512, (op->nm / div + 511) / 512 * 512);
+    const size_t nm = op->nm;
+    std::vector<double> geo;
+    double sum = 0.0;
+    for (double w = 512.0; sum < (double)nm && geo.size() < kHostChunks; w *= growth) {
+        geo.push_back(w);
+        sum += w;
+    }
     std::vector<size_t> sizes;
-    size_t left = op->nm;
-    for (size_t w = 512; w < big && left > 0; w = (w * growth / 100 + 255) / 256 * 256) {
-        sizes.push_back(std::min(w, left));
-        left -= sizes.back();
-    }
-    while (left > 0) {
-        sizes.push_back(std::min(big, left));
-        left -= sizes.back();
-    }
-    while (sizes.size() > kHostChunks) {
-        const size_t x = sizes.back();
-        sizes.pop_back();
-        sizes.back() += x;
+    size_t used = 0;
+    if (sum >= (double)nm) {
+        const double scale = (double)nm / sum;
+        for (size_t k = 0; k + 1 < geo.size(); ++k) {
+            const size_t w = std::max<size_t>(256, (size_t)std::llround(geo[k] * scale / 256.0) * 256);
+            if (used + w >= nm) break;
+            sizes.push_back(w);
+            used += w;
+        }
+        sizes.push_back(nm - used);
+    } else {  // the ramp's widest chunk, repeated; the remainder folds into the last
+        for (size_t k = 0; k + 1 < kHostChunks / 2 && used < nm; ++k) {
+            sizes.push_back(std::min<size_t>((size_t)geo[k] / 256 * 256, nm - used));
+            used += sizes.back();
+        }
+        const size_t n_eq = kHostChunks - sizes.size();
+        const size_t w = ((nm - used) / n_eq + 255) / 256 * 256;
+        while (used < nm) {
+            sizes.push_back(std::min(w, nm - used));
+            used += sizes.back();
+        }
     }
     if (!ramp_first) std::reverse(sizes.begin(), sizes.end());
     std::vector<std::pair<size_t, size_t>> plan;
