@@ -554,6 +554,15 @@ btg_status host_forward_stage(btg_op op, const double* m_host) {
     return BTG_OK;
 }
 
+// The C2R epilogue of a column chunk [j0, j0 + nc): its channel index restarts at 0,
+// so the per-channel operands (Gamma^-1, the alpha R v vector) are offset to j0.
+btg::C2REpilogue chunk_epilogue(const btg::C2REpilogue& epi, size_t j0, size_t nt, size_t v_off) {
+    btg::C2REpilogue e = epi;
+    if (e.v) e.v = epi.v + v_off;
+    if (e.gamma) e.gamma = epi.gamma + (e.gamma_mode == BTG_GAMMA_PER_SENSOR ? j0 : j0 * nt);
+    return e;
+}
+
 // d-hat spectrum in op->wa -> m (host) through chunked adjoint GEMV + C2R + D2H.
 btg_status host_adjoint_stage(btg_op op, double* m_host, const btg::C2REpilogue& epi) {
     BTG_TRY(ensure_copy_stream(op));
@@ -564,9 +573,8 @@ btg_status host_adjoint_stage(btg_op op, double* m_host, const btg::C2REpilogue&
         for (size_t c = 0; c < plan.size(); ++c) {
             const auto [j0, nc] = plan[c];
             BTG_TRY(gemv_range(op, true, op->wa, op->wb, j0, nc, false));
-            btg::C2REpilogue e = epi;
-            if (e.v) e.v = epi.v + j0 * nt;
-            BTG_TRY(run_c2r_vec(op, op->wb + j0, nc, op->hout + j0 * nt, e, op->nm));
+            BTG_TRY(run_c2r_vec(op, op->wb + j0, nc, op->hout + j0 * nt, chunk_epilogue(epi, j0, nt, j0 * nt),
+                                op->nm));
             BTG_CUDA(cudaEventRecord(op->ev[c], op->stream));
         }
     }
@@ -576,6 +584,100 @@ btg_status host_adjoint_stage(btg_op op, double* m_host, const btg::C2REpilogue&
         BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[c], 0));
         BTG_CUDA(cudaMemcpyAsync(m_host + j0 * nt, op->hout + j0 * nt, nc * nt * sizeof(double),
                                  cudaMemcpyDeviceToHost, op->copy_stream));
+    }
+    BTG_CUDA(cudaStreamSynchronize(op->copy_stream));
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    return BTG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-RHS host calls (FP64 F-hat, 3M ZGEMM engine). These are PCIe-bound: a
+// column moves nrhs x 8 N_t bytes over PCIe (~4.7 us at 32 RHS, N_t=1024) but
+// costs ~1 us of ZGEMM, so the ZGEMM (column chunks; the forward's K = j
+// partials accumulate in chunk order, deterministic) hides under the copies and
+// only the last (first) chunk's compute stays exposed: equal chunks, kHostChunks
+// of them. Each chunk moves as one 2-D copy (nrhs rows of nc x N_t values).
+// ---------------------------------------------------------------------------
+bool host_pipelined_mrhs(btg_op op, size_t nrhs) {
+    static const bool off = std::getenv("BTG_NO_HOST_PIPELINE") != nullptr;
+    return !off && nrhs > 1 && op->precision == BTG_F64 && !op->no_dmma && !op->tensor_i8 && btg::zgemm_3m() &&
+           op->nm >= 4096;
+}
+
+std::vector<std::pair<size_t, size_t>> mrhs_chunks(size_t nm) {
+    const size_t w = std::max<size_t>(256, (nm / kHostChunks + 255) / 256 * 256);
+    std::vector<std::pair<size_t, size_t>> plan;
+    for (size_t j0 = 0; j0 < nm; j0 += w) plan.emplace_back(j0, std::min(w, nm - j0));
+    return plan;
+}
+
+btg_status zgemm_range(btg_op op, bool adjoint, size_t nrhs, size_t j0, size_t nc, bool acc) {
+    const double2* F = static_cast<const double2*>(op->F);
+    const int nf = (int)op->nf, nd = (int)op->nd, nm = (int)op->nm;
+    BTG_CUDA(adjoint ? btg::launch_zgemm_adj_range(F, op->wa, op->wb, nf, nd, nm, (int)nrhs, (int)j0, (int)nc,
+                                                   op->stream)
+                     : btg::launch_zgemm_fwd_range(F, op->wa, op->wb, nf, nd, nm, (int)nrhs, (int)j0, (int)nc, acc,
+                                                   op->stream));
+    op->counters.launches++;
+    return BTG_OK;
+}
+
+void count_apply_mrhs(btg_op op, size_t nrhs) {
+    op->counters.apply.ops += 8.0 * op->nd * op->nm * op->nf * nrhs;
+    op->counters.apply.bytes += (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (op->nm + op->nd) * nrhs;
+}
+
+// m (host, nrhs x N_m x N_t) -> d-hat (nrhs stacked) in op->wb.
+btg_status host_forward_stage_mrhs(btg_op op, const double* m_host, size_t nrhs) {
+    BTG_TRY(ensure_spectral(op, nrhs));
+    BTG_TRY(ensure_copy_stream(op));
+    const size_t nt = op->nt, nm = op->nm, pitch = nm * nt * sizeof(double);
+    BTG_CUDA(cudaEventRecord(op->ev[kHostChunks], op->stream));  // hin free of earlier readers
+    BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[kHostChunks], 0));
+    const auto plan = mrhs_chunks(nm);
+    StageClock clk(op, &op->counters.apply);
+    for (size_t c = 0; c < plan.size(); ++c) {
+        const auto [j0, nc] = plan[c];
+        BTG_CUDA(cudaMemcpy2DAsync(op->hin + j0 * nt, pitch, m_host + j0 * nt, pitch, nc * nt * sizeof(double), nrhs,
+                                   cudaMemcpyHostToDevice, op->copy_stream));
+        cudaStream_t main = op->stream;
+        op->stream = op->copy_stream;
+        btg_status st = BTG_OK;
+        for (size_t r = 0; r < nrhs && st == BTG_OK; ++r)
+            st = run_r2c_vec(op, op->hin + (r * nm + j0) * nt, nc, op->wa + r * nm + j0, nrhs * nm);
+        op->stream = main;
+        BTG_TRY(st);
+        BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
+        BTG_CUDA(cudaStreamWaitEvent(op->stream, op->ev[c], 0));
+        BTG_TRY(zgemm_range(op, false, nrhs, j0, nc, c > 0));
+    }
+    count_apply_mrhs(op, nrhs);
+    return BTG_OK;
+}
+
+// d-hat spectra (nrhs stacked) in op->wa -> m (host) through chunked adjoint
+// ZGEMM + C2R + 2-D D2H.
+btg_status host_adjoint_stage_mrhs(btg_op op, double* m_host, size_t nrhs, const btg::C2REpilogue& epi) {
+    BTG_TRY(ensure_copy_stream(op));
+    const size_t nt = op->nt, nm = op->nm, pitch = nm * nt * sizeof(double);
+    const auto plan = mrhs_chunks(nm);
+    {
+        StageClock clk(op, &op->counters.apply);
+        for (size_t c = 0; c < plan.size(); ++c) {
+            const auto [j0, nc] = plan[c];
+            BTG_TRY(zgemm_range(op, true, nrhs, j0, nc, false));
+            for (size_t r = 0; r < nrhs; ++r)
+                BTG_TRY(run_c2r_vec(op, op->wb + r * nm + j0, nc, op->hout + (r * nm + j0) * nt,
+                                    chunk_epilogue(epi, j0, nt, (r * nm + j0) * nt), nrhs * nm));
+            BTG_CUDA(cudaEventRecord(op->ev[c], op->stream));
+        }
+    }
+    count_apply_mrhs(op, nrhs);
+    for (size_t c = 0; c < plan.size(); ++c) {
+        const auto [j0, nc] = plan[c];
+        BTG_CUDA(cudaStreamWaitEvent(op->copy_stream, op->ev[c], 0));
+        BTG_CUDA(cudaMemcpy2DAsync(m_host + j0 * nt, pitch, op->hout + j0 * nt, pitch, nc * nt * sizeof(double), nrhs,
+                                   cudaMemcpyDeviceToHost, op->copy_stream));
     }
     BTG_CUDA(cudaStreamSynchronize(op->copy_stream));
     BTG_CUDA(cudaStreamSynchronize(op->stream));
@@ -606,9 +708,10 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
     double* dout_p = out;
     const bool host = !(flags & BTG_DEVICE_PTRS);
     const bool chunked = host && host_pipelined(op, nrhs);
+    const bool mchunked = host && host_pipelined_mrhs(op, nrhs);
     if (host) {
         BTG_TRY(host_buffers(op, in_len, out_len));
-        if (!(chunked && !adjoint))  // the chunked forward streams its input itself
+        if (!((chunked || mchunked) && !adjoint))  // the chunked forward streams its input itself
             BTG_CUDA(cudaMemcpyAsync(op->hin, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         din_p = op->hin;
         dout_p = op->hout;
@@ -644,6 +747,16 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
         BTG_TRY(ensure_spectral(op, 1));
         BTG_TRY(run_r2c_vec(op, din_p, op->nd, op->wa));
         return host_adjoint_stage(op, out, epi);
+    }
+    if (mchunked && !adjoint) {
+        BTG_TRY(host_forward_stage_mrhs(op, in, nrhs));
+        BTG_TRY(run_c2r_vec(op, op->wb, nrhs * op->nd, dout_p, epi));
+        return finish_host(op, out, dout_p, out_len, flags);
+    }
+    if (mchunked && adjoint) {
+        BTG_TRY(ensure_spectral(op, nrhs));
+        BTG_TRY(run_r2c_vec(op, din_p, nrhs * op->nd, op->wa));
+        return host_adjoint_stage_mrhs(op, out, nrhs, epi);
     }
     BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, epi));
     return finish_host(op, out, dout_p, out_len, flags);
@@ -1032,9 +1145,10 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
     const double* vd = v;
     double* hvd = hv;
     const bool chunked = !(flags & BTG_DEVICE_PTRS) && host_pipelined(op, nrhs);
+    const bool mchunked = !(flags & BTG_DEVICE_PTRS) && host_pipelined_mrhs(op, nrhs);
     if (!(flags & BTG_DEVICE_PTRS)) {
         BTG_TRY(host_buffers(op, v_len, hv_len));
-        if (!chunked)
+        if (!chunked && !mchunked)
             BTG_CUDA(cudaMemcpyAsync(op->hin, v, v_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         vd = op->hin;
         hvd = op->hout;
@@ -1074,6 +1188,12 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
         BTG_TRY(run_c2r_vec(op, op->wb, op->nd, op->wt, e1));
         BTG_TRY(run_r2c_vec(op, op->wt, op->nd, op->wa));
         return host_adjoint_stage(op, hv, e2);
+    }
+    if (mchunked) {
+        BTG_TRY(host_forward_stage_mrhs(op, v, nrhs));
+        BTG_TRY(run_c2r_vec(op, op->wb, nrhs * op->nd, op->wt, e1));
+        BTG_TRY(run_r2c_vec(op, op->wt, nrhs * op->nd, op->wa));
+        return host_adjoint_stage_mrhs(op, hv, nrhs, e2);
     }
     BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
     BTG_TRY(pipeline(op, true, op->wt, hvd, nrhs, e2));

@@ -138,6 +138,12 @@ cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* m
                      int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream,
                      const int16_t* vexp = nullptr, int vexp_cpb = 1);
 
+// 3M kernels active (BTG_ZGEMM_4M unset): column ranges [j0, j0 + nj) supported.
+bool zgemm_3m();
+cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,
+                                   int nrhs, int j0, int nj, bool accumulate, cudaStream_t stream);
+cudaError_t launch_zgemm_adj_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,
+                                   int nrhs, int j0, int nj, cudaStream_t stream);
 cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream);
 cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,

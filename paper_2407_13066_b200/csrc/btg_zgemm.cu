@@ -317,7 +317,7 @@ __device__ __forceinline__ void mma3(double (&p1)[2][2][4], double (&p2)[2][2][4
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_zgemm3m_fwd(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
-                  int nm, int nrhs) {
+                  int nm, int nrhs, int j0, int nj, bool accumulate) {
     extern __shared__ __align__(16) double sm[];
     const int f = blockIdx.y;
     const int m0 = blockIdx.x * kTileM;
@@ -339,16 +339,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < (kTileM * kFwdKc) / kThreads; ++q) {
             const int idx = threadIdx.x + q * kThreads;
             const int row = idx / kFwdKc, col = idx % kFwdKc;
-            const int gi = m0 + row, gj = kc + col;
-            const bool ok = gi < nd && gj < nm;
+            const int gi = m0 + row, gj = j0 + kc + col;
+            const bool ok = gi < nd && kc + col < nj;
             cp_async16(As + row * kF3AStride + 2 * col, Ff + (size_t)(ok ? gi : 0) * nm + (ok ? gj : 0), ok);
         }
 #pragma unroll
         for (int q = 0; q < (kTileR * kFwdKc) / kThreads; ++q) {
             const int idx = threadIdx.x + q * kThreads;
             const int r = idx / kFwdKc, col = idx % kFwdKc;
-            const int gr = r0 + r, gj = kc + col;
-            const bool ok = gr < nrhs && gj < nm;
+            const int gr = r0 + r, gj = j0 + kc + col;
+            const bool ok = gr < nrhs && kc + col < nj;
             cp_async16(Bs + r * kM3BStride + col, Xf + (size_t)(ok ? gr : 0) * nm + (ok ? gj : 0), ok);
         }
     };
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) p1[a][b][c] = p2[a][b][c] = p3[a][b][c] = 0.0;
 
-    const int nk = (nm + kFwdKc - 1) / kFwdKc;
+    const int nk = (nj + kFwdKc - 1) / kFwdKc;
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) {
         if (s < nk) load_stage(s, s * kFwdKc);
@@ -408,19 +408,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int h = 0; h < 2; ++h) {
                     const int row = m0 + wm * 32 + mt * 16 + h * 8 + g;
                     const int c = 2 * h + q;
-                    if (row < nd)
-                        yr[row] = make_double2(p1[mt][nt][c] - p2[mt][nt][c],
-                                               p3[mt][nt][c] - p1[mt][nt][c] - p2[mt][nt][c]);
+                    if (row < nd) {
+                        double2 v = make_double2(p1[mt][nt][c] - p2[mt][nt][c],
+                                                 p3[mt][nt][c] - p1[mt][nt][c] - p2[mt][nt][c]);
+                        if (accumulate) {  // column-chunk partial sums, added in chunk order
+                            const double2 o = yr[row];
+                            v.x += o.x;
+                            v.y += o.y;
+                        }
+                        yr[row] = v;
+                    }
                 }
             }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_zgemm3m_adj(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
-                  int nm, int nrhs) {
+                  int nm, int nrhs, int jbase, int jend) {
     extern __shared__ __align__(16) double sm[];
     const int f = blockIdx.y;
-    const int j0 = blockIdx.x * kTileM;
+    const int j0 = jbase + blockIdx.x * kTileM;
     const int r0 = blockIdx.z * kTileR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int idx = threadIdx.x + q * kThreads;
             const int ii = idx / kTileM, jj = idx % kTileM;
             const int gi = kc + ii, gj = j0 + jj;
-            const bool ok = gi < nd && gj < nm;
+            const bool ok = gi < nd && gj < jend;
             cp_async16(As + ii * kA3AStride + jj, Ff + (size_t)(ok ? gi : 0) * nm + (ok ? gj : 0), ok);
         }
 #pragma unroll
@@ -505,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int h = 0; h < 2; ++h) {
                     const int jj = j0 + wm * 32 + mt * 16 + h * 8 + g;
                     const int c = 2 * h + q;
-                    if (jj < nm)
+                    if (jj < jend)
                         yr[jj] = make_double2(p1[mt][nt][c] + p2[mt][nt][c],
                                               p3[mt][nt][c] - p1[mt][nt][c] + p2[mt][nt][c]);
                 }
@@ -526,36 +533,58 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
-                             cudaStream_t stream) {
+bool zgemm_3m() { return !use_4m(); }
+
+cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,
+                                   int nrhs, int j0, int nj, bool accumulate, cudaStream_t stream) {
+    if (use_4m() && (j0 != 0 || nj != nm || accumulate)) return cudaErrorNotSupported;
     const bool m4 = use_4m();
-    const auto kern = m4 ? k_zgemm_fwd : k_zgemm3m_fwd;
     const size_t smem = kStages * (m4 ? kFwdStageDoubles : kF3StageDoubles) * sizeof(double);
-    cudaError_t e = set_smem(kern, smem);
+    cudaError_t e = m4 ? set_smem(k_zgemm_fwd, smem) : set_smem(k_zgemm3m_fwd, smem);
     if (e != cudaSuccess) return e;
     for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
         const int nb = std::min(kMaxGridY, nf - f0);
         dim3 grid((nd + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
-        kern<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nm,
-                                               Y + (size_t)f0 * nrhs * nd, nd, nm, nrhs);
+        const double2* Fb = F + (size_t)f0 * nd * nm;
+        const double2* Xb = X + (size_t)f0 * nrhs * nm;
+        double2* Yb = Y + (size_t)f0 * nrhs * nd;
+        if (m4)
+            k_zgemm_fwd<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs);
+        else
+            k_zgemm3m_fwd<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, nj, accumulate);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zgemm_fwd(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
+                             cudaStream_t stream) {
+    return launch_zgemm_fwd_range(F, X, Y, nf, nd, nm, nrhs, 0, nm, false, stream);
+}
+
+cudaError_t launch_zgemm_adj_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,
+                                   int nrhs, int j0, int nj, cudaStream_t stream) {
+    if (use_4m() && (j0 != 0 || nj != nm)) return cudaErrorNotSupported;
+    const bool m4 = use_4m();
+    const size_t smem = kStages * (m4 ? kAdjStageDoubles : kA3StageDoubles) * sizeof(double);
+    cudaError_t e = m4 ? set_smem(k_zgemm_adj, smem) : set_smem(k_zgemm3m_adj, smem);
+    if (e != cudaSuccess) return e;
+    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {
+        const int nb = std::min(kMaxGridY, nf - f0);
+        dim3 grid((nj + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
+        const double2* Fb = F + (size_t)f0 * nd * nm;
+        const double2* Xb = X + (size_t)f0 * nrhs * nd;
+        double2* Yb = Y + (size_t)f0 * nrhs * nm;
+        if (m4)
+            k_zgemm_adj<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs);
+        else
+            k_zgemm3m_adj<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, j0 + nj);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_zgemm_adj(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
                              cudaStream_t stream) {
-    const bool m4 = use_4m();
-    const auto kern = m4 ? k_zgemm_adj : k_zgemm3m_adj;
-    const size_t smem = kStages * (m4 ? kAdjStageDoubles : kA3StageDoubles) * sizeof(double);
-    cudaError_t e = set_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-    for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {
-        const int nb = std::min(kMaxGridY, nf - f0);
-        dim3 grid((nm + kTileM - 1) / kTileM, nb, (nrhs + kTileR - 1) / kTileR);
-        kern<<<grid, kThreads, smem, stream>>>(F + (size_t)f0 * nd * nm, X + (size_t)f0 * nrhs * nd,
-                                               Y + (size_t)f0 * nrhs * nm, nd, nm, nrhs);
-    }
-    return cudaGetLastError();
+    return launch_zgemm_adj_range(F, X, Y, nf, nd, nm, nrhs, 0, nm, stream);
 }
 
 }  // namespace btg
