@@ -115,6 +115,8 @@ struct btg_op_s {
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
     cudaEvent_t ev[17] = {};              // kHostChunks + 1 chunk / ordering events
+    cudaStream_t fft_stream = nullptr;   // chunk R2Cs of host-pointer forward calls
+    cudaEvent_t ev_h2d[17] = {};          // chunk H2D done (copy stream -> fft stream)
     cudaStream_t stream = nullptr;
 
     // workspace (grown on demand)
@@ -450,11 +452,22 @@ bool host_pipelined(btg_op op, size_t nrhs) {
 // ramp did (CUPTI timeline, profiles/tools/host_timeline.py; 33.5 -> 33.2 ms per
 // configs[1] e2e step). At most kHostChunks chunks (wider N_m: the ramp, then
 // equal chunks). BTG_HOST_RAMP (percent) is a tuning knob.
+//
+// When the copies are not the faster side (FP32 F-hat, small N_d: a chunk GEMV
+// costs about what its copy does or less) the copy stream is the critical path
+// and a ramp only adds small, inefficient GEMVs: equal chunks instead (FP32
+// configs[1]: a mirrored ramp measured F 6.43 ms, the x2 ramp 5.85).
+std::vector<std::pair<size_t, size_t>> mrhs_chunks(size_t nm);
+
 std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
     static const double growth = [] {
         const char* s = std::getenv("BTG_HOST_RAMP");
         return s ? std::max(1.1, std::strtod(s, nullptr) / 100.0) : 1.5;
     }();
+    // chunk GEMV ~6.5 TB/s (FP32 measured ~6 TB/s), PCIe ~55 GB/s
+    const double gemv_col = (double)op->F_elem * op->nd * op->nf / 6.5e12;
+    const double pcie_col = 8.0 * op->nt / 55.0e9;
+    if (gemv_col < 1.2 * pcie_col) return mrhs_chunks(op->nm);
     const size_t nm = op->nm;
     std::vector<double> geo;
     double sum = 0.0;
@@ -497,8 +510,11 @@ std::vector<std::pair<size_t, size_t>> chunk_plan(btg_op op, bool ramp_first) {
 
 btg_status ensure_copy_stream(btg_op op) {
     if (!op->copy_stream) BTG_CUDA(cudaStreamCreateWithFlags(&op->copy_stream, cudaStreamNonBlocking));
-    for (size_t c = 0; c <= kHostChunks; ++c)
+    if (!op->fft_stream) BTG_CUDA(cudaStreamCreateWithFlags(&op->fft_stream, cudaStreamNonBlocking));
+    for (size_t c = 0; c <= kHostChunks; ++c) {
         if (!op->ev[c]) BTG_CUDA(cudaEventCreateWithFlags(&op->ev[c], cudaEventDisableTiming));
+        if (!op->ev_h2d[c]) BTG_CUDA(cudaEventCreateWithFlags(&op->ev_h2d[c], cudaEventDisableTiming));
+    }
     return BTG_OK;
 }
 
@@ -537,16 +553,19 @@ btg_status host_forward_stage(btg_op op, const double* m_host) {
         const auto [j0, nc] = plan[c];
         BTG_CUDA(cudaMemcpyAsync(op->hin + j0 * nt, m_host + j0 * nt, nc * nt * sizeof(double),
                                  cudaMemcpyHostToDevice, op->copy_stream));
-        // the chunk's R2C runs on the copy stream behind its H2D, so it overlaps the
-        // previous chunk's GEMV instead of sitting between GEMVs on the compute stream
+        BTG_CUDA(cudaEventRecord(op->ev_h2d[c], op->copy_stream));
+        // the chunk's R2C runs on its own stream behind its H2D, so it overlaps the
+        // previous chunk's GEMV instead of sitting between GEMVs on the compute
+        // stream, and never holds up the next H2D while it waits for SMs
+        BTG_CUDA(cudaStreamWaitEvent(op->fft_stream, op->ev_h2d[c], 0));
         {
             cudaStream_t main = op->stream;
-            op->stream = op->copy_stream;
+            op->stream = op->fft_stream;
             const btg_status st = run_r2c_vec(op, op->hin + j0 * nt, nc, op->wa + j0, op->nm);
             op->stream = main;
             BTG_TRY(st);
         }
-        BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
+        BTG_CUDA(cudaEventRecord(op->ev[c], op->fft_stream));
         BTG_CUDA(cudaStreamWaitEvent(op->stream, op->ev[c], 0));
         BTG_TRY(gemv_range(op, false, op->wa, op->wb, j0, nc, c > 0));
     }
@@ -640,14 +659,16 @@ btg_status host_forward_stage_mrhs(btg_op op, const double* m_host, size_t nrhs)
         const auto [j0, nc] = plan[c];
         BTG_CUDA(cudaMemcpy2DAsync(op->hin + j0 * nt, pitch, m_host + j0 * nt, pitch, nc * nt * sizeof(double), nrhs,
                                    cudaMemcpyHostToDevice, op->copy_stream));
+        BTG_CUDA(cudaEventRecord(op->ev_h2d[c], op->copy_stream));
+        BTG_CUDA(cudaStreamWaitEvent(op->fft_stream, op->ev_h2d[c], 0));
         cudaStream_t main = op->stream;
-        op->stream = op->copy_stream;
+        op->stream = op->fft_stream;
         btg_status st = BTG_OK;
         for (size_t r = 0; r < nrhs && st == BTG_OK; ++r)
             st = run_r2c_vec(op, op->hin + (r * nm + j0) * nt, nc, op->wa + r * nm + j0, nrhs * nm);
         op->stream = main;
         BTG_TRY(st);
-        BTG_CUDA(cudaEventRecord(op->ev[c], op->copy_stream));
+        BTG_CUDA(cudaEventRecord(op->ev[c], op->fft_stream));
         BTG_CUDA(cudaStreamWaitEvent(op->stream, op->ev[c], 0));
         BTG_TRY(zgemm_range(op, false, nrhs, j0, nc, c > 0));
     }
@@ -1651,7 +1672,13 @@ void btg_destroy(btg_op op) {
             cudaStreamSynchronize(op->copy_stream);
             cudaStreamDestroy(op->copy_stream);
         }
+        if (op->fft_stream) {
+            cudaStreamSynchronize(op->fft_stream);
+            cudaStreamDestroy(op->fft_stream);
+        }
         for (cudaEvent_t e : op->ev)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : op->ev_h2d)
             if (e) cudaEventDestroy(e);
     }
     delete op;

@@ -14,7 +14,7 @@ import bench  # noqa: E402
 import paper_2407_13066_b200 as btg  # noqa: E402
 from paper_2407_13066_b200 import _lib  # noqa: E402
 
-cfg = bench.CONFIGS[os.environ.get("CFG", "B")]
+cfg = dict(bench.CONFIGS[os.environ.get("CFG", "B")], precision=int(os.environ.get("PREC", "64")))
 nt, nd, nm = cfg["nt"], cfg["nd"], cfg["nm"]
 op = bench.build_operator(cfg, 0, seed=1000)
 m = torch.empty((nm, nt), dtype=torch.float64, device="cuda:0")
