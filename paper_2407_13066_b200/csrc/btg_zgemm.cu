@@ -315,7 +315,8 @@ __device__ __forceinline__ void mma3(double (&p1)[2][2][4], double (&p2)[2][2][4
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int ST, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_zgemm3m_fwd(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
                   int nm, int nrhs, int j0, int nj, bool accumulate) {
     extern __shared__ __align__(16) double sm[];
@@ -363,20 +364,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int nk = (nj + kFwdKc - 1) / kFwdKc;
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < ST - 1; ++s) {
         if (s < nk) load_stage(s, s * kFwdKc);
         cp_async_commit();
     }
     for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait<kStages - 2>();
+        cp_async_wait<ST - 2>();
         __syncthreads();
         {
-            const int nxt = kt + kStages - 1;
-            if (nxt < nk) load_stage(nxt % kStages, nxt * kFwdKc);
+            const int nxt = kt + ST - 1;
+            if (nxt < nk) load_stage(nxt % ST, nxt * kFwdKc);
             cp_async_commit();
         }
-        const double* As = stage_a(kt % kStages);
-        const double2* Bs = stage_b(kt % kStages);
+        const double* As = stage_a(kt % ST);
+        const double2* Bs = stage_b(kt % ST);
 #pragma unroll
         for (int ks = 0; ks < kFwdKc / 4; ++ks) {
             const int kk = ks * 4 + tig;  // complex k of this lane's A column / B row
@@ -422,7 +423,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int ST, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_zgemm3m_adj(const double2* __restrict__ F, const double2* __restrict__ X, double2* __restrict__ Y, int nd,
                   int nm, int nrhs, int jbase, int jend) {
     extern __shared__ __align__(16) double sm[];
@@ -470,20 +472,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int nk = (nd + kAdjKc - 1) / kAdjKc;
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < ST - 1; ++s) {
         if (s < nk) load_stage(s, s * kAdjKc);
         cp_async_commit();
     }
     for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait<kStages - 2>();
+        cp_async_wait<ST - 2>();
         __syncthreads();
         {
-            const int nxt = kt + kStages - 1;
-            if (nxt < nk) load_stage(nxt % kStages, nxt * kAdjKc);
+            const int nxt = kt + ST - 1;
+            if (nxt < nk) load_stage(nxt % ST, nxt * kAdjKc);
             cp_async_commit();
         }
-        const double2* As = stage_a(kt % kStages);
-        const double2* Bs = stage_b(kt % kStages);
+        const double2* As = stage_a(kt % ST);
+        const double2* Bs = stage_b(kt % ST);
 #pragma unroll
         for (int ks = 0; ks < kAdjKc / 4; ++ks) {
             const int kk = ks * 4 + tig;  // complex i of this lane's A column / B row
@@ -539,8 +541,11 @@ cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* 
                                    int nrhs, int j0, int nj, bool accumulate, cudaStream_t stream) {
     if (use_4m() && (j0 != 0 || nj != nm || accumulate)) return cudaErrorNotSupported;
     const bool m4 = use_4m();
-    const size_t smem = kStages * (m4 ? kFwdStageDoubles : kF3StageDoubles) * sizeof(double);
-    cudaError_t e = m4 ? set_smem(k_zgemm_fwd, smem) : set_smem(k_zgemm3m_fwd, smem);
+    // 2 CTAs per SM (<= 128 registers, 2 stages), as the adjoint: 15.0 -> 13.7 ms at
+    // configs[3] (1 CTA x 4 stages), despite 3.5 instead of 6.9 waves.
+    const auto k3 = k_zgemm3m_fwd<2, 2>;
+    const size_t smem = (m4 ? kStages * kFwdStageDoubles : 2 * kF3StageDoubles) * sizeof(double);
+    cudaError_t e = m4 ? set_smem(k_zgemm_fwd, smem) : set_smem(k3, smem);
     if (e != cudaSuccess) return e;
     for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {  // grid.y limit: long horizons go in frequency batches
         const int nb = std::min(kMaxGridY, nf - f0);
@@ -551,7 +556,7 @@ cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* 
         if (m4)
             k_zgemm_fwd<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs);
         else
-            k_zgemm3m_fwd<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, nj, accumulate);
+            k3<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, nj, accumulate);
     }
     return cudaGetLastError();
 }
@@ -565,8 +570,12 @@ cudaError_t launch_zgemm_adj_range(const double2* F, const double2* X, double2* 
                                    int nrhs, int j0, int nj, cudaStream_t stream) {
     if (use_4m() && (j0 != 0 || nj != nm)) return cudaErrorNotSupported;
     const bool m4 = use_4m();
-    const size_t smem = kStages * (m4 ? kAdjStageDoubles : kA3StageDoubles) * sizeof(double);
-    cudaError_t e = m4 ? set_smem(k_zgemm_adj, smem) : set_smem(k_zgemm3m_adj, smem);
+    // 2 CTAs per SM (<= 128 registers, 2 stages): one CTA's prologue / epilogue
+    // overlaps the other's MMAs; K = N_d is short (configs[3]: 8 stages per tile).
+    // Measured 16.3 -> 14.1 ms at configs[3] (1 CTA x 4 stages before).
+    const auto k3 = k_zgemm3m_adj<2, 2>;
+    const size_t smem = (m4 ? kStages * kAdjStageDoubles : 2 * kA3StageDoubles) * sizeof(double);
+    cudaError_t e = m4 ? set_smem(k_zgemm_adj, smem) : set_smem(k3, smem);
     if (e != cudaSuccess) return e;
     for (int f0 = 0; f0 < nf; f0 += kMaxGridY) {
         const int nb = std::min(kMaxGridY, nf - f0);
@@ -577,7 +586,7 @@ cudaError_t launch_zgemm_adj_range(const double2* F, const double2* X, double2* 
         if (m4)
             k_zgemm_adj<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs);
         else
-            k_zgemm3m_adj<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, j0 + nj);
+            k3<<<grid, kThreads, smem, stream>>>(Fb, Xb, Yb, nd, nm, nrhs, j0, j0 + nj);
     }
     return cudaGetLastError();
 }
