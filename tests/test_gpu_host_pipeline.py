@@ -18,11 +18,11 @@ def btg():
     return m
 
 
-@pytest.mark.parametrize("nm", [4096, 5000, 9000])
-def test_chunked_host_path_matches_device_path(btg, nm):
+@pytest.mark.parametrize("nm,nt", [(4096, 64), (5000, 64), (9000, 64), (4100, 15)])
+def test_chunked_host_path_matches_device_path(btg, nm, nt):
     import torch
 
-    nd, nt = 7, 64
+    nd = 7
     blocks, m, d = R.random_problem(1300 + nm, nd, nm, nt)
     spec = R.setup_full(blocks)
     gam = np.linspace(0.5, 2.0, nd)
@@ -74,15 +74,15 @@ def test_chunked_adjoint_gamma_epilogue_offsets(btg, kind):
     assert R.rel_l2(out, want) <= 1e-12
 
 
-@pytest.mark.parametrize("nrhs", [3, 33])
-def test_chunked_multi_rhs_host_path(btg, nrhs):
+@pytest.mark.parametrize("nrhs,nt", [(3, 16), (33, 16), (4, 15)])
+def test_chunked_multi_rhs_host_path(btg, nrhs, nt):
     """Multi-RHS host calls (3M ZGEMM engine) stream column chunks as 2-D copies
     with the ZGEMM K-partials accumulated chunk by chunk: parity with the oracle
     and with the device-pointer path, epilogues included (ragged chunk, two RHS
     tiles at 33)."""
     import torch
 
-    nd, nm, nt = 20, 4500, 16
+    nd, nm = 20, 4500  # nt = 15: odd rows, the generic (unaligned) FFT path
     blocks, _, _ = R.random_problem(1600 + nrhs, nd, nm, nt)
     spec = R.setup_full(blocks)
     rng = np.random.default_rng(nrhs)
