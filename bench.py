@@ -100,7 +100,7 @@ def hbm_peak():
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,clocks.mem")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -143,7 +143,7 @@ class ClockSampler:
             rows = [ln.split(",") for ln in (lines[self.skip:] or lines[-1:])]
         except Exception:
             return None
-        sm, mx, reasons = [], [], set()
+        sm, mx, mem, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             r = [x.strip() for x in r]
@@ -157,10 +157,17 @@ class ClockSampler:
             for name, val in zip(names, r[5:9]):
                 if val.lower().startswith("active"):
                     reasons.add(name)
+            try:
+                mem.append(float(r[9]))
+            except (IndexError, ValueError):
+                pass
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if mem:
+            out["mem_mhz"] = statistics.median(mem)
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -557,12 +564,13 @@ def run_ours(args):
             btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=1)  # warm
             torch.cuda.synchronize(device)
             c0, c1 = ev(), ev()
-            c0.record(stream)
-            _, it_done, _, _ = btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=iters)
-            c1.record(stream)
-            torch.cuda.synchronize(device)
+            with ClockSampler(device) as sclk:
+                c0.record(stream)
+                _, it_done, _, _ = btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=iters)
+                c1.record(stream)
+                torch.cuda.synchronize(device)
             ms_it = c0.elapsed_time(c1) / max(1, it_done)
-            solver = {"iterations": it_done, "ms_per_iteration": ms_it,
+            solver = {"iterations": it_done, "ms_per_iteration": ms_it, "clocks": sclk.summary(),
                       "TB/s": b["H"] / (ms_it * 1e-3) / 1e12,
                       "path": "btg_cg_solve (inverse.cpp:105-156 on the device): one F* F + alpha I per iteration"}
         except Exception as exc:

@@ -116,6 +116,9 @@ struct btg_op_s {
     cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
     cudaEvent_t ev[17] = {};              // kHostChunks + 1 chunk / ordering events
     cudaStream_t fft_stream = nullptr;   // chunk R2Cs of host-pointer forward calls
+    double* pinned_scalar = nullptr;     // page-locked landing slot for solver scalars
+    double* solver_ws[11] = {};           // CG / objective vectors, kept across calls
+    size_t solver_cap[11] = {};
     cudaEvent_t ev_h2d[17] = {};          // chunk H2D done (copy stream -> fft stream)
     cudaStream_t stream = nullptr;
 
@@ -1300,22 +1303,38 @@ btg_status btg_internal_mark_ready(btg_op op) {
 // ---------------------------------------------------------------------------
 namespace {
 
+// Solver / objective vectors live in per-handle slots grown on demand and kept
+// across calls: a cudaMalloc + cudaFree of several N_m x N_t vectors per solve
+// cost tens to hundreds of milliseconds at configs[1] (measured: 20-iteration
+// solves at 17 to 57 ms per iteration with per-call allocation, the Hessian
+// itself 16 ms).
+enum CgSlot { kSlotX, kSlotR, kSlotZ, kSlotP, kSlotHp, kSlotPartial, kSlotScal, kSlotPivot, kSlotScratch,
+              kSlotRhs, kSlotGam };
 struct CgBuffers {
     double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *hp = nullptr, *partial = nullptr,
            *scal = nullptr, *pivot = nullptr, *scratch = nullptr, *rhs = nullptr, *gam = nullptr;
-    ~CgBuffers() {
-        for (double* q : {x, r, z, p, hp, partial, scal, pivot, scratch, rhs, gam}) cudaFree(q);
-    }
 };
 
-btg_status alloc(double** p, size_t n) {
-    BTG_CUDA(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(double)));
+// The slots outlive the call: every exit (errors included) drains the handle's
+// stream, so a later call on another stream never races work still in flight.
+struct DrainOnExit {
+    btg_op op;
+    ~DrainOnExit() { cudaStreamSynchronize(op->stream); }
+};
+
+btg_status slot(btg_op op, CgSlot k, double** p, size_t n) {
+    BTG_TRY(grow(op->solver_ws[k], op->solver_cap[k], std::max<size_t>(n, 1)));
+    *p = op->solver_ws[k];
     return BTG_OK;
 }
 
+// Solver scalars land in page-locked memory (a direct DMA instead of the
+// driver's pageable staging path).
 btg_status read_scalar(btg_op op, const double* dev, double* host) {
-    BTG_CUDA(cudaMemcpyAsync(host, dev, sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+    if (!op->pinned_scalar) BTG_CUDA(cudaMallocHost(&op->pinned_scalar, sizeof(double)));
+    BTG_CUDA(cudaMemcpyAsync(op->pinned_scalar, dev, sizeof(double), cudaMemcpyDeviceToHost, op->stream));
     BTG_CUDA(cudaStreamSynchronize(op->stream));
+    *host = *op->pinned_scalar;
     return BTG_OK;
 }
 
@@ -1364,22 +1383,23 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
     cudaEventRecord(t0, op->stream);
 
     CgBuffers b;
+    DrainOnExit drain{op};
     const bool dev = flags & BTG_DEVICE_PTRS;
-    BTG_TRY(alloc(&b.r, n));
-    BTG_TRY(alloc(&b.p, n));
-    BTG_TRY(alloc(&b.hp, n));
-    BTG_TRY(alloc(&b.partial, btg::kRedBlocks));
-    BTG_TRY(alloc(&b.scal, 4));
+    BTG_TRY(slot(op, kSlotR, &b.r, n));
+    BTG_TRY(slot(op, kSlotP, &b.p, n));
+    BTG_TRY(slot(op, kSlotHp, &b.hp, n));
+    BTG_TRY(slot(op, kSlotPartial, &b.partial, btg::kRedBlocks));
+    BTG_TRY(slot(op, kSlotScal, &b.scal, 4));
     const bool precond = use_reg_preconditioner != 0;
-    if (precond) BTG_TRY(alloc(&b.z, n));
+    if (precond) BTG_TRY(slot(op, kSlotZ, &b.z, n));
     double* x = dev ? x_out : nullptr;
     if (!dev) {
-        BTG_TRY(alloc(&b.x, n));
+        BTG_TRY(slot(op, kSlotX, &b.x, n));
         x = b.x;
     }
     const double* rhs_d = rhs;
     if (!dev) {
-        BTG_TRY(alloc(&b.rhs, n));
+        BTG_TRY(slot(op, kSlotRhs, &b.rhs, n));
         BTG_CUDA(cudaMemcpyAsync(b.rhs, rhs, n * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         rhs_d = b.rhs;
     }
@@ -1388,7 +1408,7 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
         const size_t glen = gamma_kind == BTG_GAMMA_PER_SENSOR ? op->nd : op->nd * op->nt;
         gd = gamma_inv;
         if (!dev) {
-            BTG_TRY(alloc(&b.gam, glen));
+            BTG_TRY(slot(op, kSlotGam, &b.gam, glen));
             BTG_CUDA(cudaMemcpyAsync(b.gam, gamma_inv, glen * sizeof(double), cudaMemcpyHostToDevice, op->stream));
             gd = b.gam;
         }
@@ -1404,8 +1424,8 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
             pivot = 2.0 + scr[t];
             piv[t] = pivot;
         }
-        BTG_TRY(alloc(&b.pivot, op->nt));
-        BTG_TRY(alloc(&b.scratch, op->nt));
+        BTG_TRY(slot(op, kSlotPivot, &b.pivot, op->nt));
+        BTG_TRY(slot(op, kSlotScratch, &b.scratch, op->nt));
         BTG_CUDA(cudaMemcpyAsync(b.pivot, piv.data(), op->nt * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         BTG_CUDA(cudaMemcpyAsync(b.scratch, scr.data(), op->nt * sizeof(double), cudaMemcpyHostToDevice,
                                  op->stream));
@@ -1502,21 +1522,22 @@ btg_status btg_objective(btg_op op, const double* m, size_t m_len, const double*
     BTG_TRY(check_len("objective", m_len, op->nm, op->nt, 1, op->nm));
     DeviceGuard g(op->device);
     CgBuffers b;
+    DrainOnExit drain{op};
     const bool dev = flags & BTG_DEVICE_PTRS;
     const double* md = m;
     const double* dd = d_obs;
     if (!dev) {
-        BTG_TRY(alloc(&b.x, m_len));
-        BTG_TRY(alloc(&b.rhs, d_len));
+        BTG_TRY(slot(op, kSlotX, &b.x, m_len));
+        BTG_TRY(slot(op, kSlotRhs, &b.rhs, d_len));
         BTG_CUDA(cudaMemcpyAsync(b.x, m, m_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         BTG_CUDA(cudaMemcpyAsync(b.rhs, d_obs, d_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
         md = b.x;
         dd = b.rhs;
     }
-    BTG_TRY(alloc(&b.r, d_len));
-    BTG_TRY(alloc(&b.p, m_len));
-    BTG_TRY(alloc(&b.partial, btg::kRedBlocks));
-    BTG_TRY(alloc(&b.scal, 1));
+    BTG_TRY(slot(op, kSlotR, &b.r, d_len));
+    BTG_TRY(slot(op, kSlotP, &b.p, m_len));
+    BTG_TRY(slot(op, kSlotPartial, &b.partial, btg::kRedBlocks));
+    BTG_TRY(slot(op, kSlotScal, &b.scal, 1));
     BTG_TRY(pipeline(op, false, md, b.r, 1, btg::C2REpilogue{}));
     BTG_CUDA(btg::launch_sub(b.r, b.r, dd, d_len, op->stream));
     double misfit = 0.0, reg = 0.0;
@@ -1676,6 +1697,8 @@ void btg_destroy(btg_op op) {
             cudaStreamSynchronize(op->fft_stream);
             cudaStreamDestroy(op->fft_stream);
         }
+        if (op->pinned_scalar) cudaFreeHost(op->pinned_scalar);
+        for (double* q : op->solver_ws) cudaFree(q);
         for (cudaEvent_t e : op->ev)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : op->ev_h2d)
