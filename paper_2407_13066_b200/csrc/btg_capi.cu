@@ -1377,9 +1377,16 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
     if (max_iterations == 0)
         max_iterations = 10 * static_cast<size_t>(std::ceil(std::sqrt(static_cast<double>(n)))) + 1;
     *result = btg_cg_result{};
-    cudaEvent_t t0, t1;
-    cudaEventCreate(&t0);
-    cudaEventCreate(&t1);
+    struct Events {  // destroyed on every exit, early errors included
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        ~Events() {
+            if (t0) cudaEventDestroy(t0);
+            if (t1) cudaEventDestroy(t1);
+        }
+    } evs;
+    BTG_CUDA(cudaEventCreate(&evs.t0));
+    BTG_CUDA(cudaEventCreate(&evs.t1));
+    const cudaEvent_t t0 = evs.t0, t1 = evs.t1;
     cudaEventRecord(t0, op->stream);
 
     CgBuffers b;
@@ -1504,8 +1511,6 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     result->seconds = ms * 1e-3;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     return BTG_OK;
 }
 
