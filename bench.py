@@ -12,8 +12,15 @@ ranks; per-op milliseconds and TB/s are in ``ops``.
 
 N=1: configs[1] (N_t=1024, N_d=100, N_m=32768, FP64; F-hat 53.7 GB).
 N>1 (torchrun, one rank per GPU): configs[2] weak scaling, N_t=1000, N_d=600,
-N_m=8192 per GPU on a 1 x N grid with NCCL (row reduce for F, row broadcast
-for F*).
+N_m=8192 per GPU on an r x c grid (--grid RxC; default: the planner's
+weak-scaling pick, 1 x N for configs[2]) through libbtg's C++ grid engine with
+NCCL (column broadcast + row reduce for F, row broadcast + column reduce for
+F*, one row all-reduce inside the Hessian). torch.distributed (gloo) is only
+the plumbing: it ships the NCCL id, runs the barriers and takes the max over
+ranks. --config E: configs[4] strong scaling (global N_t=4096, N_d=256,
+N_m=65536 split over the grid; FP64 fits from 8 GPUs, --precision 32 from 4).
+BTG_BENCH_BACKEND=gloo hands the grid's collectives to gloo instead (host
+callbacks), so several ranks can share ONE GPU for a functional check.
 """
 
 from __future__ import annotations
@@ -52,6 +59,8 @@ CONFIGS = {
               label="paper long horizon (PAPER.md:912-938): N_t=10000 N_d=100 N_m=800 FP64 (F-hat 12.8 GB)"),
     "E4f32": dict(nt=4096, nd=256, nm=16384, nrhs=1, precision=32,
                   label="configs[4] per-GPU shard of the 1x4 grid, FP32 F-hat: N_t=4096 N_d=256 N_m=65536/4"),
+    "E": dict(nt=4096, nd=256, nm=65536, nrhs=1, strong=True,
+              label="configs[4]: strong scaling long horizon N_t=4096 N_d=256 N_m=65536 total over the grid"),
 }
 CPU_SAMPLE_NM = 2048  # N_m slice the CPU reference runs on (extrapolate linearly in N_m)
 
@@ -276,12 +285,12 @@ def run_ours(args):
     # refuses duplicate devices) — the driver's runs use NCCL, one GPU per rank
     device = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(device)
+    transport = os.environ.get("BTG_BENCH_BACKEND", "nccl")
     if world > 1:
-        backend = os.environ.get("BTG_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
-        else:
-            dist.init_process_group(backend)
+        # plumbing only (NCCL id, barriers, max over ranks); the data plane is
+        # libbtg's grid engine, whose NCCL communicators are then the only ones
+        # in the process (so its pinned NCCL_ALGO / NCCL_PROTO take effect)
+        dist.init_process_group("gloo")
     cfg = dict(CONFIGS["B" if world == 1 else "C"])
     if args.config:
         cfg = dict(CONFIGS[args.config])
@@ -295,28 +304,45 @@ def run_ours(args):
         log(f"[bench] probe: {probe}")
 
     t0 = time.perf_counter()
-    if world == 1:
+    shards = None
+    if world == 1 and not cfg.get("strong"):
         op = build_operator(cfg, device, seed=1000)
         engine = None
         grid = "1x1"
+        nd_g, nm_g = nd, nm
     else:
         from paper_2407_13066_b200 import distributed as bdist
 
-        # weak scaling at fixed per-GPU (N_d, N_m): the reference planner's rule
-        # (weak_scaling_shape, grid_planner.cpp:195-207) — 1 x p when N_d < N_m
-        _, (gr, gc) = btg.weak_scaling_shape(nd / nm, world)
-        engine = bdist.GridEngine.synthetic(nd * gr, nm * gc, nt, grid=(gr, gc), seed=1000)
+        if args.grid:
+            gr, gc = btg.parse_grid(args.grid)
+        elif cfg.get("strong"):
+            gr, gc = btg.select_grid(world, math.log10(nd / nm))
+        else:
+            # weak scaling at fixed per-GPU (N_d, N_m): the planner's rule
+            # (weak_scaling_shape, grid_planner.cpp:195-207) — 1 x p when N_d < N_m
+            _, (gr, gc) = btg.weak_scaling_shape(nd / nm, world)
+        if gr * gc != world:
+            raise SystemExit(f"--grid {gr}x{gc} needs {gr * gc} ranks, have {world}")
+        # weak scaling: the per-GPU shard is (N_d, N_m); strong: the global operator is fixed
+        nd_g, nm_g = (nd, nm) if cfg.get("strong") else (nd * gr, nm * gc)
+        shards = bdist.partition_bounds(nd_g, nm_g, gr, gc)
+        engine = bdist.GridEngine.synthetic(nd_g, nm_g, nt, grid=(gr, gc), seed=1000,
+                                            precision=cfg.get("precision", 64),
+                                            transport="gloo" if transport == "gloo" else "nccl")
         op = engine.local_op
         grid = f"{gr}x{gc}"
+        sh = engine.shard
+        nd, nm = sh.local_sensors, sh.local_sources  # this rank's shard
     setup_s = time.perf_counter() - t0
-    log(f"[bench] rank {rank}: setup {setup_s:.2f} s (F-hat {16 * (nt + 1) * nd * nm / 1e9:.2f} GB/GPU)")
+    log(f"[bench] rank {rank}: setup {setup_s:.2f} s (F-hat {16 * (nt + 1) * nd * nm / 1e9:.2f} GB/GPU, grid {grid})")
 
     stream = torch.cuda.current_stream(device)
     dev = f"cuda:{device}"
     vshape = (nm, nt) if nrhs == 1 else (nrhs, nm, nt)
     m = torch.empty(vshape, dtype=torch.float64, device=dev)
     btg.fill_uniform(m, seed=7)
-    gamma = torch.empty((nd,), dtype=torch.float64, device=dev)
+    # Gamma^-1 is GLOBAL (N_d of the whole operator); each grid cell uses its rows
+    gamma = torch.empty((nd_g,), dtype=torch.float64, device=dev)
     btg.fill_uniform(gamma, seed=8, lo=0.5, hi=2.0)
 
     if engine is None:
@@ -329,14 +355,19 @@ def run_ours(args):
         def do_h(x):
             return op.hessian_apply(x, gamma_inv=gamma)
     else:
+        sh = engine.shard
+        row0, col0 = sh.grid_row == 0, sh.grid_col == 0
+        d_in = torch.empty((nd, nt), dtype=torch.float64, device=dev)
+        btg.fill_uniform(d_in, seed=9)
+
         def do_f(x):
-            return engine.forward(x)
+            return engine.forward(x if row0 else None)
 
         def do_a(y):
-            return engine.adjoint(y)
+            return engine.adjoint(d_in if col0 else None)
 
         def do_h(x):
-            return engine.hessian(x, gamma_inv=gamma)
+            return engine.hessian(x if row0 else None, gamma_inv=gamma)
 
     d = do_f(m)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -351,7 +382,7 @@ def run_ours(args):
         mm = do_a(d)
         hv = do_h(m)
     barrier()
-    c0 = op.counters()["launches"]
+    c0 = op.counters()["launches"] if op is not None else 0
     evs = [(ev(), ev(), ev(), ev()) for _ in range(args.steps)]
     with ClockSampler(device) as clk:
         barrier()
@@ -369,7 +400,7 @@ def run_ours(args):
         stop.record(stream)
         barrier()
     clocks = clk.summary()
-    launches = op.counters()["launches"] - c0
+    launches = (op.counters()["launches"] - c0) if op is not None else 0
     total_ms = start.elapsed_time(stop)
     per = {"F": [], "F*": [], "H": []}
     for e in evs:
@@ -377,7 +408,7 @@ def run_ours(args):
         per["F*"].append(e[1].elapsed_time(e[2]))
         per["H"].append(e[2].elapsed_time(e[3]))
     if world > 1:
-        t = torch.tensor([total_ms] + [statistics.mean(per[k]) for k in ("F", "F*", "H")], device=dev)
+        t = torch.tensor([total_ms] + [statistics.mean(per[k]) for k in ("F", "F*", "H")])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t[0])
         per_mean = dict(zip(("F", "F*", "H"), (float(x) for x in t[1:])))
@@ -387,7 +418,13 @@ def run_ours(args):
     prec = cfg.get("precision", 64)
     b = alg_bytes(nt, nd, nm, nrhs, elem=16 if prec == 64 else 8)
     fl = alg_flops(nt, nd, nm, nrhs)
-    step_bytes = (b["F"] + b["F*"] + b["H"]) * world
+    if shards is None:
+        step_bytes = (b["F"] + b["F*"] + b["H"]) * world
+    else:  # sum over the grid's shards (ragged / empty shards included)
+        step_bytes = 0.0
+        for s_ in shards:
+            bb = alg_bytes(nt, s_.local_sensors, s_.local_sources, nrhs, elem=16 if prec == 64 else 8)
+            step_bytes += bb["F"] + bb["F*"] + bb["H"]
     value = step_bytes / (ms_step * 1e-3) / 1e12
     ops = {k: {"ms": per_mean[k], "TB/s": b[k] / (per_mean[k] * 1e-3) / 1e12,
                "frac_of_peak": b[k] / (per_mean[k] * 1e-3) / 1e9 / peak,
@@ -474,15 +511,13 @@ def run_ours(args):
         hm = torch.empty(vshape, dtype=torch.float64, pin_memory=True)
         hm.copy_(m.cpu())
         hd = torch.empty((nd, nt), dtype=torch.float64, pin_memory=True)
-        if d is not None:
-            hd.copy_(d.cpu())
+        hd.copy_(d_in.cpu())
         out_h = torch.empty(vshape, dtype=torch.float64, pin_memory=True)
         out_m = torch.empty(vshape, dtype=torch.float64, pin_memory=True)
         out_d = torch.empty((nd, nt), dtype=torch.float64, pin_memory=True)
-        col0 = engine.shard.grid_col == 0
 
         def e2e_step_grid():
-            mdev = hm.to(dev, non_blocking=True)
+            mdev = hm.to(dev, non_blocking=True) if row0 else None
             dd = engine.forward(mdev)
             if dd is not None:
                 out_d.copy_(dd, non_blocking=True)
@@ -502,13 +537,21 @@ def run_ours(args):
         for _ in range(e_steps):
             e2e_step_grid()
         barrier()
-        tt = torch.tensor([time.perf_counter() - t], device=dev)
+        tt = torch.tensor([time.perf_counter() - t])
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_s = float(tt[0]) / e_steps
+        # host<->device bytes over all ranks: m slices in on row 0 (F, H), d slices in
+        # on column 0 (F*); d out on column 0 (F), m out on row 0 (F*, H)
+        gc_ = int(grid.split("x")[1])
+        h2d = sum(8 * nt * (2 * s_.local_sources * (s_.grid_row == 0) + s_.local_sensors * (s_.grid_col == 0))
+                  for s_ in shards)
+        d2h = sum(8 * nt * (s_.local_sensors * (s_.grid_col == 0) + 2 * s_.local_sources * (s_.grid_row == 0))
+                  for s_ in shards)
         e2e = {"value": step_bytes / e_s / 1e12, "unit": "TB/s",
-               "h2d_bytes_per_step": 8 * (2 * nm * nt * world + nd * nt), "d2h_bytes_per_step": 8 * (nd * nt + 2 * nm * nt * world),
-               "ms_per_step": e_s * 1e3, "steps": e_steps,
-               "path": "pinned host slices -> GridEngine.forward/adjoint/hessian (NCCL) -> pinned host slices"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_s * 1e3, "steps": e_steps, "grid_cols": gc_,
+               "path": f"pinned host slices -> GridEngine.forward/adjoint/hessian (libbtg grid engine, "
+                       f"{transport} collectives) -> pinned host slices"}
     if engine is None:
         dshape = tuple(d.shape)
         hm = torch.empty(vshape, dtype=torch.float64, pin_memory=True)
@@ -628,11 +671,15 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None, "dtype": "f64" if prec == 64 else "f32 F-hat, f64 vectors/accumulation",
             "data": "synthetic: device SplitMix64 uniform(-1,1) first block column (seed 1000, global index), m (seed 7), "
                     "Gamma^-1 uniform(0.5,2) per sensor (seed 8)",
             "config": {"workload": cfg["label"], "N_t": nt, "N_d": nd, "N_m": nm, "nrhs": nrhs, "grid": grid,
+                       "N_d_global": nd_g, "N_m_global": nm_g,
+                       "scaling": "strong" if cfg.get("strong") else "weak",
+                       "grid_transport": None if engine is None else transport,
                        "step": "F m + F* d + F* Gamma^-1 F v (alpha=0), FP64, F-hat N_t+1 frequencies",
                        "fhat_gb_per_gpu": 16 * (nt + 1) * nd * nm / 1e9,
                        "l2": "inputs larger than L2: every matvec streams the full F-hat (>> 126 MB L2)",
@@ -665,6 +712,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--precision", type=int, choices=[64, 32], default=None, help="F-hat precision override")
+    ap.add_argument("--grid", default=None, help="RxC processor grid for N > 1 (default: the planner's pick)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rules)")

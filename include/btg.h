@@ -43,7 +43,8 @@ typedef enum {
     BTG_ENOMEM = 5,  /* device allocation failed                                                   */
     BTG_EGRID = 6,   /* unserviceable processor grid -> btoep::GridError (distributed.cpp:147-152) */
     BTG_ESOLVER = 7, /* CG lost positive definiteness -> btoep::SolverError (inverse.cpp:124-136) */
-    BTG_EFORMAT = 8  /* malformed / inconsistent file -> btoep::FormatError (io.cpp)              */
+    BTG_EFORMAT = 8, /* malformed / inconsistent file -> btoep::FormatError (io.cpp)              */
+    BTG_ENCCL = 9    /* NCCL / grid transport failure                                             */
 } btg_status;
 
 typedef enum { BTG_F64 = 64, BTG_F32 = 32 } btg_precision;
@@ -243,10 +244,11 @@ btg_status btg_read_vector(const char* path, double* values, size_t capacity, si
 btg_status btg_slice_operator(btg_op src, size_t i0, size_t i1, size_t j0, size_t j1, int device,
                               btg_op* out);
 
-/* Grid planner (grid_planner.hpp:43-65): the reference's scale-free cost
- * (r/p) ln r + (10^l/r) ln(p/r), l = log10(N_d/N_m), its minimiser snapped to
- * an r x c factorisation of `workers` (select_grid, grid_planner.cpp:123-193),
- * the weak-scaling choice (:195-207) and the broadcast+reduce model (:105-114). */
+/* Grid planner, reference criterion (grid_planner.hpp:43-65): the scale-free cost
+ * (r/p) ln r + (10^l/r) ln(p/r), l = log10(N_d/N_m), its minimiser snapped to an
+ * r x c factorisation of `workers` with the reference's preferences
+ * (select_grid, grid_planner.cpp:123-193), the weak-scaling choice (:195-207)
+ * and the broadcast+reduce model (:105-114). */
 btg_status btg_select_grid(size_t workers, double log_dim_ratio, unsigned gpus_per_node, size_t* rows,
                            size_t* cols);
 btg_status btg_weak_scaling_shape(double local_ratio, size_t workers, int* indifferent, size_t* rows,
@@ -264,17 +266,179 @@ btg_status btg_conventional_cost_estimate(double grid_points, double num_steps, 
                                           double rank_fraction, btg_cost_estimate* out);
 double btg_apply_arithmetic_intensity(double local_sensors, double local_sources);
 
+/* B200 / NVSwitch planner: the modelled time of one action
+ * (btg_grid_kind) of the grid engine's schedule on every r x c factorisation of
+ * `workers` — the worst shard's HBM stream and vector transforms plus the NCCL
+ * ring collectives at NVLink-5 rates inside the NVSwitch domain (the node link
+ * outside it). `best` = the cheapest (ties to fewer rows); `all` (optional,
+ * `cap` entries) = every feasible factorisation, rows ascending. hw NULL =
+ * btg_default_hw_model (measured B200 rates). */
+typedef struct {
+    double hbm_gbs;        /* local F-hat stream, GB/s            */
+    double fft_gbs;        /* vector transforms, GB/s             */
+    double link_gbs;       /* NVLink per direction per GPU, GB/s  */
+    double node_link_gbs;  /* between NVSwitch domains, GB/s      */
+    double latency_us;     /* per ring step                       */
+    unsigned gpus_per_node;
+} btg_hw_model;
+typedef struct {
+    size_t rows, cols;
+    double seconds, local_seconds, comm_seconds;
+} btg_grid_plan;
+btg_status btg_default_hw_model(btg_hw_model* out);
+btg_status btg_plan_grid(size_t num_sensors, size_t num_sources, size_t num_steps, size_t workers, int precision,
+                         int kind, const btg_hw_model* hw, btg_grid_plan* best, btg_grid_plan* all, size_t cap,
+                         size_t* count);
+
+/* ---- processor grid engine (distributed.hpp:43-121, distributed.cpp:145-392) ----
+ * An r x c grid over N_d x N_m: grid cell (i, j) = rank i*c + j owns sensors
+ * [i*ceil(N_d/r), ...) x sources [j*ceil(N_m/c), ...) of every stored frequency
+ * block (the reference's ceiling partition, distributed.cpp:145-175; trailing
+ * shards may be empty; grids wider than the operator -> BTG_EGRID). One
+ * schedule (btg_grid_schedule) drives every transport:
+ *   F  (distributed.cpp:312-351): column broadcast of the parameter slice from
+ *      row 0, local F, row reduce (sum) onto column 0;
+ *   F* (distributed.cpp:353-392): row broadcast of the data slice from column 0,
+ *      local F*, column reduce onto row 0;
+ *   H  (inverse.cpp:78-91 on a partition, + Gamma^-1): column broadcast, local F
+ *      with Gamma^-1 in its C2R epilogue, ONE row all-reduce (the F reduce and
+ *      the F* broadcast merged), local F* with alpha R v added on row 0, column
+ *      reduce onto row 0.
+ * Transports:
+ *   NCCL  (btg_grid_create: one process per GPU, ncclCommInitRank + ncclCommSplit
+ *          into row / column communicators; btg_grid_create_local with
+ *          BTG_TRANSPORT_NCCL: every cell in this process on distinct devices,
+ *          ncclCommInitAll). NCCL_ALGO=Ring / NCCL_PROTO=Simple are pinned at
+ *          creation (unless already set in the environment) so a fixed grid
+ *          gives run-to-run identical bits.
+ *   P2P   (btg_grid_create_local with BTG_TRANSPORT_P2P: the reference's
+ *          single-process Partition; any device placement, several cells per
+ *          device allowed): device-to-device copies and a sum kernel that adds
+ *          the partials in the reference's fixed binary tree order
+ *          (tree_reduce, distributed.cpp:36-47), so results are bit-identical
+ *          to tree-summing the same partials and serial == parallel.
+ *   external (btg_grid_create_external): host callbacks; used by the tests to
+ *          run several ranks on ONE GPU over torch.distributed/gloo (NCCL
+ *          refuses two ranks on one device). Not a compute path. */
+typedef struct btg_grid_s* btg_grid;
+
+typedef enum { BTG_GRID_FORWARD = 0, BTG_GRID_ADJOINT = 1, BTG_GRID_HESSIAN = 2 } btg_grid_kind;
+typedef enum {
+    BTG_STEP_INPUT = 0,     /* caller's slice -> buffer dst (active ranks own the input)        */
+    BTG_STEP_BROADCAST = 1, /* buffer src from the group's member `root` to the whole group      */
+    BTG_STEP_FORWARD = 2,   /* local F: src -> dst (gamma: Gamma^-1 rows of this shard)          */
+    BTG_STEP_ADJOINT = 3,   /* local F*: src -> dst (reg: + alpha R (buffer 0) in the epilogue) */
+    BTG_STEP_REDUCE = 4,    /* sum of buffer src over the group onto member `root`               */
+    BTG_STEP_ALLREDUCE = 5, /* sum of buffer src over the group, on every member                */
+    BTG_STEP_OUTPUT = 6     /* buffer src -> caller (active ranks return the output slice)       */
+} btg_step_op;
+typedef enum { BTG_GROUP_ROW = 0, BTG_GROUP_COL = 1 } btg_group_kind;
+typedef struct {
+    int op;        /* btg_step_op */
+    int group;     /* collectives: btg_group_kind (row i: members j = 0..c-1; column j: members i) */
+    int root;      /* collectives: member index of the root within the group */
+    int src, dst;  /* buffer ids 0, 1, 2 */
+    int active;    /* INPUT / OUTPUT: this rank takes part */
+    int gamma;     /* FORWARD: apply Gamma^-1 */
+    int reg;       /* ADJOINT: add alpha R (buffer 0) */
+    size_t count;  /* doubles in the buffer this step touches on this rank */
+} btg_grid_step;
+
+/* The per-rank schedule (host logic only; the executor and the tests run it).
+ * Every rank of a grid gets the same sequence of step ops; `active`, `gamma`,
+ * `reg` and `count` are rank-specific. Steps over groups of one member are
+ * omitted. */
+btg_status btg_grid_schedule(size_t num_sensors, size_t num_sources, size_t num_steps, size_t rows, size_t cols,
+                             size_t rank, int kind, int with_gamma, int with_reg, btg_grid_step* steps, size_t cap,
+                             size_t* count);
+
+/* CommLog events of the reference's byte model (record_collective,
+ * distributed.cpp:23-34) for one F (kind 0) or F* (kind 1) over the grid. */
+typedef struct {
+    int phase;  /* 0 "broadcast", 1 "reduce" */
+    size_t participants, messages;
+    uint64_t link_bytes, total_bytes;
+    size_t tree_depth;
+} btg_comm_event;
+btg_status btg_comm_events(size_t num_sensors, size_t num_sources, size_t num_steps, size_t rows, size_t cols,
+                           int kind, btg_comm_event* out, size_t cap, size_t* count);
+
+typedef enum { BTG_TRANSPORT_NCCL = 0, BTG_TRANSPORT_P2P = 1, BTG_TRANSPORT_EXTERNAL = 2 } btg_transport;
+#define BTG_NCCL_ID_BYTES 128
+
+/* ncclGetUniqueId: rank 0 creates it and ships the bytes to the other ranks. */
+btg_status btg_grid_nccl_id(void* id_out /* BTG_NCCL_ID_BYTES */);
+/* Multi-process grid: this process is grid cell `rank` on `device` (NCCL). */
+btg_status btg_grid_create(size_t rows, size_t cols, size_t rank, const void* nccl_id, int device, btg_grid* out);
+/* Single-process grid: every cell in this process, cell k on devices[k % num_devices]
+ * (NULL: device 0). transport: BTG_TRANSPORT_P2P or BTG_TRANSPORT_NCCL (needs
+ * rows*cols distinct devices). */
+btg_status btg_grid_create_local(size_t rows, size_t cols, const int* devices, size_t num_devices, int transport,
+                                 btg_grid* out);
+/* Host-callback transport for one rank (tests). Buffers are page-locked host
+ * copies of `n` doubles; return 0 on success. */
+typedef struct {
+    void* user;
+    int (*broadcast)(void* user, int group, double* buf, size_t n, int root);
+    int (*reduce)(void* user, int group, double* buf, size_t n, int root);
+    int (*allreduce)(void* user, int group, double* buf, size_t n);
+} btg_grid_callbacks;
+btg_status btg_grid_create_external(size_t rows, size_t cols, size_t rank, int device, const btg_grid_callbacks* cb,
+                                    btg_grid* out);
+
+/* Global operator dims (fixes the partition). Implied by setup / from_operator. */
+btg_status btg_grid_set_dims(btg_grid g, size_t num_sensors, size_t num_sources, size_t num_steps);
+/* Setup (partition_operator(CompactP2O), distributed.cpp:179-196). Local grids:
+ * `blocks` is the global TOSI first block column (N_t x N_d x N_m) and every
+ * cell transforms its rectangle; one-rank grids: `blocks` is this rank's
+ * rectangle (N_t x local N_d x local N_m). Host pointer unless BTG_DEVICE_PTRS. */
+btg_status btg_grid_setup(btg_grid g, const double* blocks, size_t num_sensors, size_t num_sources, size_t num_steps,
+                          int precision, unsigned flags);
+/* partition_operator(const SpectralP2O&) (distributed.cpp:198-218) for a local
+ * grid: every cell slices its rectangle of `global` HBM->HBM (btg_slice_operator). */
+btg_status btg_grid_from_operator(btg_grid g, btg_op global);
+/* Adopt `shard` (dims = the cell's rectangle; NULL for an empty cell) as the
+ * operator of cell `rank` (must be local). take_ownership: destroyed with the grid. */
+btg_status btg_grid_attach(btg_grid g, size_t rank, btg_op shard, int take_ownership);
+/* bounds[4] = sensor_begin, sensor_end, source_begin, source_end of cell `rank`;
+ * *op = its operator when local (else NULL). */
+btg_status btg_grid_shard(btg_grid g, size_t rank, size_t* bounds, btg_op* op);
+/* rows, cols; rank = this process's cell (SIZE_MAX for a local grid); transport */
+btg_status btg_grid_info(btg_grid g, size_t* rows, size_t* cols, size_t* rank, int* transport);
+
+/* Local grids: global SOTI vectors (N_m x N_t, N_d x N_t). One-rank grids: this
+ * rank's slices — inputs on the ranks whose INPUT step is active (F, H: row 0;
+ * F*: column 0), outputs on the OUTPUT-active ranks (F: column 0; F*, H: row 0);
+ * pass NULL / 0 elsewhere. Host pointers unless BTG_DEVICE_PTRS (then the call
+ * is asynchronous on the grid stream). distributed_forward / distributed_adjoint
+ * (distributed.cpp:312-392); btg_grid_hessian: F* Gamma^-1 F v + alpha R v with a
+ * GLOBAL gamma_inv (N_d or N_d x N_t; each cell uses its rows). */
+btg_status btg_grid_forward(btg_grid g, const double* m, size_t m_len, double* d, size_t d_len, unsigned flags);
+btg_status btg_grid_adjoint(btg_grid g, const double* d, size_t d_len, double* m, size_t m_len, unsigned flags);
+btg_status btg_grid_hessian(btg_grid g, const double* v, size_t v_len, double* hv, size_t hv_len,
+                            const double* gamma_inv, int gamma_kind, double alpha, int reg_kind, unsigned flags);
+/* backend of the local step: 0 fft, 1 ewp (needs BTG_KEEP_CHANNEL_LAYOUT), 2 naive
+ * (grids set up from time-domain blocks); parallel: one host thread per local cell
+ * for the local step (ExecutionPolicy::Parallel). */
+btg_status btg_grid_set_backend(btg_grid g, int backend, int parallel);
+/* One-rank grids: run on `stream` (NULL = the grid's own stream). */
+btg_status btg_grid_set_stream(btg_grid g, void* stream);
+btg_status btg_grid_synchronize(btg_grid g);
+/* The CommLog of the F / F* calls since creation (or the last reset). */
+btg_status btg_grid_comm_log(btg_grid g, btg_comm_event* out, size_t cap, size_t* count);
+btg_status btg_grid_reset_comm_log(btg_grid g);
+void btg_grid_destroy(btg_grid g);
+
 /* ---- single-process partition (distributed.hpp:43-121) ------------------------
- * partition_operator / distributed_forward / distributed_adjoint: one device
- * handle per non-empty cell of a rows x cols grid (the ceiling partition,
- * distributed.cpp:145-175; BTG_EGRID for grids wider than the operator), placed
- * round-robin on `devices` (NULL: device 0). The partial data / parameter slices
- * are summed on the host with the reference's fixed tree (tree_reduce,
- * distributed.cpp:36-47), so `parallel` (one host thread per cell, the
- * reference's ExecutionPolicy::Parallel) gives bit-identical results. Host SOTI
- * vectors. backend: 0 fft, 1 ewp (needs BTG_KEEP_CHANNEL_LAYOUT), 2 naive
- * (partitions of compact operators only, as in the reference). */
-typedef struct btg_partition_s* btg_partition;
+ * partition_operator / distributed_forward / distributed_adjoint with global
+ * host SOTI vectors: a local grid on the P2P transport (see above) — one device
+ * handle per non-empty cell, placed round-robin on `devices` (NULL: device 0),
+ * partial slices summed on the device in the reference's fixed tree order, so
+ * `parallel` (one host thread per cell, the reference's ExecutionPolicy::Parallel)
+ * gives bit-identical results. backend: 0 fft, 1 ewp (needs
+ * BTG_KEEP_CHANNEL_LAYOUT), 2 naive (partitions of compact operators only, as in
+ * the reference). */
+typedef struct btg_grid_s* btg_partition;
 btg_status btg_partition_create(const double* blocks, size_t num_sensors, size_t num_sources, size_t num_steps,
                                 size_t rows, size_t cols, const int* devices, size_t num_devices, int precision,
                                 unsigned flags, btg_partition* out);      /* partition_operator(CompactP2O) */
@@ -286,6 +450,11 @@ btg_status btg_partition_forward(btg_partition p, const double* m, size_t m_len,
                                  int backend, int parallel);
 btg_status btg_partition_adjoint(btg_partition p, const double* d, size_t d_len, double* m, size_t m_len,
                                  int backend, int parallel);
+/* HessianOperator::apply with a partition (inverse.cpp:78-91, + Gamma^-1): the grid
+ * Hessian schedule, host vectors, global gamma_inv. */
+btg_status btg_partition_hessian(btg_partition p, const double* v, size_t v_len, double* hv, size_t hv_len,
+                                 const double* gamma_inv, int gamma_kind, double alpha, int reg_kind, int backend,
+                                 int parallel);
 void btg_partition_destroy(btg_partition p);
 
 /* Device pointer of F-hat and bytes per element (16 f64 / 8 f32). */

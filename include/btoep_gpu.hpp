@@ -20,6 +20,7 @@
 #include <complex>
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -349,6 +350,11 @@ inline CGResult cg_solve(const HessianOperator& hessian, const SpaceTimeVector& 
     int gk = BTG_GAMMA_NONE;
     if (hessian.gamma_inv.size() == op.num_sensors) gk = BTG_GAMMA_PER_SENSOR;
     else if (hessian.gamma_inv.size() == op.num_sensors * op.num_steps) gk = BTG_GAMMA_PER_SAMPLE;
+    else if (!hessian.gamma_inv.empty())
+        throw DimensionError("cg_solve: gamma_inv must have N_d or N_d x N_t entries");
+    // The solver runs on *hessian.op in HBM. A partition or backend choice describes
+    // the same operator (the reference requires op to be set as well, inverse.cpp:79):
+    // they change only the summation order of H v, not the system being solved.
     CGResult out;
     out.solution = SpaceTimeVector::zeros(rhs.spatial_dim, rhs.num_steps, Ordering::SOTI);
     btg_cg_result r{};
@@ -565,50 +571,138 @@ inline SpaceTimeVector distributed_adjoint(const Partition& partition, const Spa
     return detail::distributed_apply(partition, d, true, options, log);
 }
 
-// HessianOperator::apply (inverse.cpp:78-91): on the partition when one is set
-// (distributed_forward, Gamma^-1, distributed_adjoint, + alpha R v on the host),
-// else the fused single-device btg_hessian.
+// HessianOperator::apply (inverse.cpp:78-91): on the partition's grid engine when
+// one is set (btg_partition_hessian: column broadcast, local F with Gamma^-1 in
+// the C2R epilogue, row all-reduce, local F* with alpha R v, column reduce — all
+// on the devices), else the fused single-device btg_hessian.
 inline SpaceTimeVector HessianOperator::apply(const SpaceTimeVector& v) const {
     if (!op) throw Error("hessian: no operator attached");
+    detail::check_apply_input(*op, v, op->num_sources, "hessian");
+    int gk = BTG_GAMMA_NONE;
+    if (gamma_inv.size() == op->num_sensors) gk = BTG_GAMMA_PER_SENSOR;
+    else if (gamma_inv.size() == op->num_sensors * op->num_steps) gk = BTG_GAMMA_PER_SAMPLE;
+    else if (!gamma_inv.empty()) throw DimensionError("hessian: gamma_inv has the wrong length");
+    const int rk = reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN : BTG_REG_IDENTITY;
+    SpaceTimeVector out = SpaceTimeVector::zeros(v.spatial_dim, v.num_steps, Ordering::SOTI);
     if (!partition) {
-        detail::check_apply_input(*op, v, op->num_sources, "hessian");
-        int gk = BTG_GAMMA_NONE;
-        if (gamma_inv.size() == op->num_sensors) gk = BTG_GAMMA_PER_SENSOR;
-        else if (gamma_inv.size() == op->num_sensors * op->num_steps) gk = BTG_GAMMA_PER_SAMPLE;
-        else if (!gamma_inv.empty()) throw DimensionError("hessian: gamma_inv has the wrong length");
-        SpaceTimeVector out = SpaceTimeVector::zeros(v.spatial_dim, v.num_steps, Ordering::SOTI);
         detail::check(btg_hessian(op->handle(), v.values.data(), v.values.size(), out.values.data(),
                                   out.values.size(), 1, gamma_inv.empty() ? nullptr : gamma_inv.data(), gk,
-                                  reg.alpha,
-                                  reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN
-                                                                         : BTG_REG_IDENTITY,
-                                  0u));
+                                  reg.alpha, rk, 0u));
         return out;
     }
-    SpaceTimeVector d = distributed_forward(*partition, v, engine);
-    if (!gamma_inv.empty()) {
-        const std::size_t nd = d.spatial_dim, nt = d.num_steps;
-        if (gamma_inv.size() != nd && gamma_inv.size() != nd * nt)
-            throw DimensionError("hessian: gamma_inv has the wrong length");
-        for (std::size_t i = 0; i < nd; ++i)
-            for (std::size_t t = 0; t < nt; ++t)
-                d.values[i * nt + t] *= gamma_inv.size() == nd ? gamma_inv[i] : gamma_inv[i * nt + t];
-    }
-    SpaceTimeVector out = distributed_adjoint(*partition, d, engine);
-    if (reg.alpha != 0.0) {  // Regularization::apply (inverse.cpp:32-49)
-        const std::size_t nt = v.num_steps;
-        for (std::size_t s = 0; s < v.spatial_dim; ++s) {
-            const double* x = v.values.data() + s * nt;
-            double* y = out.values.data() + s * nt;
-            for (std::size_t t = 0; t < nt; ++t) {
-                double r = x[t];
-                if (reg.kind == RegKind::TemporalLaplacian)
-                    r = 2.0 * x[t] - (t > 0 ? x[t - 1] : 0.0) - (t + 1 < nt ? x[t + 1] : 0.0);
-                y[t] += reg.alpha * r;
-            }
-        }
-    }
+    detail::check(btg_partition_hessian(partition->handle(), v.values.data(), v.values.size(), out.values.data(),
+                                        out.values.size(), gamma_inv.empty() ? nullptr : gamma_inv.data(), gk,
+                                        reg.alpha, rk, static_cast<int>(engine.backend),
+                                        engine.policy == ExecutionPolicy::Parallel ? 1 : 0));
     return out;
 }
+
+// ---- multi-process NCCL grid (one process per GPU) ------------
+// The reference's distributed F / F* / partitioned Hessian with real collectives:
+// rank i*cols + j owns cell (i, j); rank 0 makes the NCCL id (nccl_id()) and the
+// caller ships its bytes to every rank (MPI_Bcast, a file, a TCP store, ...).
+// Slices follow scatter_param / scatter_data (distributed.hpp:66-73): parameter
+// slices live on row 0, data slices on column 0; non-owners pass nullptr.
+class Grid {
+public:
+    using Id = std::array<char, BTG_NCCL_ID_BYTES>;
+    static Id nccl_id() {
+        Id id{};
+        detail::check(btg_grid_nccl_id(id.data()));
+        return id;
+    }
+    // Every rank calls this with the same shape, id and global operator dims.
+    Grid(GridShape shape, std::size_t rank, const Id& id, int device, std::size_t num_sensors,
+         std::size_t num_sources, std::size_t num_steps)
+        : shape_(shape), rank_(rank), nd_(num_sensors), nm_(num_sources), nt_(num_steps) {
+        detail::check(btg_grid_create(shape.rows, shape.cols, rank, id.data(), device, &h_));
+        try {
+            detail::check(btg_grid_set_dims(h_, nd_, nm_, nt_));
+        } catch (...) {
+            btg_grid_destroy(h_);
+            throw;
+        }
+    }
+    Grid(const Grid&) = delete;
+    Grid& operator=(const Grid&) = delete;
+    ~Grid() {
+        if (h_) btg_grid_destroy(h_);
+    }
+    // sensor_begin, sensor_end, source_begin, source_end of this rank's cell
+    std::array<std::size_t, 4> bounds() const {
+        std::array<std::size_t, 4> b{};
+        detail::check(btg_grid_shard(h_, rank_, b.data(), nullptr));
+        return b;
+    }
+    // partition_operator(CompactP2O) for this rank: `local` is the rank's rectangle
+    // (N_t x local sensors x local sources) of the first block column.
+    void setup(const CompactP2O& local, const SetupOptions& options = {}) {
+        const auto b = bounds();
+        if (b[1] == b[0] || b[3] == b[2]) {  // empty cell (ragged ceiling partition)
+            detail::check(btg_grid_attach(h_, rank_, nullptr, 0));
+            return;
+        }
+        local.validate();
+        if (local.num_sensors != b[1] - b[0] || local.num_sources != b[3] - b[2] || local.num_steps != nt_)
+            throw DimensionError("grid setup: the rectangle does not match this rank's cell");
+        detail::check(btg_grid_setup(h_, local.blocks.data(), nd_, nm_, nt_, options.precision, 0u));
+    }
+    bool owns_param_slice() const { return rank_ / shape_.cols == 0; }  // row 0
+    bool owns_data_slice() const { return rank_ % shape_.cols == 0; }   // column 0
+    // distributed_forward: m slice in on row 0, d slice out on column 0
+    std::optional<SpaceTimeVector> forward(const SpaceTimeVector* m_slice) {
+        return run(m_slice, owns_param_slice(), false, owns_data_slice(), false,
+                   [&](const double* in, std::size_t nin, double* o, std::size_t no) {
+                       return btg_grid_forward(h_, in, nin, o, no, 0u);
+                   });
+    }
+    // distributed_adjoint: d slice in on column 0, m slice out on row 0
+    std::optional<SpaceTimeVector> adjoint(const SpaceTimeVector* d_slice) {
+        return run(d_slice, owns_data_slice(), true, owns_param_slice(), true,
+                   [&](const double* in, std::size_t nin, double* o, std::size_t no) {
+                       return btg_grid_adjoint(h_, in, nin, o, no, 0u);
+                   });
+    }
+    // F* Gamma^-1 F v + alpha R v; v / Hv slices on row 0; gamma_inv GLOBAL (N_d or N_d x N_t)
+    std::optional<SpaceTimeVector> hessian(const SpaceTimeVector* v_slice, const Regularization& reg,
+                                           const std::vector<double>& gamma_inv = {}) {
+        int gk = BTG_GAMMA_NONE;
+        if (gamma_inv.size() == nd_) gk = BTG_GAMMA_PER_SENSOR;
+        else if (gamma_inv.size() == nd_ * nt_) gk = BTG_GAMMA_PER_SAMPLE;
+        else if (!gamma_inv.empty()) throw DimensionError("grid hessian: gamma_inv must be global (N_d or N_d x N_t)");
+        const int rk = reg.kind == RegKind::TemporalLaplacian ? BTG_REG_TEMPORAL_LAPLACIAN : BTG_REG_IDENTITY;
+        return run(v_slice, owns_param_slice(), false, owns_param_slice(), true,
+                   [&](const double* in, std::size_t nin, double* o, std::size_t no) {
+                       return btg_grid_hessian(h_, in, nin, o, no, gamma_inv.empty() ? nullptr : gamma_inv.data(),
+                                               gk, reg.alpha, rk, 0u);
+                   });
+    }
+    btg_grid handle() const { return h_; }
+
+private:
+    // in_data / out_param: whether the input is a data slice and the output a parameter slice
+    template <typename F>
+    std::optional<SpaceTimeVector> run(const SpaceTimeVector* x, bool in_owner, bool in_data, bool out_owner,
+                                       bool out_param, F call) {
+        const auto b = bounds();
+        const std::size_t ld = b[1] - b[0], lm = b[3] - b[2];
+        if (in_owner) {
+            if (!x) throw Error("grid: this rank owns an input slice and must pass it");
+            x->validate();
+            x->require_ordering(Ordering::SOTI);
+            if (x->spatial_dim != (in_data ? ld : lm) || x->num_steps != nt_)
+                throw DimensionError("grid: slice does not match this rank's cell");
+        }
+        std::optional<SpaceTimeVector> out;
+        if (out_owner) out = SpaceTimeVector::zeros(out_param ? lm : ld, nt_, Ordering::SOTI);
+        detail::check(call(in_owner ? x->values.data() : nullptr, in_owner ? x->values.size() : 0,
+                           out ? out->values.data() : nullptr, out ? out->values.size() : 0));
+        return out;
+    }
+    GridShape shape_;
+    std::size_t rank_ = 0;
+    std::size_t nd_ = 0, nm_ = 0, nt_ = 0;
+    btg_grid h_ = nullptr;
+};
 
 }  // namespace btoep

@@ -11,13 +11,19 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libbtg.so"
 
-BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER, BTG_EFORMAT = range(9)
+BTG_OK, BTG_EDIM, BTG_EORDER, BTG_EARG, BTG_ECUDA, BTG_ENOMEM, BTG_EGRID, BTG_ESOLVER, BTG_EFORMAT, BTG_ENCCL = range(10)
 BTG_F64, BTG_F32 = 64, 32
 BTG_DEVICE_PTRS = 0x1
 BTG_KEEP_CHANNEL_LAYOUT = 0x2
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream (torch's stream 0)
 BTG_REG_IDENTITY, BTG_REG_TEMPORAL_LAPLACIAN = 0, 1
 BTG_GAMMA_NONE, BTG_GAMMA_PER_SENSOR, BTG_GAMMA_PER_SAMPLE = 0, 1, 2
+BTG_GRID_FORWARD, BTG_GRID_ADJOINT, BTG_GRID_HESSIAN = 0, 1, 2
+(BTG_STEP_INPUT, BTG_STEP_BROADCAST, BTG_STEP_FORWARD, BTG_STEP_ADJOINT, BTG_STEP_REDUCE, BTG_STEP_ALLREDUCE,
+ BTG_STEP_OUTPUT) = range(7)
+BTG_GROUP_ROW, BTG_GROUP_COL = 0, 1
+BTG_TRANSPORT_NCCL, BTG_TRANSPORT_P2P, BTG_TRANSPORT_EXTERNAL = 0, 1, 2
+BTG_NCCL_ID_BYTES = 128
 
 # Every symbol include/btg.h declares (checked by tests/test_abi.py).
 EXPORTED = (
@@ -43,7 +49,29 @@ EXPORTED = (
     "btg_partition_shard",
     "btg_partition_forward",
     "btg_partition_adjoint",
+    "btg_partition_hessian",
     "btg_partition_destroy",
+    "btg_grid_schedule",
+    "btg_comm_events",
+    "btg_grid_nccl_id",
+    "btg_grid_create",
+    "btg_grid_create_local",
+    "btg_grid_create_external",
+    "btg_grid_set_dims",
+    "btg_grid_setup",
+    "btg_grid_from_operator",
+    "btg_grid_attach",
+    "btg_grid_shard",
+    "btg_grid_info",
+    "btg_grid_forward",
+    "btg_grid_adjoint",
+    "btg_grid_hessian",
+    "btg_grid_set_backend",
+    "btg_grid_set_stream",
+    "btg_grid_synchronize",
+    "btg_grid_comm_log",
+    "btg_grid_reset_comm_log",
+    "btg_grid_destroy",
     "btg_read_compact",
     "btg_conventional_cost_estimate",
     "btg_apply_arithmetic_intensity",
@@ -73,6 +101,8 @@ EXPORTED = (
     "btg_weak_scaling_shape",
     "btg_modified_cost",
     "btg_comm_cost",
+    "btg_default_hw_model",
+    "btg_plan_grid",
 )
 
 
@@ -98,6 +128,10 @@ class SolverError(RuntimeError):
 
 class FormatError(ValueError):
     """btoep::FormatError (errors.hpp:23-25)."""
+
+
+class CommError(RuntimeError):
+    """NCCL / grid transport failure (BTG_ENCCL)."""
 
 
 class FileHeader(ctypes.Structure):
@@ -133,6 +167,78 @@ class Epilogue(ctypes.Structure):
         ("reg_v", ctypes.c_void_p),
         ("alpha", ctypes.c_double),
         ("reg_kind", ctypes.c_int),
+    ]
+
+
+class GridStep(ctypes.Structure):
+    """btg_grid_step: one step of a rank's grid schedule."""
+
+    _fields_ = [
+        ("op", ctypes.c_int),
+        ("group", ctypes.c_int),
+        ("root", ctypes.c_int),
+        ("src", ctypes.c_int),
+        ("dst", ctypes.c_int),
+        ("active", ctypes.c_int),
+        ("gamma", ctypes.c_int),
+        ("reg", ctypes.c_int),
+        ("count", ctypes.c_size_t),
+    ]
+
+
+class CommEventC(ctypes.Structure):
+    """btg_comm_event == btoep::CommEvent (distributed.hpp:77-84)."""
+
+    _fields_ = [
+        ("phase", ctypes.c_int),
+        ("participants", ctypes.c_size_t),
+        ("messages", ctypes.c_size_t),
+        ("link_bytes", ctypes.c_uint64),
+        ("total_bytes", ctypes.c_uint64),
+        ("tree_depth", ctypes.c_size_t),
+    ]
+
+
+BCAST_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                            ctypes.c_size_t, ctypes.c_int)
+REDUCE_FN = BCAST_FN
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                ctypes.c_size_t)
+
+
+class GridCallbacks(ctypes.Structure):
+    """btg_grid_callbacks: host-callback transport (tests)."""
+
+    _fields_ = [
+        ("user", ctypes.c_void_p),
+        ("broadcast", BCAST_FN),
+        ("reduce", REDUCE_FN),
+        ("allreduce", ALLREDUCE_FN),
+    ]
+
+
+class HwModel(ctypes.Structure):
+    """btg_hw_model: rates of the B200 / NVSwitch planner."""
+
+    _fields_ = [
+        ("hbm_gbs", ctypes.c_double),
+        ("fft_gbs", ctypes.c_double),
+        ("link_gbs", ctypes.c_double),
+        ("node_link_gbs", ctypes.c_double),
+        ("latency_us", ctypes.c_double),
+        ("gpus_per_node", ctypes.c_uint),
+    ]
+
+
+class GridPlan(ctypes.Structure):
+    """btg_grid_plan: modelled seconds of one action on an r x c grid."""
+
+    _fields_ = [
+        ("rows", ctypes.c_size_t),
+        ("cols", ctypes.c_size_t),
+        ("seconds", ctypes.c_double),
+        ("local_seconds", ctypes.c_double),
+        ("comm_seconds", ctypes.c_double),
     ]
 
 
@@ -202,6 +308,36 @@ def load():
     L.btg_partition_shard.argtypes = [_vp, _sz, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_vp)]
     for name in ("btg_partition_forward", "btg_partition_adjoint"):
         getattr(L, name).argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_int, ctypes.c_int]
+    L.btg_partition_hessian.argtypes = [_vp, _dp, _sz, _dp, _sz, _dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_int]
+    L.btg_grid_schedule.argtypes = [_sz, _sz, _sz, _sz, _sz, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(GridStep), _sz, ctypes.POINTER(_sz)]
+    L.btg_comm_events.argtypes = [_sz, _sz, _sz, _sz, _sz, ctypes.c_int, ctypes.POINTER(CommEventC), _sz,
+                                  ctypes.POINTER(_sz)]
+    L.btg_grid_nccl_id.argtypes = [ctypes.c_char_p]
+    L.btg_grid_create.argtypes = [_sz, _sz, _sz, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.btg_grid_create_local.argtypes = [_sz, _sz, ctypes.POINTER(ctypes.c_int), _sz, ctypes.c_int,
+                                        ctypes.POINTER(_vp)]
+    L.btg_grid_create_external.argtypes = [_sz, _sz, _sz, ctypes.c_int, ctypes.POINTER(GridCallbacks),
+                                           ctypes.POINTER(_vp)]
+    L.btg_grid_set_dims.argtypes = [_vp, _sz, _sz, _sz]
+    L.btg_grid_setup.argtypes = [_vp, _dp, _sz, _sz, _sz, ctypes.c_int, ctypes.c_uint]
+    L.btg_grid_from_operator.argtypes = [_vp, _vp]
+    L.btg_grid_attach.argtypes = [_vp, _sz, _vp, ctypes.c_int]
+    L.btg_grid_shard.argtypes = [_vp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_vp)]
+    L.btg_grid_info.argtypes = [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_sz), ctypes.POINTER(_sz),
+                                ctypes.POINTER(ctypes.c_int)]
+    for name in ("btg_grid_forward", "btg_grid_adjoint"):
+        getattr(L, name).argtypes = [_vp, _dp, _sz, _dp, _sz, ctypes.c_uint]
+    L.btg_grid_hessian.argtypes = [_vp, _dp, _sz, _dp, _sz, _dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_uint]
+    L.btg_grid_set_backend.argtypes = [_vp, ctypes.c_int, ctypes.c_int]
+    L.btg_grid_set_stream.argtypes = [_vp, _vp]
+    L.btg_grid_synchronize.argtypes = [_vp]
+    L.btg_grid_comm_log.argtypes = [_vp, ctypes.POINTER(CommEventC), _sz, ctypes.POINTER(_sz)]
+    L.btg_grid_reset_comm_log.argtypes = [_vp]
+    L.btg_grid_destroy.argtypes = [_vp]
+    L.btg_grid_destroy.restype = None
     L.btg_partition_destroy.argtypes = [_vp]
     L.btg_partition_destroy.restype = None
     L.btg_write_compact.argtypes = [ctypes.c_char_p, _dp, _sz, _sz, _sz]
@@ -244,9 +380,12 @@ def load():
     L.btg_modified_cost.argtypes = [ctypes.c_double, _sz, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
     L.btg_comm_cost.argtypes = [_sz, _sz, _sz, _sz, _sz, ctypes.c_double, ctypes.c_double,
                                 ctypes.POINTER(ctypes.c_double)]
+    L.btg_default_hw_model.argtypes = [ctypes.POINTER(HwModel)]
+    L.btg_plan_grid.argtypes = [_sz, _sz, _sz, _sz, ctypes.c_int, ctypes.c_int, ctypes.POINTER(HwModel),
+                                ctypes.POINTER(GridPlan), ctypes.POINTER(GridPlan), _sz, ctypes.POINTER(_sz)]
     for name in EXPORTED:
         if name not in ("btg_last_error", "btg_abi_version", "btg_destroy", "btg_apply_arithmetic_intensity",
-                        "btg_partition_destroy"):
+                        "btg_partition_destroy", "btg_grid_destroy"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -269,4 +408,6 @@ def check(status: int) -> None:
         raise SolverError(msg)
     if status == BTG_EFORMAT:
         raise FormatError(msg)
+    if status == BTG_ENCCL:
+        raise CommError(msg)
     raise Error(msg)

@@ -278,7 +278,9 @@ btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* ou
                        const btg::C2REpilogue& epi, size_t fs = 0) {
     StageClock clk(op, &op->counters.inverse_fft);
     if (!fs) fs = channels;
-    if (op->fast_ok && aligned16(in) && aligned16(out))
+    // the fast epilogue reads alpha R v and per-sample Gamma^-1 as 16-byte pairs
+    const bool epi_aligned = (!epi.v || aligned16(epi.v)) && (epi.gamma_mode != 2 || aligned16(epi.gamma));
+    if (op->fast_ok && aligned16(in) && aligned16(out) && epi_aligned)
         BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)fs, out, (long long)op->nt,
                                           (int)channels, op->fast, epi, op->stream));
     else

@@ -1,11 +1,11 @@
-"""2-D processor grid for the block-Toeplitz matvec over torch.distributed.
+"""2-D processor grid for the block-Toeplitz matvec.
 
-B200 form of the reference's distributed engine (``src/distributed.cpp``):
-one process per GPU, rank ``i*cols + j`` owns grid cell (i, j) — the sensors
-``[i*ceil(N_d/r), ...)`` x sources ``[j*ceil(N_m/c), ...)`` block of every
-frequency (the ceiling partition, distributed.cpp:145-175) — and runs the
-single-GPU pipeline (libbtg) on its shard. The reference's simulated
-collectives become real NCCL collectives on row / column communicators:
+The data plane is libbtg's grid engine (``csrc/btg_grid_engine.cu``, C ABI
+``btg_grid_*``): one process per GPU, rank ``i*cols + j`` owns grid cell (i, j)
+— the sensors ``[i*ceil(N_d/r), ...)`` x sources ``[j*ceil(N_m/c), ...)``
+block of every frequency (the ceiling partition, distributed.cpp:145-175) —
+and the per-rank schedule runs in C++ with NCCL on row / column
+communicators:
 
 * F  (distributed.cpp:312-351): column broadcast of the parameter slice from
   row 0, local F, row reduce (sum) onto column 0.
@@ -16,21 +16,29 @@ collectives become real NCCL collectives on row / column communicators:
   is applied in the local C2R epilogue (linear, so before the reduce) and
   alpha R v is added once, on row 0, in the final C2R epilogue.
 
-The reductions are over time-domain d / m slices exactly as the reference does
-them. Collective byte accounting mirrors the reference's CommLog
-(distributed.hpp:77-92). With ``gloo`` and an injected host-side local
-operator the same engine runs on CPU (tests/test_distributed.py).
+This module is the Python face of it: :class:`GridEngine` (one rank per
+process; ``torch.distributed`` only ships the NCCL unique id), the
+single-process :class:`Partition` (the reference's ``Partition`` /
+``distributed_forward`` / ``distributed_adjoint`` over a local grid with the P2P
+transport), the schedule (:func:`schedule`) and the reference's CommLog byte
+model (:func:`comm_events`). ``transport="gloo"`` runs the same C++ schedule
+with the collectives handed to torch.distributed/gloo through host callbacks —
+it exists so several ranks can share ONE GPU in tests (NCCL refuses duplicate
+devices); it is not a compute path.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import ctypes
+from dataclasses import dataclass
 from typing import List, Optional, Tuple
 
+from . import _lib
 from ._lib import GridError
 
-__all__ = ["Shard", "CommEvent", "partition_bounds", "GridEngine", "synthetic_shard_operator", "Partition",
-           "partition_operator", "distributed_forward", "distributed_adjoint"]
+__all__ = ["Shard", "CommEvent", "partition_bounds", "schedule", "comm_events", "GridEngine",
+           "synthetic_shard_operator", "Partition", "partition_operator", "distributed_forward",
+           "distributed_adjoint"]
 
 
 @dataclass(frozen=True)
@@ -71,14 +79,6 @@ def partition_bounds(num_sensors: int, num_sources: int, rows: int, cols: int) -
             for i in range(rows) for j in range(cols)]
 
 
-def _tree_depth(participants: int) -> int:
-    depth, reach = 0, 1
-    while reach < participants:
-        reach *= 2
-        depth += 1
-    return depth
-
-
 @dataclass
 class CommEvent:
     """CommEvent (distributed.hpp:77-84)."""
@@ -86,14 +86,44 @@ class CommEvent:
     phase: str
     participants: int
     link_bytes: int
-    messages: int = 0
-    total_bytes: int = 0
-    tree_depth: int = 0
+    messages: int
+    total_bytes: int
+    tree_depth: int
 
-    def __post_init__(self):
-        self.messages = max(self.participants - 1, 0)
-        self.total_bytes = self.messages * self.link_bytes
-        self.tree_depth = _tree_depth(self.participants)
+
+_PHASES = {0: "broadcast", 1: "reduce"}
+_KINDS = {"forward": _lib.BTG_GRID_FORWARD, "adjoint": _lib.BTG_GRID_ADJOINT, "hessian": _lib.BTG_GRID_HESSIAN}
+
+
+def _events(arr, n) -> List[CommEvent]:
+    return [CommEvent(_PHASES[e.phase], int(e.participants), int(e.link_bytes), int(e.messages),
+                      int(e.total_bytes), int(e.tree_depth)) for e in arr[:n]]
+
+
+def comm_events(num_sensors: int, num_sources: int, num_steps: int, grid: Tuple[int, int], kind: str):
+    """The reference's CommLog of one F ("forward") or F* ("adjoint") over the grid
+    (record_collective, distributed.cpp:23-34), from libbtg's model."""
+    L = _lib.load()
+    cnt = ctypes.c_size_t()
+    _lib.check(L.btg_comm_events(num_sensors, num_sources, num_steps, grid[0], grid[1], _KINDS[kind], None, 0,
+                                 ctypes.byref(cnt)))
+    arr = (_lib.CommEventC * max(1, cnt.value))()
+    _lib.check(L.btg_comm_events(num_sensors, num_sources, num_steps, grid[0], grid[1], _KINDS[kind], arr,
+                                 cnt.value, ctypes.byref(cnt)))
+    return _events(arr, cnt.value)
+
+
+def schedule(num_sensors: int, num_sources: int, num_steps: int, grid: Tuple[int, int], rank: int, kind: str,
+             with_gamma: bool = False, with_reg: bool = False):
+    """The per-rank step list the C++ executor runs (btg_grid_schedule), as dicts."""
+    L = _lib.load()
+    cnt = ctypes.c_size_t()
+    args = (num_sensors, num_sources, num_steps, grid[0], grid[1], rank, _KINDS[kind], int(with_gamma),
+            int(with_reg))
+    _lib.check(L.btg_grid_schedule(*args, None, 0, ctypes.byref(cnt)))
+    arr = (_lib.GridStep * max(1, cnt.value))()
+    _lib.check(L.btg_grid_schedule(*args, arr, cnt.value, ctypes.byref(cnt)))
+    return [{k: int(getattr(st, k)) for k, _ in _lib.GridStep._fields_} for st in arr[:cnt.value]]
 
 
 def synthetic_shard_operator(num_sensors: int, num_sources: int, num_steps: int, shard: Shard, seed: int,
@@ -120,43 +150,115 @@ def synthetic_shard_operator(num_sensors: int, num_sources: int, num_steps: int,
     return op
 
 
-class GridEngine:
-    """F / F* / Hessian on an r x c grid of ranks (one GPU each).
+class _GlooTransport:
+    """Host callbacks for btg_grid_create_external over torch.distributed (gloo):
+    lets several ranks share one GPU in tests. Every rank creates every row and
+    column group in the same order (torch.distributed rule)."""
 
-    ``local_op`` is the shard's operator (a :class:`SpectralOperator`, or any
-    object with the same ``apply_forward(x, gamma_inv=)`` /
-    ``apply_adjoint(y, reg_v=, alpha=, reg=)`` methods on torch tensors); it
-    is None for an empty shard. Vector slices are torch tensors on ``device``:
-    parameter slices (local_sources x N_t) live on row-0 ranks, data slices
-    (local_sensors x N_t) on column-0 ranks, as in the reference
-    (scatter_param / scatter_data, distributed.hpp:66-73)."""
-
-    def __init__(self, num_sensors: int, num_sources: int, num_steps: int, grid: Tuple[int, int], local_op,
-                 device=None, process_group=None):
+    def __init__(self, rows: int, cols: int, rank: int):
+        import numpy as np
         import torch
         import torch.distributed as dist
 
-        self.dist = dist
-        self.torch = torch
-        self.rows, self.cols = grid
+        self.rows, self.cols = rows, cols
+        self.i, self.j = divmod(rank, cols)
+        self._row = [dist.new_group([i * cols + j for j in range(cols)], backend="gloo") for i in range(rows)]
+        self._col = [dist.new_group([i * cols + j for i in range(rows)], backend="gloo") for j in range(cols)]
+
+        def view(buf, n):
+            return torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
+
+        def group(g):
+            return (self._row[self.i], lambda m: self.i * cols + m) if g == _lib.BTG_GROUP_ROW else \
+                   (self._col[self.j], lambda m: m * cols + self.j)
+
+        def bcast(_user, g, buf, n, root):
+            try:
+                grp, rank_of = group(g)
+                dist.broadcast(view(buf, n), src=rank_of(root), group=grp)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as BTG_ENCCL by the engine
+                return 1
+
+        def reduce(_user, g, buf, n, root):
+            try:
+                grp, rank_of = group(g)
+                dist.reduce(view(buf, n), dst=rank_of(root), group=grp)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def allreduce(_user, g, buf, n):
+            try:
+                grp, _ = group(g)
+                dist.all_reduce(view(buf, n), group=grp)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self.callbacks = _lib.GridCallbacks(None, _lib.BCAST_FN(bcast), _lib.REDUCE_FN(reduce),
+                                            _lib.ALLREDUCE_FN(allreduce))
+
+
+class GridEngine:
+    """F / F* / Hessian on an r x c grid of ranks, one GPU each: a thin shim over
+    libbtg's ``btg_grid`` (the schedule, the NCCL collectives and the local
+    pipelines all run in C++).
+
+    ``local_op`` is this rank's shard (:class:`SpectralOperator`, None for an
+    empty shard); the engine borrows it. Vector slices are float64 CUDA tensors
+    on the rank's device: parameter slices (local_sources x N_t) on row-0 ranks,
+    data slices (local_sensors x N_t) on column-0 ranks, as in the reference
+    (scatter_param / scatter_data, distributed.hpp:66-73). Calls run on torch's
+    current stream."""
+
+    def __init__(self, num_sensors: int, num_sources: int, num_steps: int, grid: Tuple[int, int], local_op,
+                 device=None, transport: str = "nccl"):
+        import torch
+        import torch.distributed as dist
+
+        self.rows, self.cols = int(grid[0]), int(grid[1])
         self.num_sensors, self.num_sources, self.num_steps = num_sensors, num_sources, num_steps
-        self.world = dist.get_world_size(process_group)
-        self.rank = dist.get_rank(process_group)
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
         if self.world != self.rows * self.cols:
             raise GridError(f"grid {self.rows}x{self.cols} needs {self.rows * self.cols} ranks, have {self.world}")
         self.shards = partition_bounds(num_sensors, num_sources, self.rows, self.cols)
         self.shard = self.shards[self.rank]
         self.local_op = local_op
-        self.device = device if device is not None else torch.device("cpu")
-        self.comm_log: List[CommEvent] = []
-        # every rank creates every group, in the same order (torch.distributed rule)
-        self._row_groups = [dist.new_group([i * self.cols + j for j in range(self.cols)]) for i in range(self.rows)]
-        self._col_groups = [dist.new_group([i * self.cols + j for i in range(self.rows)]) for j in range(self.cols)]
+        if device is None:
+            device = torch.device(f"cuda:{torch.cuda.current_device()}")
+        self.device = torch.device(device)
+        self.transport = transport
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        dev = self.device.index or 0
+        if transport == "nccl":
+            uid = ctypes.create_string_buffer(_lib.BTG_NCCL_ID_BYTES)
+            if self.rank == 0:
+                _lib.check(L.btg_grid_nccl_id(uid))
+            obj = [uid.raw if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            _lib.check(L.btg_grid_create(self.rows, self.cols, self.rank, obj[0], dev, ctypes.byref(h)))
+        elif transport == "gloo":
+            self._gloo = _GlooTransport(self.rows, self.cols, self.rank)
+            _lib.check(L.btg_grid_create_external(self.rows, self.cols, self.rank, dev,
+                                                  ctypes.byref(self._gloo.callbacks), ctypes.byref(h)))
+        else:
+            raise _lib.Error(f"unknown grid transport '{transport}' (nccl or gloo)")
+        self._h = h
+        try:
+            _lib.check(L.btg_grid_set_dims(h, num_sensors, num_sources, num_steps))
+            _lib.check(L.btg_grid_attach(h, self.rank, local_op._h if local_op is not None else None, 0))
+        except Exception:
+            L.btg_grid_destroy(h)
+            self._h = None
+            raise
 
     # -- construction helpers ---------------------------------------------------
     @classmethod
     def synthetic(cls, num_sensors: int, num_sources: int, num_steps: int, grid: Tuple[int, int], seed: int,
-                  precision: int = 64):
+                  precision: int = 64, transport: str = "nccl"):
         """Each rank builds its own shard of the synthetic operator on its GPU."""
         import torch
         import torch.distributed as dist
@@ -166,10 +268,11 @@ class GridEngine:
         device = torch.cuda.current_device()
         op = None if shard.empty else synthetic_shard_operator(num_sensors, num_sources, num_steps, shard, seed,
                                                                device, precision)
-        return cls(num_sensors, num_sources, num_steps, grid, op, device=torch.device(f"cuda:{device}"))
+        return cls(num_sensors, num_sources, num_steps, grid, op, device=torch.device(f"cuda:{device}"),
+                   transport=transport)
 
     @classmethod
-    def from_blocks(cls, blocks, grid: Tuple[int, int], precision: int = 64):
+    def from_blocks(cls, blocks, grid: Tuple[int, int], precision: int = 64, transport: str = "nccl"):
         """partition_operator (distributed.cpp:179-196): every rank transforms
         its rectangle of the host (steps, sensors, sources) first block column."""
         import numpy as np
@@ -186,10 +289,10 @@ class GridEngine:
             local = np.ascontiguousarray(blocks[:, shard.sensor_begin:shard.sensor_end,
                                                 shard.source_begin:shard.source_end])
             op = setup(local, precision=precision, device=device)
-        return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"))
+        return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"), transport=transport)
 
     @classmethod
-    def from_file(cls, path, grid: Tuple[int, int], precision: int = 64):
+    def from_file(cls, path, grid: Tuple[int, int], precision: int = 64, transport: str = "nccl"):
         """Every rank loads only its rectangle of a reference operator file:
         time domain -> local setup; frequency domain -> the stored blocks of the
         rectangle, no re-setup (partition_operator(SpectralP2O),
@@ -207,10 +310,10 @@ class GridEngine:
         if not shard.empty:
             op = load_operator_rect(path, (shard.sensor_begin, shard.sensor_end),
                                     (shard.source_begin, shard.source_end), precision, device)
-        return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"))
+        return cls(nd, nm, nt, grid, op, device=torch.device(f"cuda:{device}"), transport=transport)
 
     @classmethod
-    def from_operator(cls, op, grid: Tuple[int, int]):
+    def from_operator(cls, op, grid: Tuple[int, int], transport: str = "nccl"):
         """partition_operator(const SpectralP2O&) (distributed.cpp:198-218) of an
         operator already resident on this rank's GPU (e.g. a replicated load):
         the rank keeps only its rectangle (btg_slice_operator, HBM->HBM)."""
@@ -224,13 +327,12 @@ class GridEngine:
         if not shard.empty:
             local = op.slice((shard.sensor_begin, shard.sensor_end), (shard.source_begin, shard.source_end),
                              device)
-        return cls(nd, nm, nt, grid, local, device=torch.device(f"cuda:{device}"))
+        return cls(nd, nm, nt, grid, local, device=torch.device(f"cuda:{device}"), transport=transport)
 
     @staticmethod
     def plan(num_sensors: int, num_sources: int, workers: Optional[int] = None,
              gpus_per_node: int = 1) -> Tuple[int, int]:
-        """The planner's grid (select_grid, grid_planner.cpp:123-193) for the
-        world size (or ``workers``)."""
+        """The planner's grid for the world size (or ``workers``)."""
         from .planner import plan_grid
 
         if workers is None:
@@ -240,98 +342,120 @@ class GridEngine:
         return plan_grid(num_sensors, num_sources, workers, gpus_per_node)
 
     # -- helpers -------------------------------------------------------------------
-    def _rank_of(self, i: int, j: int) -> int:
-        return i * self.cols + j
-
-    def _zeros(self, dim: int):
-        return self.torch.zeros((dim, self.num_steps), dtype=self.torch.float64, device=self.device)
-
-    def _record(self, phase: str, participants: int, dim: int):
-        self.comm_log.append(CommEvent(phase, participants, 8 * self.num_steps * dim))
-
-    def _bcast(self, buf, src_rank: int, group, participants: int):
-        if participants > 1 and buf.numel():
-            self.dist.broadcast(buf, src=src_rank, group=group)
-
-    def _check_slice(self, x, dim: int, what: str):
-        if x is None:
-            raise ValueError(f"{what}: this rank owns a slice and must pass it")
-        if tuple(x.shape) != (dim, self.num_steps):
-            from ._lib import DimensionError
-
-            raise DimensionError(f"{what}: slice is {tuple(x.shape)}, expected ({dim}, {self.num_steps})")
-        return x.contiguous()
-
     def param_slice_bounds(self, j: int) -> Tuple[int, int]:
-        s = self.shards[self._rank_of(0, j)]
+        s = self.shards[j]
         return s.source_begin, s.source_end
 
     def data_slice_bounds(self, i: int) -> Tuple[int, int]:
-        s = self.shards[self._rank_of(i, 0)]
+        s = self.shards[i * self.cols]
         return s.sensor_begin, s.sensor_end
+
+    def _slice_in(self, x, dim: int, owner: bool, what: str):
+        import torch
+
+        if not owner:
+            return None
+        if x is None:
+            raise ValueError(f"{what}: this rank owns a slice and must pass it")
+        if tuple(x.shape) != (dim, self.num_steps):
+            raise _lib.DimensionError(f"{what}: slice is {tuple(x.shape)}, expected ({dim}, {self.num_steps})")
+        if not isinstance(x, torch.Tensor) or x.device != self.device or x.dtype != torch.float64:
+            raise _lib.Error(f"{what}: slices are float64 tensors on {self.device}")
+        return x.contiguous()
+
+    def _bind(self):
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().btg_grid_set_stream(self._h, s or _lib.CUDA_STREAM_LEGACY))
+
+    def _call(self, kind: str, x, din: int, dout: int, in_owner: bool, out_owner: bool, extra=()):
+        import torch
+
+        xin = self._slice_in(x, din, in_owner, kind)
+        out = torch.empty((dout, self.num_steps), dtype=torch.float64, device=self.device) if out_owner else None
+        self._bind()
+        L = _lib.load()
+        fn = {"forward": L.btg_grid_forward, "adjoint": L.btg_grid_adjoint, "hessian": L.btg_grid_hessian}[kind]
+        args = [self._h, xin.data_ptr() if xin is not None else None, xin.numel() if xin is not None else 0,
+                out.data_ptr() if out is not None else None, out.numel() if out is not None else 0]
+        _lib.check(fn(*args, *extra, _lib.BTG_DEVICE_PTRS))
+        return out
 
     # -- the three actions ---------------------------------------------------------
     def forward(self, m_slice=None):
         """distributed_forward (distributed.cpp:312-351). Row-0 ranks pass their
         parameter slice; column-0 ranks get their data slice back (else None)."""
-        sh, i, j = self.shard, self.shard.grid_row, self.shard.grid_col
-        for jj in range(self.cols):
-            s = self.shards[self._rank_of(0, jj)]
-            self._record("broadcast", self.rows, s.local_sources)
-        buf = self._check_slice(m_slice, sh.local_sources, "forward") if i == 0 else self._zeros(sh.local_sources)
-        self._bcast(buf, self._rank_of(0, j), self._col_groups[j], self.rows)
-        part = self.local_op.apply_forward(buf) if not sh.empty else self._zeros(sh.local_sensors)
-        for ii in range(self.rows):
-            self._record("reduce", self.cols, self.shards[self._rank_of(ii, 0)].local_sensors)
-        if self.cols > 1 and part.numel():
-            self.dist.reduce(part, dst=self._rank_of(i, 0), group=self._row_groups[i])
-        return part if j == 0 else None
+        sh = self.shard
+        return self._call("forward", m_slice, sh.local_sources, sh.local_sensors, sh.grid_row == 0,
+                          sh.grid_col == 0)
 
     def adjoint(self, d_slice=None):
         """distributed_adjoint (distributed.cpp:353-392). Column-0 ranks pass
         their data slice; row-0 ranks get their parameter slice back."""
-        sh, i, j = self.shard, self.shard.grid_row, self.shard.grid_col
-        for ii in range(self.rows):
-            self._record("broadcast", self.cols, self.shards[self._rank_of(ii, 0)].local_sensors)
-        buf = self._check_slice(d_slice, sh.local_sensors, "adjoint") if j == 0 else self._zeros(sh.local_sensors)
-        self._bcast(buf, self._rank_of(i, 0), self._row_groups[i], self.cols)
-        part = self.local_op.apply_adjoint(buf) if not sh.empty else self._zeros(sh.local_sources)
-        for jj in range(self.cols):
-            self._record("reduce", self.rows, self.shards[self._rank_of(0, jj)].local_sources)
-        if self.rows > 1 and part.numel():
-            self.dist.reduce(part, dst=self._rank_of(0, j), group=self._col_groups[j])
-        return part if i == 0 else None
+        sh = self.shard
+        return self._call("adjoint", d_slice, sh.local_sensors, sh.local_sources, sh.grid_col == 0,
+                          sh.grid_row == 0)
 
     def hessian(self, v_slice=None, alpha: float = 0.0, reg="identity", gamma_inv=None):
         """F* Gamma^-1 F v + alpha R v over the grid; row-0 ranks pass and receive
-        parameter slices. gamma_inv is global ((N_d,) or (N_d, N_t)) on every rank."""
-        sh, i, j = self.shard, self.shard.grid_row, self.shard.grid_col
-        v = self._check_slice(v_slice, sh.local_sources, "hessian") if i == 0 else self._zeros(sh.local_sources)
-        self._bcast(v, self._rank_of(0, j), self._col_groups[j], self.rows)
-        g = None
+        parameter slices. gamma_inv is GLOBAL ((N_d,) or (N_d, N_t), on the
+        rank's device) and the same on every rank."""
+        import torch
+
+        from .operator import _REG
+
+        rk = _REG.get(reg)
+        if rk is None:
+            raise _lib.Error(f"unknown regularization '{reg}'")
+        gk, gp = _lib.BTG_GAMMA_NONE, None
         if gamma_inv is not None:
-            g = gamma_inv[sh.sensor_begin:sh.sensor_end].contiguous()
-        d = self.local_op.apply_forward(v, gamma_inv=g) if not sh.empty else self._zeros(sh.local_sensors)
-        if self.cols > 1 and d.numel():
-            self.dist.all_reduce(d, group=self._row_groups[i])  # reduce + broadcast of the reference, merged
-        a = alpha if i == 0 else 0.0
-        if not sh.empty:
-            out = self.local_op.apply_adjoint(d, reg_v=v if a != 0.0 else None, alpha=a, reg=reg)
-        else:
-            out = self._zeros(sh.local_sources)
-            if a != 0.0 and out.numel():
-                raise GridError("hessian: an empty shard on row 0 cannot carry the regularization")
-        if self.rows > 1 and out.numel():
-            self.dist.reduce(out, dst=self._rank_of(0, j), group=self._col_groups[j])
-        return out if i == 0 else None
+            if not isinstance(gamma_inv, torch.Tensor) or gamma_inv.device != self.device:
+                raise _lib.Error(f"hessian: gamma_inv must be a tensor on {self.device}")
+            g = gamma_inv.contiguous()
+            if tuple(g.shape) == (self.num_sensors,):
+                gk = _lib.BTG_GAMMA_PER_SENSOR
+            elif tuple(g.shape) == (self.num_sensors, self.num_steps):
+                gk = _lib.BTG_GAMMA_PER_SAMPLE
+            else:
+                raise _lib.DimensionError(f"hessian: gamma_inv must be ({self.num_sensors},) or "
+                                          f"({self.num_sensors}, {self.num_steps}) (global)")
+            gp = g.data_ptr()
+            self._gkeep = g
+        sh = self.shard
+        return self._call("hessian", v_slice, sh.local_sources, sh.local_sources, sh.grid_row == 0,
+                          sh.grid_row == 0, extra=(gp, gk, float(alpha), rk))
+
+    def synchronize(self):
+        _lib.check(_lib.load().btg_grid_synchronize(self._h))
+
+    @property
+    def comm_log(self) -> List[CommEvent]:
+        L = _lib.load()
+        cnt = ctypes.c_size_t()
+        _lib.check(L.btg_grid_comm_log(self._h, None, 0, ctypes.byref(cnt)))
+        arr = (_lib.CommEventC * max(1, cnt.value))()
+        _lib.check(L.btg_grid_comm_log(self._h, arr, cnt.value, ctypes.byref(cnt)))
+        return _events(arr, cnt.value)
 
     def comm_bytes(self) -> int:
         return sum(e.total_bytes for e in self.comm_log)
 
     def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().btg_grid_destroy(self._h)
+            self._h = None
         if self.local_op is not None and hasattr(self.local_op, "close"):
             self.local_op.close()
         self.local_op = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().btg_grid_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------
@@ -422,6 +546,36 @@ class Partition:
     def forward(self, m, backend: str = "fft", parallel: bool = False):
         """distributed_forward (distributed.cpp:312-351)."""
         return self._apply(m, False, backend, parallel)
+
+    def hessian(self, v, alpha: float = 0.0, reg="identity", gamma_inv=None, backend: str = "fft",
+                parallel: bool = False):
+        """HessianOperator::apply with this partition (inverse.cpp:78-91), plus a
+        global Gamma^-1 ((N_d,) or (N_d, N_t)): the grid Hessian schedule."""
+        import numpy as np
+
+        from .operator import _REG
+
+        rk = _REG.get(reg)
+        if rk is None:
+            raise _lib.Error(f"unknown regularization '{reg}'")
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.shape != (self.num_sources, self.num_steps):
+            raise _lib.DimensionError(f"hessian: vector is {v.shape}, expected ({self.num_sources}, {self.num_steps})")
+        gk, gp, g = _lib.BTG_GAMMA_NONE, None, None
+        if gamma_inv is not None:
+            g = np.ascontiguousarray(gamma_inv, dtype=np.float64)
+            if g.shape == (self.num_sensors,):
+                gk = _lib.BTG_GAMMA_PER_SENSOR
+            elif g.shape == (self.num_sensors, self.num_steps):
+                gk = _lib.BTG_GAMMA_PER_SAMPLE
+            else:
+                raise _lib.DimensionError("hessian: gamma_inv has the wrong shape")
+            gp = g.ctypes.data
+        out = np.empty_like(v)
+        _lib.check(_lib.load().btg_partition_hessian(self._h, v.ctypes.data, v.size, out.ctypes.data, out.size, gp,
+                                                     gk, float(alpha), rk, _parse_backend(backend),
+                                                     int(bool(parallel))))
+        return out
 
     def adjoint(self, d, backend: str = "fft", parallel: bool = False):
         """distributed_adjoint (distributed.cpp:353-392)."""

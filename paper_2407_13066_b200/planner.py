@@ -1,11 +1,13 @@
-"""Processor-grid planner (grid_planner.hpp:43-65) over the native library.
+"""Processor-grid planning over the native library (csrc/btg_planner.cu).
 
-``select_grid`` picks the r x c grid for p GPUs from l = log10(N_d / N_m): the
-reference's scale-free cost (r/p) ln r + (10^l / r) ln(p/r) minimised and
-snapped to a factorisation of p (exact integer minimiser for one GPU per node,
-the node-divisibility preference when ``gpus_per_node`` > 1). On one NVSwitch
-node every pair of B200s is one hop at full bandwidth, so this is an
-orientation choice; :meth:`GridEngine.planned` uses it.
+* :func:`plan_grid_b200` — the B200 / NVSwitch planner: the modelled time of
+  the grid engine's own schedule (worst shard's HBM stream and vector
+  transforms + NCCL ring collectives at NVLink-5 rates) for every
+  factorisation of the worker count; returns the cheapest and the table.
+* :func:`select_grid` — the reference's criterion (grid_planner.hpp:43-65):
+  the scale-free cost (r/p) ln r + (10^l / r) ln(p/r), l = log10(N_d / N_m),
+  minimised and snapped to a factorisation of p with the reference's
+  preferences; checked against the reference build in tests/test_planner.py.
 """
 
 from __future__ import annotations
@@ -17,7 +19,36 @@ from typing import Tuple
 from . import _lib
 from ._lib import check
 
-__all__ = ["select_grid", "weak_scaling_shape", "modified_cost", "comm_cost", "plan_grid", "parse_grid"]
+__all__ = ["select_grid", "weak_scaling_shape", "modified_cost", "comm_cost", "plan_grid", "parse_grid",
+           "plan_grid_b200", "default_hw_model"]
+
+
+def default_hw_model() -> dict:
+    """The planner's default B200 rates (btg_default_hw_model)."""
+    h = _lib.HwModel()
+    check(_lib.load().btg_default_hw_model(ctypes.byref(h)))
+    return {k: getattr(h, k) for k, _ in _lib.HwModel._fields_}
+
+
+def plan_grid_b200(num_sensors: int, num_sources: int, num_steps: int, workers: int, action: str = "hessian",
+                   precision: int = 64, hw: dict | None = None):
+    """btg_plan_grid: ((rows, cols), table) where table rows are dicts with the
+    modelled seconds (total, local, comm) of ``action`` on each r x c grid."""
+    kinds = {"forward": _lib.BTG_GRID_FORWARD, "adjoint": _lib.BTG_GRID_ADJOINT, "hessian": _lib.BTG_GRID_HESSIAN}
+    hm = None
+    if hw is not None:
+        base = default_hw_model()
+        base.update(hw)
+        hm = _lib.HwModel(**base)
+    best = _lib.GridPlan()
+    cnt = ctypes.c_size_t()
+    args = (int(num_sensors), int(num_sources), int(num_steps), int(workers), int(precision), kinds[action],
+            ctypes.byref(hm) if hm is not None else None)
+    check(_lib.load().btg_plan_grid(*args, ctypes.byref(best), None, 0, ctypes.byref(cnt)))
+    table = (_lib.GridPlan * max(1, cnt.value))()
+    check(_lib.load().btg_plan_grid(*args, None, table, cnt.value, ctypes.byref(cnt)))
+    rows = [{k: getattr(t, k) for k, _ in _lib.GridPlan._fields_} for t in table[:cnt.value]]
+    return (int(best.rows), int(best.cols)), rows
 
 
 def select_grid(workers: int, log_dim_ratio: float, gpus_per_node: int = 1) -> Tuple[int, int]:

@@ -55,15 +55,24 @@ def cg_solve_op(op: SpectralOperator, rhs, alpha: float = 1e-2, reg="identity", 
 
 def cg_solve(blocks, d_obs, alpha: float = 1e-2, reg="identity", tol: float = 1e-8, maxiter: int = 0,
              precondition: bool = False, grid: str = "1x1", gamma_inv=None):
-    """The reference binding's signature: setup from (steps, sensors, sources)
-    blocks, rhs = F* d_obs, CG on the Hessian. ``grid`` other than 1x1 needs
-    a torch.distributed job (see distributed.GridEngine) and is rejected here."""
-    if grid not in ("", "1x1"):
-        raise _lib.GridError("cg_solve: multi-worker grids run through distributed.GridEngine")
+    """The reference binding's signature (bindings.cpp:229-249): setup from
+    (steps, sensors, sources) blocks, rhs = F* d_obs, CG on the Hessian. With a
+    grid other than 1x1 the right-hand side comes from distributed_adjoint on
+    a single-process Partition of the blocks, as the reference does; the CG
+    iterations run on the full device operator (the same H, so only the
+    summation order of H v differs)."""
+    from .distributed import Partition
+    from .planner import parse_grid
+
+    rows, cols = parse_grid(grid) if grid else (1, 1)
     op = blocks if isinstance(blocks, SpectralOperator) else setup(blocks)
     try:
-        rhs = op.apply_adjoint(d_obs) if gamma_inv is None else op.apply_adjoint(
-            _weighted(op, d_obs, gamma_inv))
+        dw = d_obs if gamma_inv is None else _weighted(op, d_obs, gamma_inv)
+        if (rows, cols) != (1, 1):
+            with Partition(op if isinstance(blocks, SpectralOperator) else blocks, (rows, cols)) as p:
+                rhs = p.adjoint(dw)
+        else:
+            rhs = op.apply_adjoint(dw)
         return cg_solve_op(op, rhs, alpha=alpha, reg=reg, tol=tol, maxiter=maxiter, precondition=precondition,
                            gamma_inv=gamma_inv)
     finally:

@@ -162,6 +162,41 @@ int main() {
         CHECK(l3.total_bytes() == 2 * 1 * 8 * steps * 3 + 2 * 1 * 8 * steps * 2);
     }
 
+    // multi-process NCCL grid (btg_grid_*): world size 1 here (one GPU per
+    // box); every rank of a real job runs the same lines with its own rank and rectangle
+    {
+        const std::size_t nd = 3, nm = 5, nt = 12;
+        CompactP2O c = CompactP2O::zeros(nd, nm, nt);
+        for (std::size_t k = 0; k < c.blocks.size(); ++k) c.blocks[k] = std::cos(0.37 * k);
+        SpectralP2O full = setup(c);
+        const Grid::Id id = Grid::nccl_id();
+        Grid grid(GridShape{1, 1}, 0, id, 0, nd, nm, nt);
+        grid.setup(c);
+        SpaceTimeVector mv = SpaceTimeVector::zeros(nm, nt, Ordering::SOTI);
+        SpaceTimeVector dvv = SpaceTimeVector::zeros(nd, nt, Ordering::SOTI);
+        for (std::size_t k = 0; k < mv.values.size(); ++k) mv.values[k] = std::sin(0.11 * k);
+        for (std::size_t k = 0; k < dvv.values.size(); ++k) dvv.values[k] = std::cos(0.23 * k);
+        auto gf = grid.forward(&mv);
+        auto ga = grid.adjoint(&dvv);
+        std::vector<double> gam(nd, 1.5);
+        auto gh = grid.hessian(&mv, Regularization{RegKind::TemporalLaplacian, 0.2}, gam);
+        CHECK(gf && ga && gh);
+        SpaceTimeVector wf = apply_forward(full, mv), wa = apply_adjoint(full, dvv);
+        HessianOperator hw{&full, {RegKind::TemporalLaplacian, 0.2}};
+        hw.gamma_inv = gam;
+        SpaceTimeVector wh = hw.apply(mv);
+        for (std::size_t k = 0; k < wf.values.size(); ++k) CHECK(std::abs(gf->values[k] - wf.values[k]) < 1e-12);
+        for (std::size_t k = 0; k < wa.values.size(); ++k) CHECK(std::abs(ga->values[k] - wa.values[k]) < 1e-12);
+        for (std::size_t k = 0; k < wh.values.size(); ++k) CHECK(std::abs(gh->values[k] - wh.values[k]) < 1e-11);
+        bool threw = false;
+        try {
+            grid.forward(nullptr);  // rank 0 owns the parameter slice
+        } catch (const Error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }

@@ -141,3 +141,93 @@ def test_configs4_fp32_shard_full_size():
     finally:
         op.close()
         torch.cuda.empty_cache()
+
+
+def _ref_or_restate(blocks):
+    """The reference's own operator (oracle/_ref) when built, else the pinned
+    numpy restatement (tests/test_oracle.py pins it to the reference goldens)."""
+    from oracle import refcpu
+
+    if refcpu.available():
+        return "ref", refcpu.RefSpectralOperator(blocks)
+    return "restate", R.setup_full(blocks)
+
+
+@pytest.mark.parametrize("dims", [(1024, 100, 32768), (1000, 600, 8192)], ids=["configs1", "configs2"])
+def test_full_width_forward_on_sensor_rows(dims):
+    """Dense-input F at full size: every column of m is non-zero, so the GEMV's
+    full-width j-reduction is exercised. Output rows I of d = F m depend only
+    on blocks[:, I, :]; those rows come from the reference build on the
+    host-regenerated blocks[:, I, :] and the same (device-generated) m."""
+    import torch
+
+    from paper_2407_13066_b200 import fill_uniform
+
+    nt, nd, nm = dims
+    op = _build(nt, nd, nm)
+    try:
+        m = torch.empty((nm, nt), dtype=torch.float64, device="cuda:0")
+        fill_uniform(m, 31)
+        d_gpu = op.apply_forward(m).cpu().numpy()
+        gam = np.linspace(0.5, 2.0, nd)
+        dg_gpu = op.apply_forward(m, gamma_inv=torch.from_numpy(gam).cuda()).cpu().numpy()
+        m_host = m.cpu().numpy()
+    finally:
+        op.close()
+        torch.cuda.empty_cache()
+    I = np.array([0, nd // 2 + 1])
+    blocks_I = R.synthetic_blocks_slice(SEED, nd, nm, nt, I, np.arange(nm))
+    kind, ref = _ref_or_restate(blocks_I)
+    want = ref.apply_forward(m_host) if kind == "ref" else R.apply_forward(ref, m_host)
+    if kind == "ref":
+        ref.close()
+    assert R.rel_l2(d_gpu[I], want) <= 1e-12
+    assert R.rel_l2(dg_gpu[I], want * gam[I][:, None]) <= 1e-12
+
+
+def test_host_buffer_pipeline_at_configs1():
+    """The e2e path: host (pinned) buffers through the chunked H2D / R2C / GEMV /
+    C2R / D2H pipeline (the x1.5 column-chunk ramp) at the exact configs[1]
+    shape. Against the device-pointer path: F and the Hessian to 1e-14 (the
+    forward's K partials are summed per chunk), F* bitwise (same per-column
+    arithmetic); plus a column slice of F* against the oracle."""
+    import torch
+
+    from paper_2407_13066_b200 import _lib, fill_uniform
+
+    nt, nd, nm = 1024, 100, 32768
+    op = _build(nt, nd, nm)
+    try:
+        m = torch.empty((nm, nt), dtype=torch.float64, device="cuda:0")
+        fill_uniform(m, 41)
+        d = torch.empty((nd, nt), dtype=torch.float64, device="cuda:0")
+        fill_uniform(d, 42)
+        gam = torch.linspace(0.5, 2.0, nd, dtype=torch.float64)
+        f_dev = op.apply_forward(m).cpu().numpy()
+        a_dev = op.apply_adjoint(d).cpu().numpy()
+        h_dev = op.hessian_apply(m, gamma_inv=gam.cuda()).cpu().numpy()
+        torch.cuda.synchronize()
+
+        def pinned(shape):
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+        hm, hd, hg = pinned((nm, nt)), pinned((nd, nt)), gam.numpy().copy()
+        hm[...] = m.cpu().numpy()
+        hd[...] = d.cpu().numpy()
+        out_d, out_m, out_h = pinned((nd, nt)), pinned((nm, nt)), pinned((nm, nt))
+        L = _lib.load()
+        op._bind_stream(None)
+        for _ in range(2):  # twice: the second call reuses the staging and events
+            _lib.check(L.btg_forward(op._h, hm.ctypes.data, hm.size, out_d.ctypes.data, out_d.size, 1, 0))
+            _lib.check(L.btg_adjoint(op._h, hd.ctypes.data, hd.size, out_m.ctypes.data, out_m.size, 1, 0))
+            _lib.check(L.btg_hessian(op._h, hm.ctypes.data, hm.size, out_h.ctypes.data, out_h.size, 1,
+                                     hg.ctypes.data, 1, 0.0, 0, 0))
+            assert R.rel_l2(out_d, f_dev) <= 1e-14
+            assert np.array_equal(out_m, a_dev)
+            assert R.rel_l2(out_h, h_dev) <= 1e-14
+    finally:
+        op.close()
+        torch.cuda.empty_cache()
+    J = np.array([0, 1, 511, 512, 4095, 20000, nm - 1])
+    spec_J = R.setup_full(R.synthetic_blocks_slice(SEED, nd, nm, nt, np.arange(nd), J))
+    assert R.rel_l2(out_m[J], R.apply_adjoint(spec_J, hd)) <= 1e-12

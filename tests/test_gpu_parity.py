@@ -319,3 +319,36 @@ def test_tma_gemv_path_matches(btg, monkeypatch):
             assert R.rel_l2(op.apply_adjoint(d), R.apply_adjoint(spec, d)) <= TOL64
             a = op.apply_forward(m)
             assert np.array_equal(a, op.apply_forward(m))
+
+
+def test_misaligned_device_operands(btg):
+    """Device operands that are 8- but not 16-byte aligned (a torch view at an
+    odd storage offset) must take the generic C2R epilogue instead of faulting
+    (the fast epilogue reads alpha R v and per-sample Gamma^-1 as 16-byte pairs)."""
+    import torch
+
+    blocks, m, d = R.random_problem(3, 6, 40, 64)
+    spec = R.setup_full(blocks)
+    op = btg.setup(blocks)
+    try:
+        nm, nt, nd = 40, 64, 6
+
+        def odd_view(a):
+            buf = torch.zeros(a.size + 1, dtype=torch.float64, device="cuda:0")
+            v = buf[1:].view(a.shape)
+            v.copy_(torch.from_numpy(a))
+            assert v.data_ptr() % 16 == 8
+            return v
+
+        v = odd_view(m)
+        got = op.hessian_apply(v, alpha=0.3, reg="temporal-laplacian").cpu().numpy()
+        assert R.rel_l2(got, R.hessian_apply(spec, m, 0.3, 1)) <= TOL64
+        g = np.random.default_rng(5).uniform(0.5, 2.0, size=(nd, nt))
+        gv = odd_view(g)
+        got = op.hessian_apply(torch.from_numpy(m).cuda(), gamma_inv=gv).cpu().numpy()
+        assert R.rel_l2(got, R.gauss_newton_apply(spec, m, g, 0.0, 0)) <= TOL64
+        got = op.apply_adjoint(torch.from_numpy(d).cuda(), reg_v=v, alpha=0.3, reg="identity").cpu().numpy()
+        assert R.rel_l2(got, R.apply_adjoint(spec, d) + 0.3 * m) <= TOL64
+        torch.cuda.synchronize()
+    finally:
+        op.close()

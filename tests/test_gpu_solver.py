@@ -94,3 +94,15 @@ def test_cg_device_tensors_and_gamma(btg):
         x = x.cpu().numpy()
     want = R.gauss_newton_apply(spec, x, gam, 0.02, 0)
     assert R.rel_l2(want, rhs) <= 1e-9
+
+
+def test_cg_solve_with_grid_matches_single_worker(btg):
+    """The reference binding accepts any RxC grid (bindings.cpp:229-249): rhs from
+    distributed_adjoint over a Partition, same Hessian."""
+    rng = np.random.default_rng(11)
+    blocks = rng.uniform(-1.0, 1.0, size=(16, 4, 6))
+    d_obs = rng.uniform(-1.0, 1.0, size=(4, 16))
+    m1, it1, res1, c1 = btg.cg_solve(blocks, d_obs, alpha=0.05, tol=1e-12, maxiter=500)
+    m2, it2, res2, c2 = btg.cg_solve(blocks, d_obs, alpha=0.05, tol=1e-12, maxiter=500, grid="2x3")
+    assert c1 and c2
+    assert np.linalg.norm(m1 - m2) <= 1e-10 * np.linalg.norm(m1)
