@@ -216,8 +216,36 @@ def cpu_reference_sample(nt, nd, nm_sample, steps, warmup):
     return {k: min(v) for k, v in per_op.items()}, cores, p, setup_s
 
 
+def host_cpu_info():
+    """the host the CPU baseline ran on (model, logical CPUs,
+    the cores this process may use)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for ln in Path("/proc/cpuinfo").read_text().splitlines():
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except Exception:
+        affinity = None
+    return {"model_name": model, "nproc": os.cpu_count(), "affinity_cores": affinity}
+
+
 def cpu_line(nt, nd, nm_full, steps, warmup, nm_sample=CPU_SAMPLE_NM):
     secs, cores, p, setup_s = cpu_reference_sample(nt, nd, nm_sample, steps, warmup)
+    host = host_cpu_info()
     b = alg_bytes(nt, nd, nm_sample)
     step_s = secs["F"] + secs["F*"] + secs["H"]
     tbps = (b["F"] + b["F*"] + b["H"]) / step_s / 1e12
@@ -230,9 +258,16 @@ def cpu_line(nt, nd, nm_full, steps, warmup, nm_sample=CPU_SAMPLE_NM):
                    f"of N_t={nt} N_d={nd} (full N_m={nm_full}); distributed_forward/adjoint + HessianOperator on "
                    f"GridShape{{1,{p}}} ExecutionPolicy::Parallel; best of {steps} after {warmup} warm-up; "
                    f"per-op s {json.dumps({k: round(v, 4) for k, v in secs.items()})}; "
-                   f"extrapolated full-N_m step {step_s * nm_full / nm_sample:.2f} s"),
+                   f"extrapolated full-N_m step {step_s * nm_full / nm_sample:.2f} s; FFTW3 is absent from the "
+                   f"image, so the reference's fft.hpp is served by oracle/ref_fft_shim.cpp (mixed-radix Stockham)"),
         "setup_s": setup_s,
         "step_s_sample": step_s,
+        "host": host,
+        "fft": "oracle/ref_fft_shim.cpp (FFTW3 absent; the reference's fft.hpp contract, fft.cpp:17-46)",
+        "nm_sample": nm_sample,
+        "nm_full": nm_full,
+        "nm_ratio": nm_full / nm_sample,
+        "rate_basis": "algorithmic TB/s of the sample; both arms scale linearly in N_m (acceptance.cpp:293-309)",
     }
 
 
@@ -248,8 +283,9 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic uniform(-1,1) (numpy default_rng(7))",
         "config": {"workload": cfg["label"] + f" — CPU sample N_m={CPU_SAMPLE_NM}", "N_t": cfg["nt"],
-                   "N_d": cfg["nd"], "N_m": CPU_SAMPLE_NM, "step": "F + F* + Hessian"},
-        "cpu_baseline": {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                   "N_d": cfg["nd"], "N_m": CPU_SAMPLE_NM, "N_m_full": cfg["nm"],
+                   "N_m_ratio": cfg["nm"] / CPU_SAMPLE_NM, "step": "F + F* + Hessian"},
+        "cpu_baseline": {k: c[k] for k in ("value", "unit", "cores", "kind", "sample", "host", "fft", "nm_ratio")},
         "e2e": {"value": c["value"], "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -660,11 +696,76 @@ def run_ours(args):
                     "scale, exact int32 level sums in TMEM; int8 F-hat slices 14 B per complex entry",
         }}
 
+    # N > 1 without --grid: every other factorisation of N on the same per-GPU
+    # workload (SURVEY §8e asks for 1xN ... Nx1), a shorter timed run each; the
+    # headline stays the planner's grid above.
+    grid_sweep = None
+    if engine is not None and not args.grid and not args.no_grid_sweep:
+        engine.close()
+        engine = None
+        op = None
+        torch.cuda.empty_cache()
+        from paper_2407_13066_b200 import distributed as bdist
+
+        grid_sweep = {grid: {"ms_per_step": ms_step, "TB/s": value, "steps": args.steps,
+                             "ops_ms": {k: per_mean[k] for k in per_mean}}}
+        for gr2 in range(1, world + 1):
+            if world % gr2:
+                continue
+            gc2 = world // gr2
+            key = f"{gr2}x{gc2}"
+            if key == grid:
+                continue
+            nd2, nm2 = (nd_g, nm_g) if cfg.get("strong") else (cfg["nd"] * gr2, cfg["nm"] * gc2)
+            try:
+                eng2 = bdist.GridEngine.synthetic(nd2, nm2, nt, grid=(gr2, gc2), seed=1000,
+                                                  precision=cfg.get("precision", 64),
+                                                  transport="gloo" if transport == "gloo" else "nccl")
+            except Exception as exc:  # e.g. a grid wider than the operator
+                grid_sweep[key] = {"error": str(exc)}
+                continue
+            sh2 = eng2.shard
+            x2 = torch.empty((sh2.local_sources, nt), dtype=torch.float64, device=dev)
+            btg.fill_uniform(x2, seed=7)
+            y2 = torch.empty((sh2.local_sensors, nt), dtype=torch.float64, device=dev)
+            btg.fill_uniform(y2, seed=9)
+            r0, c0_ = sh2.grid_row == 0, sh2.grid_col == 0
+            g2 = torch.empty((nd2,), dtype=torch.float64, device=dev)
+            btg.fill_uniform(g2, seed=8, lo=0.5, hi=2.0)
+
+            def step2():
+                eng2.forward(x2 if r0 else None)
+                eng2.adjoint(y2 if c0_ else None)
+                eng2.hessian(x2 if r0 else None, gamma_inv=g2)
+
+            for _ in range(args.warmup):
+                step2()
+            k2 = max(3, min(args.steps, 5))
+            barrier()
+            a2, b2 = ev(), ev()
+            a2.record(stream)
+            for _ in range(k2):
+                step2()
+            b2.record(stream)
+            barrier()
+            tt2 = torch.tensor([a2.elapsed_time(b2)])
+            dist.all_reduce(tt2, op=dist.ReduceOp.MAX)
+            ms2 = float(tt2[0]) / k2
+            bytes2 = 0.0
+            for s_ in bdist.partition_bounds(nd2, nm2, gr2, gc2):
+                bb = alg_bytes(nt, s_.local_sensors, s_.local_sources, 1, elem=16 if prec == 64 else 8)
+                bytes2 += bb["F"] + bb["F*"] + bb["H"]
+            grid_sweep[key] = {"ms_per_step": ms2, "TB/s": bytes2 / (ms2 * 1e-3) / 1e12, "steps": k2,
+                               "N_d_global": nd2, "N_m_global": nm2}
+            eng2.close()
+            del x2, y2, g2
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and nrhs == 1:
         try:
             c = cpu_line(nt, nd, nm, steps=2, warmup=1) if nrhs == 1 else None
-            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample", "host", "fft", "nm_ratio")}
         except Exception as exc:  # the CPU leg must not kill the GPU line
             cpu = {"value": None, "unit": "TB/s", "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
@@ -695,11 +796,16 @@ def run_ours(args):
             line["alt_engines"] = alt
         if solver:
             line["solver"] = solver
+        if grid_sweep:
+            line["grid_sweep"] = grid_sweep
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    op.close() if engine is None else engine.close()
+    if engine is not None:
+        engine.close()
+    elif op is not None:
+        op.close()
     return 0
 
 
@@ -713,6 +819,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--precision", type=int, choices=[64, 32], default=None, help="F-hat precision override")
     ap.add_argument("--grid", default=None, help="RxC processor grid for N > 1 (default: the planner's pick)")
+    ap.add_argument("--no-grid-sweep", action="store_true",
+                    help="N > 1 without --grid: skip timing the other factorisations of N")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rules)")

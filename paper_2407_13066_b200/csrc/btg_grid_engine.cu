@@ -672,20 +672,26 @@ btg_status new_grid(size_t rows, size_t cols, int transport, Grid** out) {
     return BTG_OK;
 }
 
-// NCCL row / column communicators of the local cells (one group call).
+// NCCL row / column communicators of the local cells. Every rank of the parent
+// takes part in each split; the two splits run one after the other (each a
+// group call over the local cells, so a single thread can drive all the cells
+// of a local grid). A split is skipped when its groups would have one member.
 btg_status split_comms(Grid* g) {
-    if (g->rows * g->cols == 1) return BTG_OK;
-    G_NCCL(ncclGroupStart());
-    for (auto& c : g->cells) {
-        DevGuard dg(c.device);
-        ncclResult_t r = ncclCommSplit(c.world, (int)c.i, (int)c.j, &c.row, nullptr);
-        if (r == ncclSuccess) r = ncclCommSplit(c.world, (int)(g->rows + c.j), (int)c.i, &c.col, nullptr);
-        if (r != ncclSuccess) {
-            ncclGroupEnd();
-            return gfail(BTG_ENCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+    for (int round = 0; round < 2; ++round) {
+        const bool rows_split = round == 0;
+        if (rows_split ? g->cols == 1 : g->rows == 1) continue;
+        G_NCCL(ncclGroupStart());
+        for (auto& c : g->cells) {
+            DevGuard dg(c.device);
+            const ncclResult_t r = rows_split ? ncclCommSplit(c.world, (int)c.i, (int)c.j, &c.row, nullptr)
+                                              : ncclCommSplit(c.world, (int)c.j, (int)c.i, &c.col, nullptr);
+            if (r != ncclSuccess) {
+                ncclGroupEnd();
+                return gfail(BTG_ENCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+            }
         }
+        G_NCCL(ncclGroupEnd());
     }
-    G_NCCL(ncclGroupEnd());
     return BTG_OK;
 }
 

@@ -93,3 +93,31 @@ def test_reference_planner_cases():
             assert btg.modified_cost(float(r), p, float(l)) <= brute * (1 + 1e-12)
     assert btg.weak_scaling_shape(2.0, 6) == (False, (6, 1))
     assert btg.weak_scaling_shape(0.1, 6) == (False, (1, 6))
+
+
+def test_b200_planner_costs_the_schedule():
+    """btg_plan_grid: every factorisation costed, the pick is the cheapest;
+    configs[4] (N_d << N_m) goes 1 x 8; a square operator goes 2-D (the replicated
+    vector transforms shrink with both cuts); inter-node groups cost more."""
+    from paper_2407_13066_b200.planner import default_hw_model, plan_grid_b200
+
+    best, table = plan_grid_b200(256, 65536, 4096, 8, "hessian")
+    assert [(t["rows"], t["cols"]) for t in table] == [(1, 8), (2, 4), (4, 2), (8, 1)]
+    assert best == (1, 8)
+    assert min(table, key=lambda t: t["seconds"])["rows"] == best[0]
+    for t in table:
+        assert t["seconds"] == pytest.approx(t["local_seconds"] + t["comm_seconds"])
+    best_sq, tsq = plan_grid_b200(65536, 65536, 1024, 8, "hessian")
+    assert best_sq[0] > 1 and best_sq[1] > 1
+    # configs[2] weak-scaling shape at 8 GPUs (global 600 x 65536): 1 x 8, as the reference's rule
+    assert plan_grid_b200(600, 8 * 8192, 1000, 8, "forward")[0] == (1, 8)
+    # a slow inter-node link makes grids whose groups leave the NVSwitch domain dearer
+    _, t16 = plan_grid_b200(4096, 4096, 1024, 16, "hessian", hw={"gpus_per_node": 8})
+    _, t16b = plan_grid_b200(4096, 4096, 1024, 16, "hessian", hw={"gpus_per_node": 16})
+    assert sum(t["comm_seconds"] for t in t16) > sum(t["comm_seconds"] for t in t16b)
+    assert default_hw_model()["gpus_per_node"] == 8
+    # grids wider than the operator are not offered; none fits -> GridError
+    _, small = plan_grid_b200(2, 3, 8, 4, "forward")
+    assert [(t["rows"], t["cols"]) for t in small] == [(2, 2)]
+    with pytest.raises(btg.GridError):
+        plan_grid_b200(1, 1, 8, 4, "forward")
