@@ -120,6 +120,92 @@ __global__ void __launch_bounds__(kThreads) k_reg_apply_inverse(double* __restri
     }
 }
 
+// ---- device-resident CG control (btg_cg_solve's graph loop) -----------------
+// The scalars of inverse.cpp:105-156 live in device memory (CgState) so that a
+// whole iteration — Hessian, curvature, update, convergence test, beta, new
+// direction — runs without a host round trip, inside the body of a CUDA graph
+// WHILE node whose condition the check kernel clears. The arithmetic is the
+// host loop's, operation for operation (same divisions, same fixed-grid
+// reductions), so both loops produce the same bits.
+
+// x += (rho / pHp) p ; r -= (rho / pHp) hp ; partial ||r||^2. A non-positive
+// curvature leaves x and r untouched (the reference throws before updating).
+__global__ void __launch_bounds__(kThreads) k_cg_update_dev(double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ hp,
+                                                            const double* __restrict__ st, size_t n,
+                                                            double* __restrict__ partial) {
+    __shared__ double sh[kThreads / 32];
+    const double curv = st[kCgCurvature];
+    double acc = 0.0;
+    if (curv > 0.0) {
+        const double s = st[kCgRho] / curv;
+        for (size_t i = blockIdx.x * (size_t)kThreads + threadIdx.x; i < n; i += (size_t)gridDim.x * kThreads) {
+            x[i] += s * p[i];
+            const double ri = r[i] - s * hp[i];
+            r[i] = ri;
+            acc = fma(ri, ri, acc);
+        }
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// ||r||^2 from the partials, then the loop control of inverse.cpp:137-150:
+// curvature test, iteration count, relative residual, tolerance, iteration
+// cap; unpreconditioned CG also takes beta = rn2 / rho here.
+__global__ void __launch_bounds__(kThreads) k_cg_check(const double* __restrict__ partial, int count,
+                                                       double* __restrict__ st, cudaGraphConditionalHandle cond,
+                                                       int precond) {
+    __shared__ double sh[kThreads / 32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += kThreads) acc += partial[i];
+    const double rn2 = block_sum(acc, sh);
+    if (threadIdx.x != 0) return;
+    if (!(st[kCgCurvature] > 0.0)) {
+        st[kCgStatus] = kCgBadCurvature;
+        cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const double it = st[kCgIterations] + 1.0;
+    st[kCgIterations] = it;
+    st[kCgRn2] = rn2;
+    const double rel = sqrt(rn2) / st[kCgRhsNorm];
+    st[kCgRelRes] = rel;
+    if (rel <= st[kCgTol]) {
+        st[kCgStatus] = kCgConverged;
+        cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (it >= st[kCgMaxIt]) {
+        st[kCgStatus] = kCgMaxIterations;
+        cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (!precond) {
+        st[kCgBeta] = rn2 / st[kCgRho];
+        st[kCgRho] = rn2;
+    }
+}
+
+// beta = (r . z) / rho ; rho = r . z  (preconditioned CG, inverse.cpp:146-151)
+__global__ void k_cg_beta(double* __restrict__ st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && st[kCgStatus] == kCgRunning) {
+        const double rho_next = st[kCgRhoNext];
+        st[kCgBeta] = rho_next / st[kCgRho];
+        st[kCgRho] = rho_next;
+    }
+}
+
+// p = z + beta p with beta from the state (inverse.cpp:152-153)
+__global__ void __launch_bounds__(kThreads) k_xpby_dev(double* __restrict__ p, const double* __restrict__ z,
+                                                       const double* __restrict__ st, size_t n) {
+    if (st[kCgStatus] != kCgRunning) return;
+    const double beta = st[kCgBeta];
+    for (size_t i = blockIdx.x * (size_t)kThreads + threadIdx.x; i < n; i += (size_t)gridDim.x * kThreads)
+        p[i] = z[i] + beta * p[i];
+}
+
 int grid_for(size_t n) {
     const size_t want = (n + kThreads - 1) / kThreads;
     return (int)(want < (size_t)kRedBlocks ? (want ? want : 1) : kRedBlocks);
@@ -143,6 +229,28 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
 
 cudaError_t launch_xpby(double* p, const double* z, double beta, size_t n, cudaStream_t stream) {
     k_xpby<<<grid_for(n), kThreads, 0, stream>>>(p, z, beta, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_update_dev(double* x, double* r, const double* p, const double* hp, const double* st, size_t n,
+                                 double* partial, cudaStream_t stream) {
+    k_cg_update_dev<<<kRedBlocks, kThreads, 0, stream>>>(x, r, p, hp, st, n, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_check(const double* partial, double* st, cudaGraphConditionalHandle cond, int precond,
+                            cudaStream_t stream) {
+    k_cg_check<<<1, kThreads, 0, stream>>>(partial, kRedBlocks, st, cond, precond);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_beta(double* st, cudaStream_t stream) {
+    k_cg_beta<<<1, 32, 0, stream>>>(st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpby_dev(double* p, const double* z, const double* st, size_t n, cudaStream_t stream) {
+    k_xpby_dev<<<grid_for(n), kThreads, 0, stream>>>(p, z, st, n);
     return cudaGetLastError();
 }
 

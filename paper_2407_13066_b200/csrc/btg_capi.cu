@@ -114,9 +114,11 @@ struct btg_op_s {
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
+    cudaStream_t capture_stream = nullptr;  // CUDA-graph capture of the CG iteration
     cudaEvent_t ev[17] = {};              // kHostChunks + 1 chunk / ordering events
     cudaStream_t fft_stream = nullptr;   // chunk R2Cs of host-pointer forward calls
     double* pinned_scalar = nullptr;     // page-locked landing slot for solver scalars
+    double* pinned_state = nullptr;      // page-locked copy of the device CG state
     double* solver_ws[11] = {};           // CG / objective vectors, kept across calls
     size_t solver_cap[11] = {};
     cudaEvent_t ev_h2d[17] = {};          // chunk H2D done (copy stream -> fft stream)
@@ -1358,6 +1360,184 @@ btg_status hessian_dev(btg_op op, const double* vd, double* hvd, const double* g
     return pipeline(op, true, op->wt, hvd, 1, e2);
 }
 
+// CG building blocks shared by the host-driven and the graph loop.
+btg_status cg_precondition(btg_op op, const CgBuffers& b, bool lap, size_t n, double* zout, const double* rin) {
+    if (lap) {
+        BTG_CUDA(btg::launch_reg_apply_inverse(zout, rin, b.pivot, b.scratch, op->nm, (int)op->nt, op->stream));
+    } else {
+        BTG_CUDA(cudaMemcpyAsync(zout, rin, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
+    }
+    op->counters.launches++;
+    return BTG_OK;
+}
+
+btg_status cg_dot(btg_op op, const CgBuffers& b, size_t n, const double* a, const double* c, double* host) {
+    BTG_CUDA(btg::launch_dot(a, c, n, b.partial, b.scal, op->stream));
+    op->counters.launches += 2;
+    return read_scalar(op, b.scal, host);
+}
+
+btg_status cg_bad_curvature(double curvature) {
+    return fail(BTG_ESOLVER, "cg: direction of non-positive curvature, p^T H p = %g; the Hessian is "
+                             "not positive definite", curvature);
+}
+
+// inverse.cpp:118-153 driven from the host: two scalar read-backs per
+// iteration (BTG_CG_HOST_LOOP=1; the graph loop below is the default and
+// produces the same bits).
+btg_status cg_host_loop(btg_op op, const CgBuffers& b, double* x, const double* gd, int gamma_kind, double alpha,
+                        int reg_kind, bool precond, bool lap, double tol, size_t max_iterations, double rho,
+                        double rhs_norm, size_t n, btg_cg_result* result) {
+    for (size_t it = 1; it <= max_iterations; ++it) {
+        BTG_TRY(hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind));
+        double curvature = 0.0;
+        BTG_TRY(cg_dot(op, b, n, b.p, b.hp, &curvature));
+        if (!(curvature > 0.0)) return cg_bad_curvature(curvature);
+        const double step = rho / curvature;
+        double rn2 = 0.0;
+        BTG_CUDA(btg::launch_cg_update(x, b.r, b.p, b.hp, step, n, b.partial, b.scal, op->stream));
+        op->counters.launches += 2;
+        BTG_TRY(read_scalar(op, b.scal, &rn2));
+        result->iterations = it;
+        result->relative_residual = std::sqrt(rn2) / rhs_norm;
+        if (result->relative_residual <= tol) {
+            result->converged = 1;
+            break;
+        }
+        double rho_next = rn2;
+        if (precond) {
+            BTG_TRY(cg_precondition(op, b, lap, n, b.z, b.r));
+            BTG_TRY(cg_dot(op, b, n, b.r, b.z, &rho_next));
+        }
+        const double beta = rho_next / rho;
+        rho = rho_next;
+        BTG_CUDA(btg::launch_xpby(b.p, precond ? b.z : b.r, beta, n, op->stream));
+        op->counters.launches++;
+    }
+    return BTG_OK;
+}
+
+// The whole iteration loop as ONE graph launch: a WHILE conditional node whose
+// body (captured once from the same stream code) is Hessian -> p.Hp ->
+// update + ||r||^2 -> loop control (k_cg_check clears the condition on
+// convergence, the iteration cap or a non-positive curvature) -> [M^-1 r,
+// r.z, beta] -> p = z + beta p. No host round trip until the loop ends; the
+// scalars never leave the device.
+struct GraphGuard {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t e = nullptr;
+    cudaStream_t capturing = nullptr;
+    ~GraphGuard() {
+        if (capturing) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(capturing, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            cudaGetLastError();
+        }
+        if (e) cudaGraphExecDestroy(e);
+        if (g) cudaGraphDestroy(g);
+    }
+};
+
+btg_status cg_graph_loop(btg_op op, const CgBuffers& b, double* x, const double* gd, int gamma_kind, double alpha,
+                         int reg_kind, bool precond, bool lap, double tol, size_t max_iterations, double rho,
+                         double rhs_norm, size_t n, btg_cg_result* result) {
+    using namespace btg;
+    double st0[kCgStateLen] = {};
+    st0[kCgRho] = rho;
+    st0[kCgRhsNorm] = rhs_norm;
+    st0[kCgTol] = tol;
+    st0[kCgRelRes] = 1.0;
+    st0[kCgMaxIt] = (double)max_iterations;
+    st0[kCgStatus] = kCgRunning;
+    double* st = b.scal;
+    BTG_CUDA(cudaMemcpyAsync(st, st0, sizeof(st0), cudaMemcpyHostToDevice, op->stream));
+    // everything the body touches is allocated before the capture
+    BTG_TRY(grow(op->wt, op->wtcap, op->nd * op->nt));
+    BTG_TRY(ensure_spectral(op, 1));
+    BTG_CUDA(cudaStreamSynchronize(op->stream));  // st0 is a stack array
+
+    GraphGuard gg;
+    BTG_CUDA(cudaGraphCreate(&gg.g, 0));
+    cudaGraphConditionalHandle cond;
+    BTG_CUDA(cudaGraphConditionalHandleCreate(&cond, gg.g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    BTG_CUDA(cudaGraphAddNode(&node, gg.g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot capture); the graph then runs on the caller's
+    if (!op->capture_stream) BTG_CUDA(cudaStreamCreateWithFlags(&op->capture_stream, cudaStreamNonBlocking));
+    const cudaStream_t run_stream = op->stream;
+    const bool timing = op->timing;
+    op->timing = false;  // no event sync inside a capture
+    const btg_counters c0 = op->counters;
+    BTG_CUDA(cudaStreamBeginCaptureToGraph(op->capture_stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    op->stream = op->capture_stream;
+    gg.capturing = op->capture_stream;
+    btg_status s = hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind);
+    cudaError_t e = cudaSuccess;
+    if (s == BTG_OK) {
+        e = launch_dot(b.p, b.hp, n, b.partial, st + kCgCurvature, op->stream);
+        if (e == cudaSuccess) e = launch_cg_update_dev(x, b.r, b.p, b.hp, st, n, b.partial, op->stream);
+        if (e == cudaSuccess) e = launch_cg_check(b.partial, st, cond, precond ? 1 : 0, op->stream);
+        op->counters.launches += 4;
+    }
+    if (s == BTG_OK && e == cudaSuccess && precond) {
+        s = cg_precondition(op, b, lap, n, b.z, b.r);
+        if (s == BTG_OK) e = launch_dot(b.r, b.z, n, b.partial, st + kCgRhoNext, op->stream);
+        if (e == cudaSuccess) e = launch_cg_beta(st, op->stream);
+        op->counters.launches += 3;
+    }
+    if (s == BTG_OK && e == cudaSuccess) {
+        e = launch_xpby_dev(b.p, precond ? b.z : b.r, st, n, op->stream);
+        op->counters.launches++;
+    }
+    op->timing = timing;
+    op->stream = run_stream;
+    gg.capturing = nullptr;
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(op->capture_stream, &captured);
+    if (s != BTG_OK) return s;
+    BTG_CUDA(e);
+    BTG_CUDA(ec);
+    // per-iteration counters from the capture, scaled by the iterations run below
+    btg_counters delta = op->counters;
+    op->counters = c0;
+
+    BTG_CUDA(cudaGraphInstantiate(&gg.e, gg.g, 0));
+    BTG_CUDA(cudaGraphLaunch(gg.e, op->stream));
+    if (!op->pinned_state) BTG_CUDA(cudaMallocHost(&op->pinned_state, kCgStateLen * sizeof(double)));
+    BTG_CUDA(cudaMemcpyAsync(op->pinned_state, st, kCgStateLen * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+    BTG_CUDA(cudaStreamSynchronize(op->stream));
+    const double* fin = op->pinned_state;
+    const double bodies = fin[kCgIterations] + (fin[kCgStatus] == kCgBadCurvature ? 1.0 : 0.0);
+    auto scale = [&](btg_stage_counters& dst, const btg_stage_counters& d0, const btg_stage_counters& d1) {
+        dst.ops += bodies * (d1.ops - d0.ops);
+        dst.bytes += bodies * (d1.bytes - d0.bytes);
+    };
+    scale(op->counters.pad, c0.pad, delta.pad);
+    scale(op->counters.forward_fft, c0.forward_fft, delta.forward_fft);
+    scale(op->counters.reorder_in, c0.reorder_in, delta.reorder_in);
+    scale(op->counters.apply, c0.apply, delta.apply);
+    scale(op->counters.reorder_out, c0.reorder_out, delta.reorder_out);
+    scale(op->counters.inverse_fft, c0.inverse_fft, delta.inverse_fft);
+    scale(op->counters.unpad, c0.unpad, delta.unpad);
+    op->counters.launches += (uint64_t)bodies * (delta.launches - c0.launches);
+
+    result->iterations = (size_t)fin[kCgIterations];
+    if (fin[kCgIterations] > 0) result->relative_residual = fin[kCgRelRes];
+    if (fin[kCgStatus] == kCgConverged) result->converged = 1;
+    if (fin[kCgStatus] == kCgBadCurvature) return cg_bad_curvature(fin[kCgCurvature]);
+    return BTG_OK;
+}
+
 }  // namespace
 
 btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_out, size_t x_len,
@@ -1398,7 +1578,7 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
     BTG_TRY(slot(op, kSlotP, &b.p, n));
     BTG_TRY(slot(op, kSlotHp, &b.hp, n));
     BTG_TRY(slot(op, kSlotPartial, &b.partial, btg::kRedBlocks));
-    BTG_TRY(slot(op, kSlotScal, &b.scal, 4));
+    BTG_TRY(slot(op, kSlotScal, &b.scal, btg::kCgStateLen));
     const bool precond = use_reg_preconditioner != 0;
     if (precond) BTG_TRY(slot(op, kSlotZ, &b.z, n));
     double* x = dev ? x_out : nullptr;
@@ -1439,24 +1619,9 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
         BTG_CUDA(cudaMemcpyAsync(b.scratch, scr.data(), op->nt * sizeof(double), cudaMemcpyHostToDevice,
                                  op->stream));
     }
-    auto precondition = [&](double* zout, const double* rin) -> btg_status {
-        if (lap) {
-            BTG_CUDA(btg::launch_reg_apply_inverse(zout, rin, b.pivot, b.scratch, op->nm, (int)op->nt, op->stream));
-        } else {
-            BTG_CUDA(cudaMemcpyAsync(zout, rin, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
-        }
-        op->counters.launches++;
-        return BTG_OK;
-    };
-    auto dot = [&](const double* a, const double* c, double* host) -> btg_status {
-        BTG_CUDA(btg::launch_dot(a, c, n, b.partial, b.scal, op->stream));
-        op->counters.launches += 2;
-        return read_scalar(op, b.scal, host);
-    };
-
     BTG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), op->stream));
     double rhs_n2 = 0.0;
-    BTG_TRY(dot(rhs_d, rhs_d, &rhs_n2));
+    BTG_TRY(cg_dot(op, b, n, rhs_d, rhs_d, &rhs_n2));
     const double rhs_norm = std::sqrt(rhs_n2);
     btg_status status = BTG_OK;
     if (rhs_norm == 0.0) {
@@ -1465,45 +1630,22 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
         BTG_CUDA(cudaMemcpyAsync(b.r, rhs_d, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
         const double* zp = b.r;
         if (precond) {
-            BTG_TRY(precondition(b.z, b.r));
+            BTG_TRY(cg_precondition(op, b, lap, n, b.z, b.r));
             zp = b.z;
         }
         BTG_CUDA(cudaMemcpyAsync(b.p, zp, n * sizeof(double), cudaMemcpyDeviceToDevice, op->stream));
         double rho = 0.0;
-        BTG_TRY(dot(b.r, zp, &rho));
+        BTG_TRY(cg_dot(op, b, n, b.r, zp, &rho));
         if (rho <= 0.0 && precond)
             return fail(BTG_ESOLVER, "cg: preconditioned residual product r^T z = %g <= 0; regularization is not "
                                      "positive definite", rho);
         result->relative_residual = 1.0;
-        for (size_t it = 1; it <= max_iterations; ++it) {
-            BTG_TRY(hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind));
-            double curvature = 0.0;
-            BTG_TRY(dot(b.p, b.hp, &curvature));
-            if (!(curvature > 0.0)) {
-                status = fail(BTG_ESOLVER, "cg: direction of non-positive curvature, p^T H p = %g; the Hessian is "
-                                           "not positive definite", curvature);
-                break;
-            }
-            const double step = rho / curvature;
-            double rn2 = 0.0;
-            BTG_CUDA(btg::launch_cg_update(x, b.r, b.p, b.hp, step, n, b.partial, b.scal, op->stream));
-            op->counters.launches += 2;
-            BTG_TRY(read_scalar(op, b.scal, &rn2));
-            result->iterations = it;
-            result->relative_residual = std::sqrt(rn2) / rhs_norm;
-            if (result->relative_residual <= tol) {
-                result->converged = 1;
-                break;
-            }
-            double rho_next = rn2;
-            if (precond) {
-                BTG_TRY(precondition(b.z, b.r));
-                BTG_TRY(dot(b.r, b.z, &rho_next));
-            }
-            const double beta = rho_next / rho;
-            rho = rho_next;
-            BTG_CUDA(btg::launch_xpby(b.p, precond ? b.z : b.r, beta, n, op->stream));
-            op->counters.launches++;
+        if (std::getenv("BTG_CG_HOST_LOOP")) {
+            status = cg_host_loop(op, b, x, gd, gamma_kind, alpha, reg_kind, precond, lap, tol, max_iterations, rho,
+                                  rhs_norm, n, result);
+        } else {
+            status = cg_graph_loop(op, b, x, gd, gamma_kind, alpha, reg_kind, precond, lap, tol, max_iterations, rho,
+                                   rhs_norm, n, result);
         }
     }
     if (status != BTG_OK) return status;
@@ -1696,6 +1838,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->gam);
         cudaFree(op->vcopy);
         if (op->own_stream) cudaStreamDestroy(op->own_stream);
+        if (op->capture_stream) cudaStreamDestroy(op->capture_stream);
         if (op->copy_stream) {
             cudaStreamSynchronize(op->copy_stream);
             cudaStreamDestroy(op->copy_stream);
@@ -1705,6 +1848,7 @@ void btg_destroy(btg_op op) {
             cudaStreamDestroy(op->fft_stream);
         }
         if (op->pinned_scalar) cudaFreeHost(op->pinned_scalar);
+        if (op->pinned_state) cudaFreeHost(op->pinned_state);
         for (double* q : op->solver_ws) cudaFree(q);
         for (cudaEvent_t e : op->ev)
             if (e) cudaEventDestroy(e);

@@ -157,6 +157,19 @@ cudaError_t launch_dot(const double* a, const double* b, size_t n, double* parti
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* hp, double s, size_t n,
                              double* partial, double* rnorm2, cudaStream_t stream);
 cudaError_t launch_xpby(double* p, const double* z, double beta, size_t n, cudaStream_t stream);
+// Device-side CG loop (btg_cg_solve's CUDA graph WHILE body): scalars in a
+// CgState array of kCgStateLen doubles.
+enum CgStateIdx {
+    kCgRho = 0, kCgCurvature, kCgRn2, kCgRhoNext, kCgRhsNorm, kCgTol, kCgRelRes, kCgIterations, kCgMaxIt,
+    kCgStatus, kCgBeta, kCgStateLen
+};
+constexpr double kCgRunning = 0.0, kCgConverged = 1.0, kCgBadCurvature = 2.0, kCgMaxIterations = 3.0;
+cudaError_t launch_cg_update_dev(double* x, double* r, const double* p, const double* hp, const double* st, size_t n,
+                                 double* partial, cudaStream_t stream);
+cudaError_t launch_cg_check(const double* partial, double* st, cudaGraphConditionalHandle cond, int precond,
+                            cudaStream_t stream);
+cudaError_t launch_cg_beta(double* st, cudaStream_t stream);
+cudaError_t launch_xpby_dev(double* p, const double* z, const double* st, size_t n, cudaStream_t stream);
 cudaError_t launch_sub(double* y, const double* a, const double* b, size_t n, cudaStream_t stream);
 cudaError_t launch_reg_apply(double* y, const double* v, size_t rows, int nt, int kind, cudaStream_t stream);
 cudaError_t launch_reg_apply_inverse(double* x, const double* b, const double* pivot, const double* scratch,

@@ -1,0 +1,37 @@
+"""CG ms/iteration, graph loop (default) vs host loop (BTG_CG_HOST_LOOP=1), at
+configs[0] (launch-bound) and an N_m slice of configs[1]. Dev tool only."""
+import os, sys, json
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", ".."))
+import numpy as np, torch
+import paper_2407_13066_b200 as btg
+from oracle import restate as R
+
+def run(blocks, iters, reps=5):
+    out = {}
+    with btg.setup(blocks) as op:
+        nm, nt = blocks.shape[2], blocks.shape[0]
+        m = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (nm, nt))).cuda()
+        for mode in ("graph", "host"):
+            if mode == "host":
+                os.environ["BTG_CG_HOST_LOOP"] = "1"
+            else:
+                os.environ.pop("BTG_CG_HOST_LOOP", None)
+            btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=iters)
+            torch.cuda.synchronize()
+            best = 1e30
+            for _ in range(reps):
+                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(); _, it, _, _ = btg.cg_solve_op(op, m, alpha=1e-2, tol=0.0, maxiter=iters); e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1) / it)
+            out[mode] = best
+        os.environ.pop("BTG_CG_HOST_LOOP", None)
+    return out
+
+res = {}
+b0, _, _ = R.random_problem(1, 8, 256, 64)
+res["configs[0] N_t=64 N_d=8 N_m=256 (200 it)"] = run(b0, 200)
+rng = np.random.default_rng(5)
+b1 = rng.uniform(-1, 1, (1024, 100, 2048))
+res["configs[1] slice N_t=1024 N_d=100 N_m=2048 (20 it)"] = run(b1, 20)
+print(json.dumps(res, indent=1))

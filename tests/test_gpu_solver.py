@@ -106,3 +106,40 @@ def test_cg_solve_with_grid_matches_single_worker(btg):
     m2, it2, res2, c2 = btg.cg_solve(blocks, d_obs, alpha=0.05, tol=1e-12, maxiter=500, grid="2x3")
     assert c1 and c2
     assert np.linalg.norm(m1 - m2) <= 1e-10 * np.linalg.norm(m1)
+
+
+@pytest.mark.parametrize("reg,precond,gamma", [("identity", False, False), ("temporal-laplacian", True, True),
+                                               ("temporal-laplacian", False, True)])
+def test_cg_graph_loop_matches_host_loop_bitwise(btg, monkeypatch, reg, precond, gamma):
+    """The default solver runs the whole iteration loop as one CUDA graph WHILE
+    node with the scalars on the device; BTG_CG_HOST_LOOP=1 selects the loop
+    that reads pHp and ||r||^2 back every iteration. Same operations, same
+    fixed-grid reductions: identical iterates, residuals and counts."""
+    blocks, m_true, _ = R.random_problem(73, 6, 24, 48)
+    spec = R.setup_full(blocks)
+    rhs = R.apply_adjoint(spec, R.apply_forward(spec, m_true))
+    gam = np.linspace(0.5, 2.0, 6) if gamma else None
+    with btg.setup(blocks) as op:
+        outs = []
+        for host in (False, True):
+            if host:
+                monkeypatch.setenv("BTG_CG_HOST_LOOP", "1")
+            else:
+                monkeypatch.delenv("BTG_CG_HOST_LOOP", raising=False)
+            outs.append(btg.cg_solve_op(op, rhs, alpha=0.03, reg=reg, tol=1e-10, maxiter=3000,
+                                        precondition=precond, gamma_inv=gam))
+        monkeypatch.delenv("BTG_CG_HOST_LOOP", raising=False)
+        (xg, itg, resg, cg), (xh, ith, resh, ch) = outs
+        assert cg == ch
+        assert itg == ith
+        assert resg == resh
+        assert np.array_equal(xg, xh)
+        # an iteration cap stops both loops at the same iterate
+        x5g, it5g, res5g, c5g = btg.cg_solve_op(op, rhs, alpha=0.03, reg=reg, tol=1e-30, maxiter=5,
+                                                precondition=precond, gamma_inv=gam)
+        monkeypatch.setenv("BTG_CG_HOST_LOOP", "1")
+        x5h, it5h, res5h, c5h = btg.cg_solve_op(op, rhs, alpha=0.03, reg=reg, tol=1e-30, maxiter=5,
+                                                precondition=precond, gamma_inv=gam)
+        monkeypatch.delenv("BTG_CG_HOST_LOOP", raising=False)
+        assert it5g == it5h == 5 and not c5g and not c5h
+        assert res5g == res5h and np.array_equal(x5g, x5h)
