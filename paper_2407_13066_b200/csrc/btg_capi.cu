@@ -80,6 +80,28 @@ constexpr size_t kScratchCapBytes = 1ull << 30;    // global FFT scratch bound
 
 }  // namespace
 
+struct HessKey {
+    const double* v;
+    double* hv;
+    size_t nrhs;
+    const double* gamma;
+    int gamma_mode;
+    double alpha;
+    int reg_kind;
+    const void *wa, *wb, *wt, *F;
+    bool i8, no_dmma, legacy;
+    bool operator==(const HessKey& o) const {
+        return v == o.v && hv == o.hv && nrhs == o.nrhs && gamma == o.gamma && gamma_mode == o.gamma_mode &&
+               alpha == o.alpha && reg_kind == o.reg_kind && wa == o.wa && wb == o.wb && wt == o.wt && F == o.F &&
+               i8 == o.i8 && no_dmma == o.no_dmma && legacy == o.legacy;
+    }
+};
+struct HessGraph {
+    HessKey key{};
+    cudaGraphExec_t exec = nullptr;
+    btg_counters delta{};
+};
+
 struct btg_op_s {
     int device = 0;
     int precision = BTG_F64;
@@ -114,7 +136,7 @@ struct btg_op_s {
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host<->device chunks of host-pointer calls
-    cudaStream_t capture_stream = nullptr;  // CUDA-graph capture of the CG iteration
+    cudaStream_t capture_stream = nullptr;  // CUDA-graph capture (CG iteration, Hessian replay)
     cudaEvent_t ev[17] = {};              // kHostChunks + 1 chunk / ordering events
     cudaStream_t fft_stream = nullptr;   // chunk R2Cs of host-pointer forward calls
     double* pinned_scalar = nullptr;     // page-locked landing slot for solver scalars
@@ -138,6 +160,7 @@ struct btg_op_s {
     double* vcopy = nullptr;
     size_t vcap = 0;
 
+    HessGraph hess_graph;  // last device-pointer Hessian chain, replayed while its key matches
     std::vector<char> rows_ready;
     size_t rows_ready_count = 0;
 
@@ -790,6 +813,71 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
     return finish_host(op, out, dout_p, out_len, flags);
 }
 
+// Device-pointer Hessian calls replay a captured graph of the whole
+// F -> C2R(Gamma^-1) -> R2C -> F* -> C2R(alpha R v) chain (6+ launches, one
+// graph launch) when the pointers, epilogues and engine match the previous
+// call; anything else re-captures. The workspace is grown before the capture,
+// so a replay never sees a reallocated buffer (the key holds those pointers).
+void add_counters(btg_counters& dst, const btg_counters& d) {
+    auto add = [](btg_stage_counters& a, const btg_stage_counters& b) {
+        a.ops += b.ops;
+        a.bytes += b.bytes;
+    };
+    add(dst.pad, d.pad);
+    add(dst.forward_fft, d.forward_fft);
+    add(dst.reorder_in, d.reorder_in);
+    add(dst.apply, d.apply);
+    add(dst.reorder_out, d.reorder_out);
+    add(dst.inverse_fft, d.inverse_fft);
+    add(dst.unpad, d.unpad);
+    dst.launches += d.launches;
+}
+
+btg_status hessian_graph(btg_op op, const double* vd, double* hvd, size_t nrhs, const btg::C2REpilogue& e1,
+                         const btg::C2REpilogue& e2) {
+    // grow everything the chain touches before keying / capturing
+    BTG_TRY(grow(op->wt, op->wtcap, op->nd * op->nt * nrhs));
+    BTG_TRY(ensure_spectral(op, (nrhs > 1 && op->precision == BTG_F64 && !op->no_dmma) ? nrhs : 1));
+    if (op->tensor_i8 && nrhs > 1) {
+        // the int8 engine allocates lazily on first use: run it eagerly once
+        BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
+        return pipeline(op, true, op->wt, hvd, nrhs, e2);
+    }
+    const HessKey key{vd, hvd, nrhs, e1.gamma, e1.gamma_mode, e2.alpha, e2.reg_kind, op->wa, op->wb, op->wt,
+                      op->F, op->tensor_i8, op->no_dmma, op->legacy_gemv};
+    HessGraph& hg = op->hess_graph;
+    if (!hg.exec || !(hg.key == key)) {
+        if (hg.exec) cudaGraphExecDestroy(hg.exec);
+        hg.exec = nullptr;
+        if (!op->capture_stream) BTG_CUDA(cudaStreamCreateWithFlags(&op->capture_stream, cudaStreamNonBlocking));
+        const cudaStream_t run_stream = op->stream;
+        const btg_counters c0 = op->counters;
+        op->counters = btg_counters{};
+        BTG_CUDA(cudaStreamBeginCapture(op->capture_stream, cudaStreamCaptureModeRelaxed));
+        op->stream = op->capture_stream;
+        btg_status s = pipeline(op, false, vd, op->wt, nrhs, e1);
+        if (s == BTG_OK) s = pipeline(op, true, op->wt, hvd, nrhs, e2);
+        op->stream = run_stream;
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(op->capture_stream, &g);
+        hg.delta = op->counters;
+        op->counters = c0;
+        if (s != BTG_OK) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return s;
+        }
+        BTG_CUDA(ec);
+        const cudaError_t ei = cudaGraphInstantiate(&hg.exec, g, 0);
+        cudaGraphDestroy(g);
+        BTG_CUDA(ei);
+        hg.key = key;
+    }
+    BTG_CUDA(cudaGraphLaunch(hg.exec, op->stream));
+    add_counters(op->counters, hg.delta);
+    return BTG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1222,6 +1310,10 @@ btg_status btg_hessian(btg_op op, const double* v, size_t v_len, double* hv, siz
         BTG_TRY(run_c2r_vec(op, op->wb, nrhs * op->nd, op->wt, e1));
         BTG_TRY(run_r2c_vec(op, op->wt, nrhs * op->nd, op->wa));
         return host_adjoint_stage_mrhs(op, hv, nrhs, e2);
+    }
+    if ((flags & BTG_DEVICE_PTRS) && !op->timing && !std::getenv("BTG_NO_GRAPH")) {
+        BTG_TRY(hessian_graph(op, vd, hvd, nrhs, e1, e2));
+        return BTG_OK;
     }
     BTG_TRY(pipeline(op, false, vd, op->wt, nrhs, e1));
     BTG_TRY(pipeline(op, true, op->wt, hvd, nrhs, e2));
@@ -1838,6 +1930,7 @@ void btg_destroy(btg_op op) {
         cudaFree(op->gam);
         cudaFree(op->vcopy);
         if (op->own_stream) cudaStreamDestroy(op->own_stream);
+        if (op->hess_graph.exec) cudaGraphExecDestroy(op->hess_graph.exec);
         if (op->capture_stream) cudaStreamDestroy(op->capture_stream);
         if (op->copy_stream) {
             cudaStreamSynchronize(op->copy_stream);

@@ -35,3 +35,33 @@ rng = np.random.default_rng(5)
 b1 = rng.uniform(-1, 1, (1024, 100, 2048))
 res["configs[1] slice N_t=1024 N_d=100 N_m=2048 (20 it)"] = run(b1, 20)
 print(json.dumps(res, indent=1))
+
+# device-pointer Hessian call: graph replay (default) vs eager chain (BTG_NO_GRAPH=1)
+from paper_2407_13066_b200 import _lib
+L = _lib.load()
+hres = {}
+for name, blocks in (("configs[0]", b0), ("configs[1] slice N_m=2048", b1)):
+    with btg.setup(blocks) as op:
+        nt, nd, nm = blocks.shape
+        v = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, (nm, nt))).cuda()
+        out = torch.empty_like(v)
+        op._bind_stream(v)
+        for mode in ("graph", "eager"):
+            if mode == "eager":
+                os.environ["BTG_NO_GRAPH"] = "1"
+            else:
+                os.environ.pop("BTG_NO_GRAPH", None)
+            call = lambda: _lib.check(L.btg_hessian(op._h, v.data_ptr(), v.numel(), out.data_ptr(), out.numel(), 1,
+                                                    None, 0, 0.1, 1, _lib.BTG_DEVICE_PTRS))
+            for _ in range(5):
+                call()
+            torch.cuda.synchronize()
+            n = 200 if name == "configs[0]" else 20
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(n):
+                call()
+            e1.record(); torch.cuda.synchronize()
+            hres[f"{name} {mode}"] = e0.elapsed_time(e1) / n
+        os.environ.pop("BTG_NO_GRAPH", None)
+print(json.dumps({"hessian_ms_per_call": hres}, indent=1))
