@@ -952,6 +952,8 @@ btg_status btg_create(size_t nd, size_t nm, size_t nt, int precision, int device
         op->fast.hi = op->d_fast + 32;
         op->fast.post_lo = op->d_fast + 32 + hi;
         op->fast.post_hi = op->d_fast + 64 + hi;
+        op->fast.wn = op->d_tw;
+        op->fast.w2n = op->d_post;
         op->fast_ok = true;
     }
     op->no_dmma = std::getenv("BTG_DISABLE_DMMA") != nullptr;

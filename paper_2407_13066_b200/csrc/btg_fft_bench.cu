@@ -54,7 +54,13 @@ struct Run {
         double2* dt;
         CK(cudaMalloc(&dt, t.size() * sizeof(double2)));
         CK(cudaMemcpy(dt, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
-        FastTables tabs{dt, dt + 32, dt + 32 + hi, dt + 64 + hi};
+        std::vector<double2> wt(N + N + 1);
+        for (int k = 0; k < N; ++k) wt[k] = root(k, N);
+        for (int k = 0; k <= N; ++k) wt[N + k] = root(k, 2LL * N);
+        double2* dw;
+        CK(cudaMalloc(&dw, wt.size() * sizeof(double2)));
+        CK(cudaMemcpy(dw, wt.data(), wt.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        FastTables tabs{dt, dt + 32, dt + 32 + hi, dt + 64 + hi, dw, dw + N};
 
         const size_t nx = (size_t)C * N, nf = (size_t)(N + 1) * C;
         double *x, *y;
@@ -76,8 +82,8 @@ struct Run {
 #endif
         auto r2c = tma_r ? fast::k_r2c_tma<N, CPBR> : pf_r ? fast::k_r2c_pf<N, CPBR> : fast::k_r2c_fast<N, CPBR>;
         auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
-        constexpr size_t smem_r = tma_r ? fast::smem_bytes_tma<N, CPBR>() : fast::smem_bytes<N, CPBR>();
-        constexpr size_t smem_c = fast::smem_bytes<N, CPBC>();
+        constexpr size_t smem_r = tma_r ? fast::smem_bytes_tma<N, CPBR>() : fast::smem_dir<N, CPBR, true>();
+        constexpr size_t smem_c = fast::smem_dir<N, CPBC, false>();
         CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
         CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
         int occ_r = 1, occ_c = 1, sms = 148;

@@ -116,9 +116,44 @@ __device__ __forceinline__ double2 tw_lookup(const double2* lo, const double2* h
     return w;
 }
 
-template <int R, int SIGN>
+// dft4 of (a, b, 0, 0): the zero-padded half of an R2C first pass
+template <int SIGN>
+__device__ __forceinline__ void dft4_half(double2* v) {
+    const double2 a = v[0], b = v[1], c = mul_si<SIGN>(v[1]);
+    v[0] = cadd(a, b);
+    v[1] = cadd(a, c);
+    v[2] = csub(a, b);
+    v[3] = csub(a, c);
+}
+
+// HALF: inputs v[q], q >= R/2, are zero and never read (the R2C zero pad);
+// the first butterfly stage then skips the additions of zeros — IEEE x + 0
+// cannot be folded by the compiler, so these were real DADDs before.
+template <int R, int SIGN, bool HALF = false>
 __device__ __forceinline__ void dft(double2* v) {
-    if constexpr (R == 2) dft2<SIGN>(v);
+    if constexpr (HALF && R == 4) dft4_half<SIGN>(v);
+    else if constexpr (HALF && R == 8) {
+        double2 e[4] = {v[0], v[2], {}, {}};
+        double2 o[4] = {v[1], v[3], {}, {}};
+        dft4_half<SIGN>(e);
+        dft4_half<SIGN>(o);
+        constexpr double r = 0.70710678118654752440;
+        const double2 o1 = make_double2(r * (o[1].x - SIGN * o[1].y), r * (o[1].y + SIGN * o[1].x));
+        const double2 o2 = mul_si<SIGN>(o[2]);
+        const double2 o3 = make_double2(-r * (o[3].x + SIGN * o[3].y), r * (SIGN * o[3].x - o[3].y));
+        v[0] = cadd(e[0], o[0]);
+        v[4] = csub(e[0], o[0]);
+        v[1] = cadd(e[1], o1);
+        v[5] = csub(e[1], o1);
+        v[2] = cadd(e[2], o2);
+        v[6] = csub(e[2], o2);
+        v[3] = cadd(e[3], o3);
+        v[7] = csub(e[3], o3);
+    } else if constexpr (HALF && R != 16) {
+#pragma unroll
+        for (int q = R / 2; q < R; ++q) v[q] = make_double2(0.0, 0.0);
+        dft<R, SIGN>(v);
+    } else if constexpr (R == 2) dft2<SIGN>(v);
     else if constexpr (R == 3) dft3<SIGN>(v);
     else if constexpr (R == 4) dft4<SIGN>(v);
     else if constexpr (R == 5) dft5<SIGN>(v);
@@ -129,8 +164,9 @@ __device__ __forceinline__ void dft(double2* v) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a[r][q] = v[r + 4 * q];
-            dft4<SIGN>(a[r]);
+            for (int q = 0; q < (HALF ? 2 : 4); ++q) a[r][q] = v[r + 4 * q];
+            if constexpr (HALF) dft4_half<SIGN>(a[r]);
+            else dft4<SIGN>(a[r]);
         }
         constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
         constexpr double c2 = 0.70710678118654752440;
@@ -161,15 +197,125 @@ __device__ __forceinline__ void dft(double2* v) {
     }
 }
 
+// ---- direct twiddle tables ---------------------------------------------------
+// (a) W_2N^e for e in [0, N/4] (`w2q`, one octant of the 2N circle; the rest by
+//     the symmetries W^{Q-r} = -i conj W^r and W^{qQ+r} = (-i)^q W^r, Q = N/2:
+//     integer selects, no FP64 work). Serves the R2C split / C2R pre-split
+//     twiddles and the first power of every generated pass twiddle.
+// (b) Per-pass tables [k][q] = W_N^{k q N/(NS R)} (row stride R+1: the 8
+//     distinct k of a warp hit 8 distinct bank groups) for the passes whose
+//     table fits the plan's budget (TabPlan): their R-1 twiddles become R-1
+//     shared loads (broadcast over the CPB channel lanes) instead of one lookup
+//     product and R-2 power products.
+// Largest per-pass table (entries) each direction may keep in shared memory,
+// and whether the plan uses the octant table.
+// Measured on B200 (N_t = 1024, 32768 / 524288 channels): the vector FFTs are
+// latency-bound, not FP64-bound — removing the generation products moved the
+// R2C by <= 1 % (and its extra shared memory costs the non-TMA R2C a CTA per
+// SM), the C2R gained 5 % at 32768 channels from the octant table alone; the
+// pass tables were neutral or slower. Defaults: octant table for the C2R only.
+#ifndef BTG_TAB_R2C
+#define BTG_TAB_R2C 0
+#define BTG_TAB_C2R 0
+#define BTG_TAB_W2Q_R2C 0
+#define BTG_TAB_W2Q_C2R 1
+#endif
+template <int N>
+struct TabPlan {
+    static constexpr int R2C = BTG_TAB_R2C, C2R = BTG_TAB_C2R;
+    static constexpr bool W2Q_R2C = BTG_TAB_W2Q_R2C, W2Q_C2R = BTG_TAB_W2Q_C2R;
+};
+template <int N, bool C2R>
+constexpr bool kUseW2Q = (C2R ? TabPlan<N>::W2Q_C2R : TabPlan<N>::W2Q_R2C) && (N % 4 == 0) && N <= 4096;
+template <int N, bool C2R>
+__host__ __device__ constexpr int w2q_entries() { return kUseW2Q<N, C2R> ? N / 4 + 1 : 0; }
+template <int R, int NS, int LIM>
+__host__ __device__ constexpr bool pass_tab() { return NS > 1 && NS * (R + 1) <= LIM; }
+template <int NS, int LIM, int R>
+__host__ __device__ constexpr int tab_entries(Radices<R>) { return pass_tab<R, NS, LIM>() ? NS * (R + 1) : 0; }
+template <int NS, int LIM, int R, int R2, int... Rest>
+__host__ __device__ constexpr int tab_entries(Radices<R, R2, Rest...>) {
+    return (pass_tab<R, NS, LIM>() ? NS * (R + 1) : 0) + tab_entries<NS * R, LIM>(Radices<R2, Rest...>{});
+}
+template <int N, bool R2C>
+__host__ __device__ constexpr int ptab_entries() {
+    if constexpr (R2C) return tab_entries<1, TabPlan<N>::R2C>(typename FastPlan<N>::R2C{});
+    else return tab_entries<1, TabPlan<N>::C2R>(typename FastPlan<N>::C2R{});
+}
+// entries of the tables of all passes but the last (offset of the last pass's table)
+template <int NS, int LIM, int R>
+__host__ __device__ constexpr int tab_entries_but_last(Radices<R>) { return 0; }
+template <int NS, int LIM, int R, int R2, int... Rest>
+__host__ __device__ constexpr int tab_entries_but_last(Radices<R, R2, Rest...>) {
+    return (pass_tab<R, NS, LIM>() ? NS * (R + 1) : 0) + tab_entries_but_last<NS * R, LIM>(Radices<R2, Rest...>{});
+}
+// Shared-memory bytes of a direction's kernel: channel buffers + split tables
+// (smem_bytes) + the octant table + the pass tables.
+template <int N, int CPB, bool R2C>
+__host__ __device__ constexpr size_t smem_dir() {
+    return smem_bytes<N, CPB>() + sizeof(double2) * (w2q_entries<N, !R2C>() + ptab_entries<N, R2C>());
+}
+
+template <int N, int NS, int LIM, int R>
+__device__ __forceinline__ void fill_one_tab(double2* t, const double2* wn) {
+    if constexpr (pass_tab<R, NS, LIM>()) {
+        constexpr int step = N / (NS * R);
+        for (int i = threadIdx.x; i < NS * (R + 1); i += blockDim.x) {
+            const int k = i / (R + 1), q = i % (R + 1);
+            t[i] = wn[(k * q * step) % N];
+        }
+    }
+}
+template <int N, int NS, int LIM, int R>
+__device__ __forceinline__ void fill_pass_tabs(double2* t, const double2* wn, Radices<R>) {
+    fill_one_tab<N, NS, LIM, R>(t, wn);
+}
+template <int N, int NS, int LIM, int R, int R2, int... Rest>
+__device__ __forceinline__ void fill_pass_tabs(double2* t, const double2* wn, Radices<R, R2, Rest...>) {
+    fill_one_tab<N, NS, LIM, R>(t, wn);
+    fill_pass_tabs<N, NS * R, LIM>(t + (pass_tab<R, NS, LIM>() ? NS * (R + 1) : 0), wn, Radices<R2, Rest...>{});
+}
+
+// W_2N^e, e in [0, 2N): octant table when the plan has one, else the split tables.
+template <int N, bool C2R>
+__device__ __forceinline__ double2 w2n_lookup(const double2* w2q, const double2* plo, const double2* phi, int e) {
+    if constexpr (kUseW2Q<N, C2R>) {
+        constexpr int Q = N / 2, O = N / 4;
+        const int qd = e / Q;
+        const int r = e - qd * Q;
+        const bool fold = r > O;
+        const double2 t = w2q[fold ? Q - r : r];
+        double2 w = fold ? make_double2(-t.y, -t.x) : t;  // -i conj(t)
+        if (qd & 1) w = make_double2(w.y, -w.x);        // * (-i)
+        if (qd & 2) w = make_double2(-w.x, -w.y);       // * (-1)
+        return w;
+    } else {
+        return tw_lookup<-1>(plo, phi, e);
+    }
+}
+
+// Fill the octant table and the pass tables (from the global W_N / W_2N tables).
+template <int N, int LIM, typename RL, bool C2R>
+__device__ __forceinline__ void load_direct_tables(double2* w2q, double2* ptab, const FastTables& tabs) {
+    for (int i = threadIdx.x; i < w2q_entries<N, C2R>(); i += blockDim.x) w2q[i] = tabs.w2n[i];
+    fill_pass_tabs<N, 1, LIM>(ptab, tabs.wn, RL{});
+}
+
 // Butterfly j of a radix-R pass: v[q] = s[j + q N/R] * W^{k q N/(NS R)}, k = j % NS.
 // One table lookup; the powers q = 2..R-1 are products of lower powers.
 template <int N, int R, int NS, int SIGN>
-__device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2* lo, const double2* hi) {
+__device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2* lo, const double2* hi,
+                                               const double2* w2q = nullptr) {
     if constexpr (NS > 1) {
         const int k = j % NS;
         constexpr int step = N / (NS * R);
         double2 w[R];
-        w[1] = tw_lookup<SIGN>(lo, hi, k * step);
+        if constexpr (kUseW2Q<N, (SIGN > 0)>) {
+            w[1] = w2n_lookup<N, (SIGN > 0)>(w2q, lo, hi, 2 * k * step);  // W_N^e = W_2N^{2e}
+            if (SIGN > 0) w[1].y = -w[1].y;
+        } else {
+            w[1] = tw_lookup<SIGN>(lo, hi, k * step);
+        }
 #pragma unroll
         for (int q = 2; q < R; ++q) w[q] = cmul(w[q / 2], w[q - q / 2]);
 #pragma unroll
@@ -177,9 +323,27 @@ __device__ __forceinline__ void twiddle_inputs(double2* v, int j, const double2*
     }
 }
 
+// Pass twiddles from the pass's table when it has one (LIM), else generated.
+template <int N, int R, int NS, int SIGN, int LIM>
+__device__ __forceinline__ void twiddle_pass(double2* v, int j, const double2* lo, const double2* hi,
+                                             const double2* w2q, const double2* ptab) {
+    if constexpr (pass_tab<R, NS, LIM>()) {
+        const double2* row = ptab + (j % NS) * (R + 1);
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+            double2 w = row[q];
+            if (SIGN > 0) w.y = -w.y;
+            v[q] = cmul(v[q], w);
+        }
+    } else {
+        twiddle_inputs<N, R, NS, SIGN>(v, j, lo, hi, w2q);
+    }
+}
+
 // One in-place radix-R pass over the channel buffer `s` (smem, padded).
-template <int N, int TPC, int R, int NS, int SIGN>
-__device__ __forceinline__ void pass_smem(double2* s, int tc, const double2* lo, const double2* hi) {
+template <int N, int TPC, int R, int NS, int SIGN, int LIM>
+__device__ __forceinline__ void pass_smem(double2* s, int tc, const double2* lo, const double2* hi,
+                                          const double2* w2q, const double2* ptab) {
     constexpr int NB = N / R;
     constexpr int BF = (NB + TPC - 1) / TPC;
     double2 v[BF][R];
@@ -189,7 +353,7 @@ __device__ __forceinline__ void pass_smem(double2* s, int tc, const double2* lo,
         if (NB % TPC == 0 || j < NB) {
 #pragma unroll
             for (int q = 0; q < R; ++q) v[b][q] = s[pad_idx(j + q * NB)];
-            twiddle_inputs<N, R, NS, SIGN>(v[b], j, lo, hi);
+            twiddle_pass<N, R, NS, SIGN, LIM>(v[b], j, lo, hi, w2q, ptab);
             dft<R, SIGN>(v[b]);
         }
     }
@@ -223,13 +387,17 @@ template <int R, int R2, int... Rest>
 __host__ __device__ constexpr int ns_of_last(Radices<R, R2, Rest...>) { return R * ns_of_last(Radices<R2, Rest...>{}); }
 
 // Apply every pass of the list but the last, starting at NS.
-template <int N, int TPC, int NS, int SIGN, int R>
-__device__ __forceinline__ void passes_but_last(double2*, int, const double2*, const double2*, Radices<R>) {}
-template <int N, int TPC, int NS, int SIGN, int R, int R2, int... Rest>
+// ptab: this pass's table (tables are laid out in pass order, see tab_entries).
+template <int N, int TPC, int NS, int SIGN, int LIM, int R>
+__device__ __forceinline__ void passes_but_last(double2*, int, const double2*, const double2*, const double2*,
+                                                const double2*, Radices<R>) {}
+template <int N, int TPC, int NS, int SIGN, int LIM, int R, int R2, int... Rest>
 __device__ __forceinline__ void passes_but_last(double2* s, int tc, const double2* lo, const double2* hi,
-                                                Radices<R, R2, Rest...>) {
-    pass_smem<N, TPC, R, NS, SIGN>(s, tc, lo, hi);
-    passes_but_last<N, TPC, NS * R, SIGN>(s, tc, lo, hi, Radices<R2, Rest...>{});
+                                                const double2* w2q, const double2* ptab, Radices<R, R2, Rest...>) {
+    pass_smem<N, TPC, R, NS, SIGN, LIM>(s, tc, lo, hi, w2q, ptab);
+    passes_but_last<N, TPC, NS * R, SIGN, LIM>(s, tc, lo, hi, w2q,
+                                               ptab + (pass_tab<R, NS, LIM>() ? NS * (R + 1) : 0),
+                                               Radices<R2, Rest...>{});
 }
 
 __device__ __forceinline__ void load_tables(double2* lo, double2* hi, int hi_count, const double2* g_lo,
@@ -320,6 +488,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, false>();
+    constexpr int LIM = TabPlan<N>::R2C;
+    load_direct_tables<N, LIM, RL, false>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
     const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
@@ -341,7 +514,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 #pragma unroll
                 for (int q = 0; q < R; ++q)
                     v[bf][q] = (q < R / 2 && live) ? __ldg(row + j + q * NB) : make_double2(0.0, 0.0);
-                dft<R, -1>(v[bf]);
+                dft<R, -1, true>(v[bf]);
             }
         }
 #pragma unroll
@@ -355,7 +528,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
         __syncthreads();
     }
     // ---- middle passes
-    passes_but_last<N, TPC, first_radix(RL{}), -1>(s, tc, lo, hi, tail(RL{}));
+    passes_but_last<N, TPC, first_radix(RL{}), -1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
 
     // ---- last pass on butterfly pairs (j, NB-j) + split in registers
     constexpr int R = last_radix(RL{});
@@ -377,8 +550,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
             va[q] = s[pad_idx(ja + q * NB)];
             vb[q] = s[pad_idx(jb + q * NB)];
         }
-        twiddle_inputs<N, R, NS, -1>(va, ja, lo, hi);
-        twiddle_inputs<N, R, NS, -1>(vb, jb, lo, hi);
+        twiddle_pass<N, R, NS, -1, LIM>(va, ja, lo, hi, w2q, ptab_last);
+        twiddle_pass<N, R, NS, -1, LIM>(vb, jb, lo, hi, w2q, ptab_last);
         dft<R, -1>(va);
         dft<R, -1>(vb);
         if (u != 0) {
@@ -386,7 +559,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const int k = ja + q * NB;
-                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(va[q], vb[R - 1 - q], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
@@ -403,7 +576,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 const int qp = (R - q) % R;
                 if (q > qp && q != 0) continue;
                 const int k = q * NB;
-                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(va[q], va[qp], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
@@ -419,7 +592,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 const int qp = R - 1 - q;
                 if (q > qp) continue;
                 const int k = NB / 2 + q * NB;
-                const double2 w = tw_lookup<-1>(plo, phi, k);
+                const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(vb[q], vb[qp], w, xk, xn);
                 orow[(long long)k * out_fs] = xk;
@@ -451,6 +624,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, true>();
+    constexpr int LIM = TabPlan<N>::C2R;
+    load_direct_tables<N, LIM, RL, true>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
     const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
@@ -478,7 +656,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                 for (int q = 0; q < R; ++q) {
                     const int k = ja + q * NB;  // partner N - k = jb + (R-1-q) NB
                     const double2 xk = X(k), xn = X(N - k);
-                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                     presplit_pair(xk, xn, w, inv_len, va[uf][q], vb[uf][R - 1 - q]);
                 }
             } else {
@@ -488,7 +666,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     if (q > qp && q != 0) continue;
                     const int k = q * NB;
                     const double2 xk = X(k), xn = X(N - k);  // q = 0: X_0 and X_N
-                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                     double2 zk, zn;
                     presplit_pair(xk, xn, w, inv_len, zk, zn);
                     va[uf][q] = zk;
@@ -500,7 +678,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     if (q > qp) continue;
                     const int k = NB / 2 + q * NB;
                     const double2 xk = X(k), xn = X(N - k);
-                    const double2 w = tw_lookup<-1>(plo, phi, k);
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                     double2 zk, zn;
                     presplit_pair(xk, xn, w, inv_len, zk, zn);
                     vb[uf][q] = zk;
@@ -525,7 +703,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
         __syncthreads();
     }
     // ---- middle passes
-    passes_but_last<N, TPC, first_radix(RL{}), +1>(s, tc, lo, hi, tail(RL{}));
+    passes_but_last<N, TPC, first_radix(RL{}), +1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
 
     // ---- last pass: outputs p = j + q NB; keep p < N/2 (t = 2p, 2p+1 < N)
     constexpr int R = last_radix(RL{});
@@ -558,7 +736,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
             double2 v[R];
             #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
-            twiddle_inputs<N, R, NS, +1>(v, j, lo, hi);
+            twiddle_pass<N, R, NS, +1, LIM>(v, j, lo, hi, w2q, ptab_last);
             dft<R, +1>(v);
             #pragma unroll
             for (int q = 0; q < NQ; ++q) {  // keep p = j + q*NB < N/2 (unpad)
@@ -616,6 +794,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, false>();
+    constexpr int LIM = TabPlan<N>::R2C;
+    load_direct_tables<N, LIM, RL, false>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
@@ -647,7 +830,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
             for (int bf = 0; bf < BF1; ++bf) {
 #pragma unroll
                 for (int q = 0; q < R1; ++q) v[bf][q] = q < QH ? pre[bf][q] : make_double2(0.0, 0.0);
-                dft<R1, -1>(v[bf]);
+                dft<R1, -1, true>(v[bf]);
             }
             prefetch(g + gridDim.x);
 #pragma unroll
@@ -661,7 +844,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
             __syncthreads();
         }
         // ---- middle passes
-        passes_but_last<N, TPC, R1, -1>(s, tc, lo, hi, tail(RL{}));
+        passes_but_last<N, TPC, R1, -1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
 
         // ---- last pass on butterfly pairs (j, NB-j) + split in registers
         constexpr int R = last_radix(RL{});
@@ -683,8 +866,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                     va[q] = s[pad_idx(ja + q * NB)];
                     vb[q] = s[pad_idx(jb + q * NB)];
                 }
-                twiddle_inputs<N, R, NS, -1>(va, ja, lo, hi);
-                twiddle_inputs<N, R, NS, -1>(vb, jb, lo, hi);
+                twiddle_pass<N, R, NS, -1, LIM>(va, ja, lo, hi, w2q, ptab_last);
+                twiddle_pass<N, R, NS, -1, LIM>(vb, jb, lo, hi, w2q, ptab_last);
                 dft<R, -1>(va);
                 dft<R, -1>(vb);
                 if (u != 0) {
@@ -692,7 +875,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
                         const int k = ja + q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], vb[R - 1 - q], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
@@ -709,7 +892,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         const int qp = (R - q) % R;
                         if (q > qp && q != 0) continue;
                         const int k = q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], va[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
@@ -725,7 +908,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         const int qp = R - 1 - q;
                         if (q > qp) continue;
                         const int k = NB / 2 + q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(vb[q], vb[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
@@ -764,6 +947,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     double2* phi = plo + kTwLo;
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, true>();
+    constexpr int LIM = TabPlan<N>::C2R;
+    load_direct_tables<N, LIM, RL, true>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
@@ -816,7 +1004,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
 #pragma unroll
                     for (int q = 0; q < R1; ++q) {
                         const int k = ja + q * NB1;  // partner N - k = jb + (R-1-q) NB
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                         presplit_pair(xa[uf][q], xb[uf][q], w, inv_len, va[uf][q], vb[uf][R1 - 1 - q]);
                     }
                 } else {
@@ -825,7 +1013,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                         const int qp = (R1 - q) % R1;
                         if (q > qp && q != 0) continue;
                         const int k = q * NB1;  // q = 0: X_0 and X_N
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                         double2 zk, zn;
                         presplit_pair(xa[uf][q], xb[uf][q], w, inv_len, zk, zn);
                         va[uf][q] = zk;
@@ -836,7 +1024,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                         const int qp = R1 - 1 - q;
                         if (q > qp) continue;
                         const int k = NB1 / 2 + q * NB1;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
                         double2 zk, zn;
                         presplit_pair(xc[q], xd[q], w, inv_len, zk, zn);
                         vb[uf][q] = zk;
@@ -862,7 +1050,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
             __syncthreads();
         }
         // ---- middle passes
-        passes_but_last<N, TPC, R1, +1>(s, tc, lo, hi, tail(RL{}));
+        passes_but_last<N, TPC, R1, +1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
 
         // ---- last pass: outputs p = j + q NB; keep p < N/2 (t = 2p, 2p+1 < N)
         constexpr int R = last_radix(RL{});
@@ -895,7 +1083,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     double2 v[R];
                     #pragma unroll
                     for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
-                    twiddle_inputs<N, R, NS, +1>(v, j, lo, hi);
+                    twiddle_pass<N, R, NS, +1, LIM>(v, j, lo, hi, w2q, ptab_last);
                     dft<R, +1>(v);
                     #pragma unroll
                     for (int q = 0; q < NQ; ++q) {  // keep p = j + q*NB < N/2 (unpad)
@@ -936,13 +1124,14 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
 // copy per row, mbarrier completion) into a shared staging area as soon as the
 // first pass has read the current ones, so the loads overlap the shared-memory
 // passes and the stores without costing registers. Staging rows are padded by
-// 16 bytes so the CPB channels of a warp hit different banks.
+// 32 bytes so the CPB channels of a warp hit different banks.
 // ---------------------------------------------------------------------------
 template <int N>
-__host__ __device__ constexpr int stage_stride() { return N + 2; }  // doubles per staged row
+__host__ __device__ constexpr int stage_stride() { return N + 4; }  // doubles per staged row: +32 B, so the
+// CPB channel lanes of a quarter-warp hit 8 distinct 16-byte bank groups
 template <int N, int CPB>
 __host__ __device__ constexpr size_t smem_bytes_tma() {
-    return smem_bytes<N, CPB>() + sizeof(double) * CPB * stage_stride<N>() + 16;
+    return smem_dir<N, CPB, true>() + sizeof(double) * CPB * stage_stride<N>() + 16;
 }
 // Plans that have the TMA-staged R2C, and the largest channel count it is used for:
 // measured on B200 at N_t = 1024 it wins up to ~2e5 channels (32768: 0.194 vs 0.220 ms;
@@ -993,7 +1182,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
     double2* hi = lo + kTwLo;
     double2* plo = hi + HI;
     double2* phi = plo + kTwLo;
-    double* stage = reinterpret_cast<double*>(sm) + 2 * ((size_t)CPB * CS + 2 * kTwLo + 2 * HI + 2);
+    double* stage = reinterpret_cast<double*>(sm) + 2 * (smem_dir<N, CPB, true>() / sizeof(double2));
     uint64_t* bar = reinterpret_cast<uint64_t*>(stage + CPB * stage_stride<N>());
     const int b = threadIdx.x % CPB;
     const int tc = threadIdx.x / CPB;
@@ -1016,6 +1205,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
     if (threadIdx.x == 0 && blockIdx.x < groups) issue(blockIdx.x);
     load_tables(lo, hi, HI, tabs.lo, tabs.hi);
     load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, false>();
+    constexpr int LIM = TabPlan<N>::R2C;
+    load_direct_tables<N, LIM, RL, false>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     __syncthreads();
 
     uint32_t phase = 0;
@@ -1033,7 +1227,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                 for (int q = 0; q < R1; ++q)
                     v[bf][q] = (q < QH && live && (NB1 % TPC == 0 || j < NB1)) ? row[j + q * NB1]
                                                                                 : make_double2(0.0, 0.0);
-                dft<R1, -1>(v[bf]);
+                dft<R1, -1, true>(v[bf]);
             }
             __syncthreads();  // every staged row consumed: refill with the next group
             if (threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
@@ -1047,7 +1241,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
             }
             __syncthreads();
         }
-        passes_but_last<N, TPC, R1, -1>(s, tc, lo, hi, tail(RL{}));
+        passes_but_last<N, TPC, R1, -1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
 
         constexpr int R = last_radix(RL{});
         constexpr int NS = ns_of_last(RL{});
@@ -1068,15 +1262,15 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                     va[q] = s[pad_idx(ja + q * NB)];
                     vb[q] = s[pad_idx(jb + q * NB)];
                 }
-                twiddle_inputs<N, R, NS, -1>(va, ja, lo, hi);
-                twiddle_inputs<N, R, NS, -1>(vb, jb, lo, hi);
+                twiddle_pass<N, R, NS, -1, LIM>(va, ja, lo, hi, w2q, ptab_last);
+                twiddle_pass<N, R, NS, -1, LIM>(vb, jb, lo, hi, w2q, ptab_last);
                 dft<R, -1>(va);
                 dft<R, -1>(vb);
                 if (u != 0) {
 #pragma unroll
                     for (int q = 0; q < R; ++q) {
                         const int k = ja + q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], vb[R - 1 - q], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
@@ -1092,7 +1286,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                         const int qp = (R - q) % R;
                         if (q > qp && q != 0) continue;
                         const int k = q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], va[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;
@@ -1107,7 +1301,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                         const int qp = R - 1 - q;
                         if (q > qp) continue;
                         const int k = NB / 2 + q * NB;
-                        const double2 w = tw_lookup<-1>(plo, phi, k);
+                        const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(vb[q], vb[qp], w, xk, xn);
                         orow[(long long)k * out_fs] = xk;

@@ -752,10 +752,10 @@ template <int N, int CPB>
 cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
                         const FastTables& tabs, cudaStream_t stream, const R2CBlockMax& bm) {
     using P = fast::FastPlan<N>;
-    if constexpr (P::TPC * CPB > 1024 || fast::smem_bytes<N, CPB>() > 227 * 1024) {
+    if constexpr (P::TPC * CPB > 1024 || fast::smem_dir<N, CPB, true>() > 227 * 1024) {
         return cudaErrorNotSupported;
     } else {
-        constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        constexpr size_t smem = fast::smem_dir<N, CPB, true>();
         if constexpr (fast::UseTmaR2C<N>::value && CPB == P::CPB_R2C) {
             if (channels <= fast::UseTmaR2C<N>::max_channels) {
                 constexpr size_t smem_t = fast::smem_bytes_tma<N, CPB>();
@@ -783,10 +783,10 @@ template <int N, int CPB>
 cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
                         const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
     using P = fast::FastPlan<N>;
-    if constexpr (P::TPC * CPB > 1024 || fast::smem_bytes<N, CPB>() > 227 * 1024) {
+    if constexpr (P::TPC * CPB > 1024 || fast::smem_dir<N, CPB, false>() > 227 * 1024) {
         return cudaErrorNotSupported;
     } else {
-        constexpr size_t smem = fast::smem_bytes<N, CPB>();
+        constexpr size_t smem = fast::smem_dir<N, CPB, false>();
         auto kern = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;

@@ -37,6 +37,8 @@ struct FastTables {
     const double2* hi = nullptr;
     const double2* post_lo = nullptr;
     const double2* post_hi = nullptr;
+    const double2* wn = nullptr;   // W_N^k, k < N (direct pass tables)
+    const double2* w2n = nullptr;  // W_2N^k, k <= N (octant table)
 };
 
 // Lengths N = N_t with a register-resident compile-time plan.
