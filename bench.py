@@ -499,7 +499,9 @@ def run_ours(args):
             # 3M complex products (csrc/btg_zgemm.cu): the tensor pipe executes 6 real
             # flops per complex MAC; BTG_ZGEMM_4M=1 selects the 8-flop real embedding
             m4 = bool(os.environ.get("BTG_ZGEMM_4M"))
-            kname = f"k_zgemm_{dom}" if m4 else f"k_zgemm3m_{dom}"
+            legacy = os.environ.get("BTG_ZGEMM_LEGACY", "0") not in ("", "0")
+            # default: the warp-specialised TMA kernels (csrc/btg_zgemm_ws.cu)
+            kname = f"k_zgemm_{dom}" if m4 else (f"k_zgemm3m_{dom}" if legacy else f"k_zgemm3m_{dom}_tma")
             tpeak = (probe or {}).get("dmma_f64_tflops") or None
             executed = fl["gemv"] * (1.0 if m4 else 0.75)
             ach = executed / (dur * 1e-3) / 1e12

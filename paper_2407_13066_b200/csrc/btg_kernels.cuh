@@ -140,6 +140,12 @@ cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* m
                      int nf, int nd, int nm, int nrhs, int* mB, uint8_t* Bq, cudaStream_t stream,
                      const int16_t* vexp = nullptr, int vexp_cpb = 1);
 
+// Warp-specialised persistent 3M kernels (btg_zgemm_ws.cu; the default unless
+// BTG_ZGEMM_LEGACY / BTG_ZGEMM_4M): one CTA per SM, producer warp on bulk copies.
+cudaError_t launch_zgemm3m_fwd_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
+                                  int j0, int nj, bool accumulate, cudaStream_t stream);
+cudaError_t launch_zgemm3m_adj_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
+                                  int j0, int nj, cudaStream_t stream);
 // 3M kernels active (BTG_ZGEMM_4M unset): column ranges [j0, j0 + nj) supported.
 bool zgemm_3m();
 cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,

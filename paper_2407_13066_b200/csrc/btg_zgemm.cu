@@ -525,6 +525,12 @@ bool use_4m() {
     static const bool v = std::getenv("BTG_ZGEMM_4M") != nullptr;
     return v;
 }
+// BTG_ZGEMM_LEGACY=1: the two-CTAs-per-SM cp.async kernels below instead of the
+// warp-specialised ones (btg_zgemm_ws.cu). Read per call (A/B measurements).
+bool use_legacy() {
+    const char* v = std::getenv("BTG_ZGEMM_LEGACY");
+    return v && *v && *v != '0';
+}
 
 constexpr int kMaxGridY = 65535;
 
@@ -541,6 +547,7 @@ cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* 
                                    int nrhs, int j0, int nj, bool accumulate, cudaStream_t stream) {
     if (use_4m() && (j0 != 0 || nj != nm || accumulate)) return cudaErrorNotSupported;
     const bool m4 = use_4m();
+    if (!m4 && !use_legacy()) return launch_zgemm3m_fwd_ws(F, X, Y, nf, nd, nm, nrhs, j0, nj, accumulate, stream);
     // 2 CTAs per SM (<= 128 registers, 2 stages), as the adjoint: 15.0 -> 13.7 ms at
     // configs[3] (1 CTA x 4 stages), despite 3.5 instead of 6.9 waves.
     const auto k3 = k_zgemm3m_fwd<2, 2>;
@@ -570,6 +577,7 @@ cudaError_t launch_zgemm_adj_range(const double2* F, const double2* X, double2* 
                                    int nrhs, int j0, int nj, cudaStream_t stream) {
     if (use_4m() && (j0 != 0 || nj != nm)) return cudaErrorNotSupported;
     const bool m4 = use_4m();
+    if (!m4 && !use_legacy()) return launch_zgemm3m_adj_ws(F, X, Y, nf, nd, nm, nrhs, j0, nj, stream);
     // 2 CTAs per SM (<= 128 registers, 2 stages): one CTA's prologue / epilogue
     // overlaps the other's MMAs; K = N_d is short (configs[3]: 8 stages per tile).
     // Measured 16.3 -> 14.1 ms at configs[3] (1 CTA x 4 stages before).
