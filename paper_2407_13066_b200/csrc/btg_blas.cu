@@ -220,6 +220,11 @@ cudaError_t launch_dot(const double* a, const double* b, size_t n, double* parti
     return cudaGetLastError();
 }
 
+cudaError_t launch_sum_partials(const double* partial, int count, double* out, cudaStream_t stream) {
+    k_sum_partials<<<1, kThreads, 0, stream>>>(partial, count, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* hp, double s, size_t n,
                              double* partial, double* rnorm2, cudaStream_t stream) {
     k_cg_update<<<kRedBlocks, kThreads, 0, stream>>>(x, r, p, hp, s, n, partial);

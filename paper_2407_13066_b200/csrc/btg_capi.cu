@@ -300,17 +300,24 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
 }
 
 btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* out,
-                       const btg::C2REpilogue& epi, size_t fs = 0) {
+                       const btg::C2REpilogue& epi, size_t fs = 0, int* dot_ctas = nullptr) {
     StageClock clk(op, &op->counters.inverse_fft);
     if (!fs) fs = channels;
     // the fast epilogue reads alpha R v and per-sample Gamma^-1 as 16-byte pairs
     const bool epi_aligned = (!epi.v || aligned16(epi.v)) && (epi.gamma_mode != 2 || aligned16(epi.gamma));
-    if (op->fast_ok && aligned16(in) && aligned16(out) && epi_aligned)
+    const bool dot_aligned = !epi.dot_out || aligned16(epi.dot_v);
+    if (dot_ctas) *dot_ctas = 0;
+    if (op->fast_ok && aligned16(in) && aligned16(out) && epi_aligned && dot_aligned) {
         BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)fs, out, (long long)op->nt,
-                                          (int)channels, op->fast, epi, op->stream));
-    else
+                                          (int)channels, op->fast, epi, op->stream, dot_ctas));
+    } else {
+        // the generic kernels have no folded dot: the caller falls back (dot_ctas = 0)
+        btg::C2REpilogue e = epi;
+        e.dot_v = nullptr;
+        e.dot_out = nullptr;
         BTG_CUDA(btg::launch_c2r(in, (long long)fs, 1, out, (long long)op->nt, (int)channels,
-                                 (int)op->nt, op->plan, op->fft_batch, epi, op->stream, op->gscratch));
+                                 (int)op->nt, op->plan, op->fft_batch, e, op->stream, op->gscratch));
+    }
     op->counters.launches++;
     op->counters.inverse_fft.ops += fft_ops(channels, op->nt);
     op->counters.inverse_fft.bytes += 16.0 * op->nf * channels + 8.0 * channels * op->nt;
@@ -397,7 +404,7 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
 // FP64: all right-hand sides go through one R2C, one ZGEMM (DMMA) and one C2R;
 // FP32 F-hat: one GEMV stream per right-hand side.
 btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size_t nrhs,
-                    const btg::C2REpilogue& epi) {
+                    const btg::C2REpilogue& epi, int* dot_ctas = nullptr) {
     const size_t cin = adjoint ? op->nd : op->nm;
     const size_t cout = adjoint ? op->nm : op->nd;
     if (nrhs > 1 && op->precision == BTG_F64 && !op->no_dmma) {
@@ -427,7 +434,7 @@ btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size
         BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, 1));
         btg::C2REpilogue e = epi;
         if (e.v) e.v = epi.v + r * cout * op->nt;
-        BTG_TRY(run_c2r_vec(op, op->wb, cout, out + r * cout * op->nt, e));
+        BTG_TRY(run_c2r_vec(op, op->wb, cout, out + r * cout * op->nt, e, 0, nrhs == 1 ? dot_ctas : nullptr));
     }
     return BTG_OK;
 }
@@ -1411,6 +1418,7 @@ enum CgSlot { kSlotX, kSlotR, kSlotZ, kSlotP, kSlotHp, kSlotPartial, kSlotScal, 
 struct CgBuffers {
     double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *hp = nullptr, *partial = nullptr,
            *scal = nullptr, *pivot = nullptr, *scratch = nullptr, *rhs = nullptr, *gam = nullptr;
+    size_t partial_cap = 0;  // doubles: reduction partials / folded-dot CTA partials
 };
 
 // The slots outlive the call: every exit (errors included) drains the handle's
@@ -1436,9 +1444,12 @@ btg_status read_scalar(btg_op op, const double* dev, double* host) {
     return BTG_OK;
 }
 
-// H v on device pointers (the body of btg_hessian without staging).
+// H v on device pointers (the body of btg_hessian without staging). With
+// `curv`, also v^T H v into *curv (device): folded into the final C2R's stores
+// (per-CTA partials in `part`, capacity `part_cap`, summed in index order), or a
+// separate dot when the generic C2R ran.
 btg_status hessian_dev(btg_op op, const double* vd, double* hvd, const double* gd, int gamma_kind, double alpha,
-                       int reg_kind) {
+                       int reg_kind, double* part = nullptr, size_t part_cap = 0, double* curv = nullptr) {
     BTG_TRY(grow(op->wt, op->wtcap, op->nd * op->nt));
     btg::C2REpilogue e1{};
     e1.gamma = gd;
@@ -1451,7 +1462,21 @@ btg_status hessian_dev(btg_op op, const double* vd, double* hvd, const double* g
         e2.alpha = alpha;
         e2.reg_kind = reg_kind;
     }
-    return pipeline(op, true, op->wt, hvd, 1, e2);
+    if (!curv) return pipeline(op, true, op->wt, hvd, 1, e2);
+    e2.dot_v = vd;
+    e2.dot_out = part;
+    int ctas = 0;
+    BTG_TRY(pipeline(op, true, op->wt, hvd, 1, e2, &ctas));
+    const size_t n = op->nm * op->nt;
+    if (ctas > 0 && (size_t)ctas <= part_cap) {
+        BTG_CUDA(btg::launch_sum_partials(part, ctas, curv, op->stream));
+        op->counters.launches++;
+    } else {
+        if (ctas > 0) return fail(BTG_EARG, "internal: %d folded-dot partials exceed %zu", ctas, part_cap);
+        BTG_CUDA(btg::launch_dot(vd, hvd, n, part, curv, op->stream));
+        op->counters.launches += 2;
+    }
+    return BTG_OK;
 }
 
 // CG building blocks shared by the host-driven and the graph loop.
@@ -1483,9 +1508,9 @@ btg_status cg_host_loop(btg_op op, const CgBuffers& b, double* x, const double* 
                         int reg_kind, bool precond, bool lap, double tol, size_t max_iterations, double rho,
                         double rhs_norm, size_t n, btg_cg_result* result) {
     for (size_t it = 1; it <= max_iterations; ++it) {
-        BTG_TRY(hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind));
+        BTG_TRY(hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind, b.partial, b.partial_cap, b.scal));
         double curvature = 0.0;
-        BTG_TRY(cg_dot(op, b, n, b.p, b.hp, &curvature));
+        BTG_TRY(read_scalar(op, b.scal, &curvature));
         if (!(curvature > 0.0)) return cg_bad_curvature(curvature);
         const double step = rho / curvature;
         double rn2 = 0.0;
@@ -1575,13 +1600,13 @@ btg_status cg_graph_loop(btg_op op, const CgBuffers& b, double* x, const double*
                                            cudaStreamCaptureModeRelaxed));
     op->stream = op->capture_stream;
     gg.capturing = op->capture_stream;
-    btg_status s = hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind);
+    btg_status s = hessian_dev(op, b.p, b.hp, gd, gamma_kind, alpha, reg_kind, b.partial, b.partial_cap,
+                               st + kCgCurvature);
     cudaError_t e = cudaSuccess;
     if (s == BTG_OK) {
-        e = launch_dot(b.p, b.hp, n, b.partial, st + kCgCurvature, op->stream);
-        if (e == cudaSuccess) e = launch_cg_update_dev(x, b.r, b.p, b.hp, st, n, b.partial, op->stream);
+        e = launch_cg_update_dev(x, b.r, b.p, b.hp, st, n, b.partial, op->stream);
         if (e == cudaSuccess) e = launch_cg_check(b.partial, st, cond, precond ? 1 : 0, op->stream);
-        op->counters.launches += 4;
+        op->counters.launches += 2;
     }
     if (s == BTG_OK && e == cudaSuccess && precond) {
         s = cg_precondition(op, b, lap, n, b.z, b.r);
@@ -1671,7 +1696,9 @@ btg_status btg_cg_solve(btg_op op, const double* rhs, size_t rhs_len, double* x_
     BTG_TRY(slot(op, kSlotR, &b.r, n));
     BTG_TRY(slot(op, kSlotP, &b.p, n));
     BTG_TRY(slot(op, kSlotHp, &b.hp, n));
-    BTG_TRY(slot(op, kSlotPartial, &b.partial, btg::kRedBlocks));
+    // the folded p^T H p writes one partial per C2R CTA (<= one per source channel)
+    b.partial_cap = std::max<size_t>(btg::kRedBlocks, op->nm);
+    BTG_TRY(slot(op, kSlotPartial, &b.partial, b.partial_cap));
     BTG_TRY(slot(op, kSlotScal, &b.scal, btg::kCgStateLen));
     const bool precond = use_reg_preconditioner != 0;
     if (precond) BTG_TRY(slot(op, kSlotZ, &b.z, n));
@@ -1779,7 +1806,9 @@ btg_status btg_objective(btg_op op, const double* m, size_t m_len, const double*
     }
     BTG_TRY(slot(op, kSlotR, &b.r, d_len));
     BTG_TRY(slot(op, kSlotP, &b.p, m_len));
-    BTG_TRY(slot(op, kSlotPartial, &b.partial, btg::kRedBlocks));
+    // the folded p^T H p writes one partial per C2R CTA (<= one per source channel)
+    b.partial_cap = std::max<size_t>(btg::kRedBlocks, op->nm);
+    BTG_TRY(slot(op, kSlotPartial, &b.partial, b.partial_cap));
     BTG_TRY(slot(op, kSlotScal, &b.scal, 1));
     BTG_TRY(pipeline(op, false, md, b.r, 1, btg::C2REpilogue{}));
     BTG_CUDA(btg::launch_sub(b.r, b.r, dd, d_len, op->stream));

@@ -470,6 +470,21 @@ __device__ __forceinline__ void block_max(const R2CBlockMax& bm, int c0, int b, 
     if (b == 0) bm.pexp[(size_t)(c0 / CPB) * bm.nf + k] = (int16_t)e;
 }
 
+// CTA sum of the folded dot product (C2REpilogue::dot_out), one value per CTA.
+__device__ __forceinline__ void cta_dot_store(double acc, double* out) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) red[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        out[blockIdx.x] = t;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // r2c: SOTI rows (time contiguous) -> frequency-major out[k*out_fs + c]
 // ---------------------------------------------------------------------------
@@ -710,9 +725,11 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     constexpr int NS = ns_of_last(RL{});
     constexpr int NB = N / R;
     constexpr int BF = (NB + TPC - 1) / TPC;
-    if (!live) return;
+    double dacc = 0.0;  // folded dot (epi.dot_out)
+    if (live) {
     double* orow = out + (long long)c * out_cs;
     const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+    const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
 #pragma unroll
     for (int bf = 0; bf < BF; ++bf) {
         const int j = tc + bf * TPC;
@@ -763,9 +780,15 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     y1 += epi.alpha * r1;
                 }
                 reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
+                if (drow) {
+                    const double2 dv = __ldg(reinterpret_cast<const double2*>(drow) + p);
+                    dacc = fma(dv.x, y0, fma(dv.y, y1, dacc));
+                }
             }
         }
     }
+    }
+    if (epi.dot_out) cta_dot_store(dacc, epi.dot_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -989,6 +1012,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     prefetch(blockIdx.x);
     __syncthreads();
 
+    double dacc = 0.0;  // folded dot (epi.dot_out), over every group of this CTA
     for (int g = blockIdx.x; g < groups; g += gridDim.x) {
         const int c = g * CPB + b;
         const bool live = c < channels;
@@ -1060,6 +1084,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
         if (live) {
             double* orow = out + (long long)c * out_cs;
             const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+            const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
 #pragma unroll
             for (int bf = 0; bf < BF; ++bf) {
                 const int j = tc + bf * TPC;
@@ -1110,12 +1135,17 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                             y1 += epi.alpha * r1;
                         }
                         reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
+                        if (drow) {
+                            const double2 dv = __ldg(reinterpret_cast<const double2*>(drow) + p);
+                            dacc = fma(dv.x, y0, fma(dv.y, y1, dacc));
+                        }
                     }
                 }
             }
         }
         __syncthreads();  // the next group's first pass overwrites s
     }
+    if (epi.dot_out) cta_dot_store(dacc, epi.dot_out);
 }
 
 // ---------------------------------------------------------------------------

@@ -781,7 +781,7 @@ cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long lo
 
 template <int N, int CPB>
 cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
-                        const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
+                        const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream, int* ctas) {
     using P = fast::FastPlan<N>;
     if constexpr (P::TPC * CPB > 1024 || fast::smem_dir<N, CPB, false>() > 227 * 1024) {
         return cudaErrorNotSupported;
@@ -792,6 +792,7 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         if (e != cudaSuccess) return e;
         const int groups = (channels + CPB - 1) / CPB;
         const int grid = P::PF_C2R ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
+        if (ctas) *ctas = grid;
         kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
         return cudaGetLastError();
     }
@@ -812,13 +813,14 @@ cudaError_t r2c_fast_n(const double* in, long long in_cs, double2* out, long lon
 
 template <int N>
 cudaError_t c2r_fast_n(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
-                       const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream) {
+                       const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream, int* ctas) {
     switch (fft_cpb(fast::FastPlan<N>::CPB_C2R)) {
-        case 1: return c2r_fast_nc<N, 1>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
-        case 2: return c2r_fast_nc<N, 2>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
-        case 4: return c2r_fast_nc<N, 4>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
-        case 8: return c2r_fast_nc<N, 8>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
-        default: return c2r_fast_nc<N, fast::FastPlan<N>::CPB_C2R>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+        case 1: return c2r_fast_nc<N, 1>(in, in_fs, out, out_cs, channels, tabs, epi, stream, ctas);
+        case 2: return c2r_fast_nc<N, 2>(in, in_fs, out, out_cs, channels, tabs, epi, stream, ctas);
+        case 4: return c2r_fast_nc<N, 4>(in, in_fs, out, out_cs, channels, tabs, epi, stream, ctas);
+        case 8: return c2r_fast_nc<N, 8>(in, in_fs, out, out_cs, channels, tabs, epi, stream, ctas);
+        default: return c2r_fast_nc<N, fast::FastPlan<N>::CPB_C2R>(in, in_fs, out, out_cs, channels, tabs, epi, stream,
+                                                                   ctas);
     }
 }
 
@@ -856,10 +858,10 @@ cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double
 
 cudaError_t launch_c2r_vec_fast(int n, const double2* in, long long in_fs, double* out, long long out_cs,
                                 int channels, const FastTables& tabs, const C2REpilogue& epi,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int* ctas) {
     if (channels <= 0) return cudaSuccess;
 #define BTG_CASE(N) \
-    if (n == N) return c2r_fast_n<N>(in, in_fs, out, out_cs, channels, tabs, epi, stream);
+    if (n == N) return c2r_fast_n<N>(in, in_fs, out, out_cs, channels, tabs, epi, stream, ctas);
     BTG_FAST_SIZES(BTG_CASE)
 #undef BTG_CASE
     return cudaErrorNotSupported;

@@ -18,6 +18,11 @@ struct C2REpilogue {
     const double* v = nullptr;      // SOTI vector sharing the output layout
     double alpha = 0.0;
     int reg_kind = 0;               // 0 identity, 1 temporal Laplacian (inverse.cpp:32-49)
+    // Optional dot product folded into the stores (CG's p^T H p): each CTA writes
+    // sum_t dot_v[c][t] * y[c][t] over its channels to dot_out[blockIdx.x] (fast
+    // kernels only; the launcher reports the CTA count).
+    const double* dot_v = nullptr;  // SOTI vector sharing the output layout
+    double* dot_out = nullptr;
 };
 
 // Split twiddle tables of the compile-time-N vector FFTs (btg_fft_fast.cuh):
@@ -54,7 +59,7 @@ cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double
                                 const R2CBlockMax& bm = R2CBlockMax{});
 cudaError_t launch_c2r_vec_fast(int n, const double2* in, long long in_fs, double* out, long long out_cs,
                                 int channels, const FastTables& tabs, const C2REpilogue& epi,
-                                cudaStream_t stream);
+                                cudaStream_t stream, int* ctas = nullptr);
 
 // Per-channel shared-memory footprint (complex elements) of an FFT of length n.
 __host__ __device__ inline int fft_channel_stride(int n) { return n + 1; }
@@ -165,6 +170,8 @@ cudaError_t launch_dot(const double* a, const double* b, size_t n, double* parti
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* hp, double s, size_t n,
                              double* partial, double* rnorm2, cudaStream_t stream);
 cudaError_t launch_xpby(double* p, const double* z, double beta, size_t n, cudaStream_t stream);
+// out = sum of partial[0..count) in index order (one block; deterministic)
+cudaError_t launch_sum_partials(const double* partial, int count, double* out, cudaStream_t stream);
 // Device-side CG loop (btg_cg_solve's CUDA graph WHILE body): scalars in a
 // CgState array of kCgStateLen doubles.
 enum CgStateIdx {
