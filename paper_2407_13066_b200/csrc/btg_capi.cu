@@ -277,11 +277,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // R2C of `channels` SOTI rows into a frequency-major array whose frequency
 // stride is `fs` (default: channels; a column chunk of a wider array otherwise).
+// blocked: write the channel-blocked layout (btg::kBlockedFs; the caller checked
+// mrhs_blocked, which implies the fast plan runs kSpecBlock channels per CTA).
 btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out, size_t fs = 0,
-                       const btg::R2CBlockMax* bm = nullptr) {
+                       const btg::R2CBlockMax* bm = nullptr, bool blocked = false) {
     StageClock clk(op, &op->counters.forward_fft);
     if (!fs) fs = channels;
-    if (op->fast_ok && aligned16(v) && aligned16(out))
+    if (blocked)
+        BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, btg::kBlockedFs, (int)channels,
+                                          op->fast, op->stream));
+    else if (op->fast_ok && aligned16(v) && aligned16(out))
         BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, v, (long long)op->nt, out, (long long)fs,
                                           (int)channels, op->fast, op->stream, bm ? *bm : btg::R2CBlockMax{}));
     else if (bm)
@@ -300,14 +305,19 @@ btg_status run_r2c_vec(btg_op op, const double* v, size_t channels, double2* out
 }
 
 btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* out,
-                       const btg::C2REpilogue& epi, size_t fs = 0, int* dot_ctas = nullptr) {
+                       const btg::C2REpilogue& epi, size_t fs = 0, int* dot_ctas = nullptr, bool blocked = false) {
     StageClock clk(op, &op->counters.inverse_fft);
     if (!fs) fs = channels;
     // the fast epilogue reads alpha R v and per-sample Gamma^-1 as 16-byte pairs
     const bool epi_aligned = (!epi.v || aligned16(epi.v)) && (epi.gamma_mode != 2 || aligned16(epi.gamma));
     const bool dot_aligned = !epi.dot_out || aligned16(epi.dot_v);
     if (dot_ctas) *dot_ctas = 0;
-    if (op->fast_ok && aligned16(in) && aligned16(out) && epi_aligned && dot_aligned) {
+    if (blocked) {
+        if (!(aligned16(out) && epi_aligned && dot_aligned))
+            return fail(BTG_EARG, "internal: blocked C2R needs 16-byte aligned vectors");
+        BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, btg::kBlockedFs, out, (long long)op->nt, (int)channels,
+                                          op->fast, epi, op->stream, dot_ctas));
+    } else if (op->fast_ok && aligned16(in) && aligned16(out) && epi_aligned && dot_aligned) {
         BTG_CUDA(btg::launch_c2r_vec_fast((int)op->nt, in, (long long)fs, out, (long long)op->nt,
                                           (int)channels, op->fast, epi, op->stream, dot_ctas));
     } else {
@@ -360,7 +370,7 @@ btg_status ensure_oz(btg_op op, size_t nrhs) {
 }
 
 btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, size_t nrhs,
-                     const int16_t* vexp = nullptr, int vexp_cpb = 1) {
+                     const int16_t* vexp = nullptr, int vexp_cpb = 1, bool blocked = false) {
     StageClock clk(op, &op->counters.apply);
     const size_t nin = adjoint ? op->nd : op->nm;
     const size_t nout = adjoint ? op->nm : op->nd;
@@ -376,8 +386,13 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
         // ZGEMM on the FP64 tensor cores (btg_zgemm.cu); FP64 F-hat only.
         if (op->precision != BTG_F64) return fail(BTG_EARG, "internal: batched apply needs FP64 F-hat");
         const double2* F = static_cast<const double2*>(op->F);
-        e = adjoint ? btg::launch_zgemm_adj(F, in, out, nf, nd, nm, (int)nrhs, op->stream)
-                    : btg::launch_zgemm_fwd(F, in, out, nf, nd, nm, (int)nrhs, op->stream);
+        if (blocked)  // the N_m side (X forward, G adjoint) channel-blocked
+            e = adjoint ? btg::launch_zgemm3m_adj_ws(F, in, out, nf, nd, nm, (int)nrhs, 0, nm, op->stream, true)
+                        : btg::launch_zgemm3m_fwd_ws(F, in, out, nf, nd, nm, (int)nrhs, 0, nm, false, op->stream,
+                                                     true);
+        else
+            e = adjoint ? btg::launch_zgemm_adj(F, in, out, nf, nd, nm, (int)nrhs, op->stream)
+                        : btg::launch_zgemm_fwd(F, in, out, nf, nd, nm, (int)nrhs, op->stream);
     } else if (op->precision == BTG_F64 && !op->legacy_gemv) {
         // persistent TMA-staged stream (btg_gemv_tma.cu)
         const double2* F = static_cast<const double2*>(op->F);
@@ -398,6 +413,19 @@ btg_status run_apply(btg_op op, bool adjoint, const double2* in, double2* out, s
     op->counters.apply.bytes +=
         (double)op->F_elem * op->nf * op->nd * op->nm + 16.0 * op->nf * (nin + nout) * nrhs;
     return BTG_OK;
+}
+
+// Multi-RHS device pipeline with the N_m-side spectrum channel-blocked
+// (btg::kBlockedFs): FP64 3M ZGEMM on its TMA kernels, a fast plan with
+// kSpecBlock channels per CTA in both directions, aligned vectors.
+// BTG_SPEC_BLOCKED=0 keeps the frequency-major layout (A/B).
+bool mrhs_blocked(btg_op op, const double* in, const double* out, const btg::C2REpilogue& epi) {
+    const char* v = std::getenv("BTG_SPEC_BLOCKED");
+    if (v && *v == '0') return false;
+    return op->precision == BTG_F64 && !op->no_dmma && !op->tensor_i8 && op->fast_ok &&
+           btg::spec_blocked_ok((int)op->nt) && btg::zgemm_ws_active() && btg::zgemm_tma_ok((int)op->nm) &&
+           aligned16(in) && aligned16(out) && aligned16(op->wa) && aligned16(op->wb) &&
+           (!epi.v || aligned16(epi.v)) && (epi.gamma_mode != 2 || aligned16(epi.gamma));
 }
 
 // One direction (forward or adjoint) for nrhs right-hand sides, device pointers.
@@ -423,9 +451,12 @@ btg_status pipeline(btg_op op, bool adjoint, const double* in, double* out, size
             BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi));
             return BTG_OK;
         }
-        BTG_TRY(run_r2c_vec(op, in, nrhs * cin, op->wa));
-        BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, nrhs));
-        BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi));
+        // The N_m-side spectrum (x-hat forward, g-hat adjoint) in the channel-blocked
+        // layout: the big R2C writes / C2R reads stream contiguous blocks
+        const bool blk = mrhs_blocked(op, in, out, epi);
+        BTG_TRY(run_r2c_vec(op, in, nrhs * cin, op->wa, 0, nullptr, blk && !adjoint));
+        BTG_TRY(run_apply(op, adjoint, op->wa, op->wb, nrhs, nullptr, 1, blk));
+        BTG_TRY(run_c2r_vec(op, op->wb, nrhs * cout, out, epi, 0, nullptr, blk && adjoint));
         return BTG_OK;
     }
     BTG_TRY(ensure_spectral(op, 1));

@@ -69,7 +69,18 @@ BTG_PLAN(256,   16,  16, 16,  512,  256,  true,  true,  BTG_R(16, 4, 4),        
 BTG_PLAN(500,   64,  4,  4,   1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
 BTG_PLAN(512,   64,  4,  4,   256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
 BTG_PLAN(1000,  128, 2,  2,   1024, 1024, false, false, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
-BTG_PLAN(1024,  64,  4,  4,   768,  256,  false, true,  BTG_R(16, 16, 4),       BTG_R(4, 16, 16))
+// (BTG_P1024_* override the N_t = 1024 plan in plan sweeps)
+#ifndef BTG_P1024_TPC
+#define BTG_P1024_TPC 64
+#define BTG_P1024_CPBR 4
+#define BTG_P1024_CPBC 4
+#define BTG_P1024_RESR 768
+#define BTG_P1024_RESC 256
+#define BTG_P1024_PFR false
+#define BTG_P1024_PFC true
+#endif
+BTG_PLAN(1024,  BTG_P1024_TPC, BTG_P1024_CPBR, BTG_P1024_CPBC, BTG_P1024_RESR, BTG_P1024_RESC, BTG_P1024_PFR,
+         BTG_P1024_PFC, BTG_R(16, 16, 4), BTG_R(4, 16, 16))
 BTG_PLAN(2000,  128, 2,  2,   512,  384,  false, false, BTG_R(16, 5, 5, 5),     BTG_R(5, 5, 5, 16))
 BTG_PLAN(2048,  128, 2,  2,   512,  256,  false, false, BTG_R(16, 8, 4, 4),     BTG_R(4, 4, 8, 16))
 BTG_PLAN(4096,  256, 2,  1,   512,  256,  true,  false, BTG_R(16, 16, 4, 4),    BTG_R(4, 4, 16, 16))
@@ -470,6 +481,23 @@ __device__ __forceinline__ void block_max(const R2CBlockMax& bm, int c0, int b, 
     if (b == 0) bm.pexp[(size_t)(c0 / CPB) * bm.nf + k] = (int16_t)e;
 }
 
+// Spectral-vector addressing. fs > 0: frequency-major, element k of channel c at
+// [c + k fs]. fs < 0 (kBlockedFs): channel-blocked, [c / G][k][c % G] with
+// N + 1 frequencies, G = kSpecBlock: the R2C writes (C2R reads) of a CTA's CPB
+// channels hit G x 16-byte rows (shared with the neighbouring CTAs of the same
+// block, which run at the same time) instead of CPB x 16 bytes per frequency
+// row spread over the whole vector — 64-byte segments cap HBM at ~3 TB/s at
+// 524288 channels, 128-byte ones at 5.4-6.1 TB/s (profiles/r02s2_scatter_bw.md).
+template <int N, int CPB>
+__device__ __forceinline__ long long spec_base(int c, long long fs) {
+    static_assert(kSpecBlock % CPB == 0 || CPB > kSpecBlock, "channel groups tile the spectral blocks");
+    return fs < 0 ? (long long)(c / kSpecBlock) * (N + 1) * kSpecBlock + c % kSpecBlock : (long long)c;
+}
+template <int CPB>
+__device__ __forceinline__ long long spec_stride(long long fs) {
+    return fs < 0 ? kSpecBlock : fs;
+}
+
 // CTA sum of the folded dot product (C2REpilogue::dot_out), one value per CTA.
 __device__ __forceinline__ void cta_dot_store(double acc, double* out) {
     __shared__ double red[32];
@@ -509,6 +537,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     load_direct_tables<N, LIM, RL, false>(w2q, ptab, tabs);
     const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
+    const long long ofs = spec_stride<CPB>(out_fs);
     const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
     const bool live = c < channels;
@@ -552,7 +581,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     constexpr int NU = NB / 2;
     constexpr int UF = (NU + TPC - 1) / TPC;
     if (!live) return;  // no barrier follows
-    double2* orow = out + c;
+    double2* orow = out + spec_base<N, CPB>(c, out_fs);
 #pragma unroll
     for (int uf = 0; uf < UF; ++uf) {
         const int u = tc + uf * TPC;
@@ -577,8 +606,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(va[q], vb[R - 1 - q], w, xk, xn);
-                orow[(long long)k * out_fs] = xk;
-                orow[(long long)(N - k) * out_fs] = xn;
+                orow[(long long)k * ofs] = xk;
+                orow[(long long)(N - k) * ofs] = xn;
                 if (bm.pexp) {
                     block_max<CPB>(bm, c - b, b, k, xk);
                     block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -594,8 +623,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(va[q], va[qp], w, xk, xn);
-                orow[(long long)k * out_fs] = xk;
-                if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                orow[(long long)k * ofs] = xk;
+                if (q != qp || q == 0) orow[(long long)(N - k) * ofs] = xn;
                 if (bm.pexp) {
                     block_max<CPB>(bm, c - b, b, k, xk);
                     if (q != qp || q == 0) block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -610,8 +639,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                 const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                 double2 xk, xn;
                 split_pair(vb[q], vb[qp], w, xk, xn);
-                orow[(long long)k * out_fs] = xk;
-                if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                orow[(long long)k * ofs] = xk;
+                if (q != qp) orow[(long long)(N - k) * ofs] = xn;
                 if (bm.pexp) {
                     block_max<CPB>(bm, c - b, b, k, xk);
                     if (q != qp) block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -645,6 +674,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     load_direct_tables<N, LIM, RL, true>(w2q, ptab, tabs);
     const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
+    const long long ifs = spec_stride<CPB>(in_fs);
     const int tc = threadIdx.x / CPB;
     const int c = blockIdx.x * CPB + b;
     const bool live = c < channels;
@@ -658,8 +688,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
         constexpr int NU = NB / 2;
         constexpr int UF = (NU + TPC - 1) / TPC;
         constexpr double inv_len = 0.5 / N;
-        const double2* col = in + c;
-        auto X = [&](int k) { return live ? __ldg(col + (long long)k * in_fs) : make_double2(0.0, 0.0); };
+        const double2* col = in + spec_base<N, CPB>(c, in_fs);
+        auto X = [&](int k) { return live ? __ldg(col + (long long)k * ifs) : make_double2(0.0, 0.0); };
         double2 va[UF][R], vb[UF][R];
 #pragma unroll
         for (int uf = 0; uf < UF; ++uf) {
@@ -823,6 +853,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
     load_direct_tables<N, LIM, RL, false>(w2q, ptab, tabs);
     const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
+    const long long ofs = spec_stride<CPB>(out_fs);
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
     const int groups = (channels + CPB - 1) / CPB;
@@ -876,7 +907,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
         constexpr int NU = NB / 2;
         constexpr int UF = (NU + TPC - 1) / TPC;
         if (live) {
-            double2* orow = out + c;
+            double2* orow = out + spec_base<N, CPB>(c, out_fs);
 #pragma unroll
             for (int uf = 0; uf < UF; ++uf) {
                 const int u = tc + uf * TPC;
@@ -901,8 +932,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], vb[R - 1 - q], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -918,8 +949,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], va[qp], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        if (q != qp || q == 0) orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             if (q != qp || q == 0) block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -934,8 +965,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(vb[q], vb[qp], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        if (q != qp) orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             if (q != qp) block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -976,6 +1007,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     load_direct_tables<N, LIM, RL, true>(w2q, ptab, tabs);
     const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
     const int b = threadIdx.x % CPB;
+    const long long ifs = spec_stride<CPB>(in_fs);
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
     const int groups = (channels + CPB - 1) / CPB;
@@ -986,9 +1018,9 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     auto prefetch = [&](int g) {
         const int c = g * CPB + b;
         const bool ok = g < groups && c < channels;
-        const double2* col = in + (ok ? c : 0);
+        const double2* col = in + spec_base<N, CPB>(ok ? c : 0, in_fs);
         auto X = [&](int k, bool use) {
-            return (ok && use) ? __ldg(col + (long long)k * in_fs) : make_double2(0.0, 0.0);
+            return (ok && use) ? __ldg(col + (long long)k * ifs) : make_double2(0.0, 0.0);
         };
 #pragma unroll
         for (int uf = 0; uf < UF1; ++uf) {
@@ -1215,6 +1247,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
     double* stage = reinterpret_cast<double*>(sm) + 2 * (smem_dir<N, CPB, true>() / sizeof(double2));
     uint64_t* bar = reinterpret_cast<uint64_t*>(stage + CPB * stage_stride<N>());
     const int b = threadIdx.x % CPB;
+    const long long ofs = spec_stride<CPB>(out_fs);
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
     const int groups = (channels + CPB - 1) / CPB;
@@ -1279,7 +1312,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
         constexpr int NU = NB / 2;
         constexpr int UF = (NU + TPC - 1) / TPC;
         if (live) {
-            double2* orow = out + c;
+            double2* orow = out + spec_base<N, CPB>(c, out_fs);
 #pragma unroll
             for (int uf = 0; uf < UF; ++uf) {
                 const int u = tc + uf * TPC;
@@ -1303,8 +1336,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], vb[R - 1 - q], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -1319,8 +1352,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(va[q], va[qp], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        if (q != qp || q == 0) orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        if (q != qp || q == 0) orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             if (q != qp || q == 0) block_max<CPB>(bm, c - b, b, N - k, xn);
@@ -1334,8 +1367,8 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
                         const double2 w = w2n_lookup<N, false>(w2q, plo, phi, k);
                         double2 xk, xn;
                         split_pair(vb[q], vb[qp], w, xk, xn);
-                        orow[(long long)k * out_fs] = xk;
-                        if (q != qp) orow[(long long)(N - k) * out_fs] = xn;
+                        orow[(long long)k * ofs] = xk;
+                        if (q != qp) orow[(long long)(N - k) * ofs] = xn;
                         if (bm.pexp) {
                             block_max<CPB>(bm, c - b, b, k, xk);
                             if (q != qp) block_max<CPB>(bm, c - b, b, N - k, xn);

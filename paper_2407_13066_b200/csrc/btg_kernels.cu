@@ -752,12 +752,20 @@ template <int N, int CPB>
 cudaError_t r2c_fast_nc(const double* in, long long in_cs, double2* out, long long out_fs, int channels,
                         const FastTables& tabs, cudaStream_t stream, const R2CBlockMax& bm) {
     using P = fast::FastPlan<N>;
+    if (out_fs < 0 && (kSpecBlock % CPB || bm.pexp)) return cudaErrorNotSupported;
     if constexpr (P::TPC * CPB > 1024 || fast::smem_dir<N, CPB, true>() > 227 * 1024) {
         return cudaErrorNotSupported;
     } else {
         constexpr size_t smem = fast::smem_dir<N, CPB, true>();
         if constexpr (fast::UseTmaR2C<N>::value && CPB == P::CPB_R2C) {
-            if (channels <= fast::UseTmaR2C<N>::max_channels) {
+            static const long long tma_max = [] {  // BTG_R2C_TMA_MAX: crossover override (sweeps)
+                const char* v = std::getenv("BTG_R2C_TMA_MAX");
+                return v && *v ? std::atoll(v) : (long long)fast::UseTmaR2C<N>::max_channels;
+            }();
+            // channel-blocked output: the TMA kernel at every size (524288 channels at
+            // N_t = 1024: 2.55 ms vs 2.99 ms for the 3-CTA kernel; frequency-major
+            // output keeps the measured crossover)
+            if (channels <= tma_max || out_fs < 0) {
                 constexpr size_t smem_t = fast::smem_bytes_tma<N, CPB>();
                 auto kt = fast::k_r2c_tma<N, CPB>;
                 cudaError_t e = set_smem(kt, smem_t);
@@ -783,6 +791,7 @@ template <int N, int CPB>
 cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long long out_cs, int channels,
                         const FastTables& tabs, const C2REpilogue& epi, cudaStream_t stream, int* ctas) {
     using P = fast::FastPlan<N>;
+    if (in_fs < 0 && kSpecBlock % CPB) return cudaErrorNotSupported;
     if constexpr (P::TPC * CPB > 1024 || fast::smem_dir<N, CPB, false>() > 227 * 1024) {
         return cudaErrorNotSupported;
     } else {
@@ -834,6 +843,15 @@ int fast_r2c_cpb(int n) {
     BTG_FAST_SIZES(BTG_CASE)
 #undef BTG_CASE
     return 0;
+}
+
+bool spec_blocked_ok(int n) {
+#define BTG_CASE(N)                                                                                       \
+    if (n == N)                                                                                           \
+        return kSpecBlock % fft_cpb(fast::FastPlan<N>::CPB_R2C) == 0 && kSpecBlock % fft_cpb(fast::FastPlan<N>::CPB_C2R) == 0;
+    BTG_FAST_SIZES(BTG_CASE)
+#undef BTG_CASE
+    return false;
 }
 
 bool fast_fft_supported(int n) {

@@ -52,6 +52,16 @@ bool fast_fft_supported(int n);
 int fast_r2c_cpb(int n);
 int fast_fft_hi_count(int n);  // entries of hi (post_hi has one more)
 
+// Channel-blocked spectral layout (out_fs / in_fs = kBlockedFs): [c / kSpecBlock]
+// [k][c % kSpecBlock], N_t + 1 frequencies (btg_fft_fast.cuh spec_base). Only
+// lengths whose fast R2C and C2R channels per CTA divide kSpecBlock take it
+// (spec_blocked_ok); the multi-RHS ZGEMM (TMA kernels) reads / writes it.
+constexpr long long kBlockedFs = -1;
+#ifndef BTG_SPEC_BLOCK
+#define BTG_SPEC_BLOCK 4
+#endif
+constexpr int kSpecBlock = BTG_SPEC_BLOCK;
+bool spec_blocked_ok(int n);
 // SOTI rows (16-byte aligned) -> frequency-major; returns cudaErrorNotSupported
 // when N has no compile-time plan.
 cudaError_t launch_r2c_vec_fast(int n, const double* in, long long in_cs, double2* out, long long out_fs,
@@ -147,10 +157,16 @@ cudaError_t oz_apply(bool adjoint, const int8_t* Aq, const unsigned long long* m
 
 // Warp-specialised persistent 3M kernels (btg_zgemm_ws.cu; the default unless
 // BTG_ZGEMM_LEGACY / BTG_ZGEMM_4M): one CTA per SM, producer warp on bulk copies.
+// xblocked / yblocked: the N_m-side spectrum in the channel-blocked layout
+// (kBlockedFs; TMA kernels only — cudaErrorNotSupported otherwise).
 cudaError_t launch_zgemm3m_fwd_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
-                                  int j0, int nj, bool accumulate, cudaStream_t stream);
+                                  int j0, int nj, bool accumulate, cudaStream_t stream, bool xblocked = false);
 cudaError_t launch_zgemm3m_adj_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
-                                  int j0, int nj, cudaStream_t stream);
+                                  int j0, int nj, cudaStream_t stream, bool yblocked = false);
+// the TMA ZGEMM (and with it the blocked layout) is available for this N_m
+bool zgemm_tma_ok(int nm);
+// the warp-specialised 3M kernels are selected (not BTG_ZGEMM_LEGACY / BTG_ZGEMM_4M)
+bool zgemm_ws_active();
 // 3M kernels active (BTG_ZGEMM_4M unset): column ranges [j0, j0 + nj) supported.
 bool zgemm_3m();
 cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,

@@ -542,6 +542,7 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 bool zgemm_3m() { return !use_4m(); }
+bool zgemm_ws_active() { return !use_4m() && !use_legacy(); }
 
 cudaError_t launch_zgemm_fwd_range(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm,
                                    int nrhs, int j0, int nj, bool accumulate, cudaStream_t stream) {

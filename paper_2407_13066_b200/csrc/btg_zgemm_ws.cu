@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // masked in the fragments.
 // ---------------------------------------------------------------------------
 constexpr int kTmaStages = 5;
+constexpr bool kXBlockSwizzle = kSpecBlock == 8;  // blocked X tile swizzled (128-byte inner box)
+static_assert(kSpecBlock == 4 || kSpecBlock == 8, "one or two spectral blocks per 8-complex K half");
 constexpr uint32_t kTmaA = kTM * 256;  // 2 halves x 128 rows x 128 B
 constexpr uint32_t kTmaB = kTR * 256;
 constexpr uint32_t kTmaStage = kTmaA + kTmaB;  // 40 KB, 1024-byte aligned
@@ -271,9 +273,19 @@ __device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap* map, 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap* map, int x, int y, int z, int w,
+                                          uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(umma::smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_zgemm3m_fwd_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      double2* __restrict__ Y, int nf, int nd, int nm, int nrhs, int j0, int nj, bool accumulate) {
+                      double2* __restrict__ Y, int nf, int nd, int nm, int nrhs, int j0, int nj, bool accumulate,
+                      bool xblocked) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     const uint32_t base_u = (umma::smem_u32(smraw) + 1023u) & ~1023u;
     unsigned char* base = smraw + (base_u - umma::smem_u32(smraw));
@@ -310,7 +322,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         tma_load3(sa + h * (kTmaA / 2), &tmA, x + 16 * h, d.m0, d.f, full + st, pol_a);
-                        tma_load3(sa + kTmaA + h * (kTmaB / 2), &tmB, x + 16 * h, d.r0, d.f, full + st, pol_b);
+                        if (xblocked)  // X channel-blocked: (G complex, f, j / G, r), 8 / G j blocks per half
+                            tma_load4(sa + kTmaA + h * (kTmaB / 2), &tmB, 0, d.f,
+                                      (j0 + kt * kKC) / kSpecBlock + (8 / kSpecBlock) * h, d.r0, full + st, pol_b);
+                        else
+                            tma_load3(sa + kTmaA + h * (kTmaB / 2), &tmB, x + 16 * h, d.r0, d.f, full + st, pol_b);
                     }
                 }
             }
@@ -344,7 +360,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 const int kk = 8 * half + c;
                 const int sw = (c ^ g) << 4;  // every fragment row here is = g (mod 8)
                 const unsigned char* Ah = sa + half * (kTmaA / 2) + sw;
-                const unsigned char* Bh = sa + kTmaA + half * (kTmaB / 2) + sw;
+                // blocked X arrives unswizzled (a 64-byte inner box cannot take the
+                // 128-byte swizzle): 2-way conflicts on the two B loads only
+                const unsigned char* Bh = sa + kTmaA + half * (kTmaB / 2) + (xblocked && !kXBlockSwizzle ? c << 4 : sw);
                 double2 a[kMT][2], b[2];
 #pragma unroll
                 for (int mt = 0; mt < kMT; ++mt)
@@ -519,7 +537,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // Everything past N_d / N_m / nrhs is zero-filled by the TMA unit.
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_zgemm3m_adj_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      double2* __restrict__ Y, int nf, int nd, int nm, int nrhs, int jbase, int jend) {
+                      double2* __restrict__ Y, int nf, int nd, int nm, int nrhs, int jbase, int jend,
+                      bool yblocked) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     const uint32_t base_u = (umma::smem_u32(smraw) + 1023u) & ~1023u;
     unsigned char* base = smraw + (base_u - umma::smem_u32(smraw));
@@ -621,9 +640,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     for (int h = 0; h < 2; ++h) {
                         const int jj = d.j0 + wm * (16 * kMT) + mt * 16 + h * 8 + g;
                         const int cc = 2 * h + q;
-                        if (jj < jend)
-                            yr[jj] = make_double2(p1[mt][nt][cc] + p2[mt][nt][cc],
-                                                  p3[mt][nt][cc] - p1[mt][nt][cc] + p2[mt][nt][cc]);
+                        if (jj < jend) {
+                            const double2 v = make_double2(p1[mt][nt][cc] + p2[mt][nt][cc],
+                                                           p3[mt][nt][cc] - p1[mt][nt][cc] + p2[mt][nt][cc]);
+                            if (yblocked) {  // channel c = r nm + j, blocks of kSpecBlock channels
+                                const size_t ch = (size_t)r * nm + jj;
+                                Y[((ch / kSpecBlock) * nf + d.f) * kSpecBlock + ch % kSpecBlock] = v;
+                            } else {
+                                yr[jj] = v;
+                            }
+                        }
                     }
                 }
     }
@@ -658,6 +684,25 @@ bool encode_rows(CUtensorMap* m, const void* ptr, int cols, int rows, int planes
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// X channel-blocked ([r nm + j] / 4, f, (r nm + j) % 4): dims (8 doubles, nf, nm / 4, nrhs), box (8, 1, 2, 32)
+bool encode_blocked(CUtensorMap* m, const void* ptr, int nm, int nrhs, int nf) {
+    const EncodeTiled fn = encode_fn();
+    if (!fn || nm % kSpecBlock) return false;
+    const cuuint64_t blk = (cuuint64_t)kSpecBlock * 16;  // bytes per (block, f)
+    const cuuint64_t dims[4] = {(cuuint64_t)2 * kSpecBlock, (cuuint64_t)nf, (cuuint64_t)nm / kSpecBlock,
+                                (cuuint64_t)nrhs};
+    const cuuint64_t strides[3] = {blk, blk * nf, blk * nf * (nm / kSpecBlock)};
+    const cuuint32_t box[4] = {2 * kSpecBlock, 1, 8 / kSpecBlock, (cuuint32_t)kTR};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    // 8-channel blocks: 128-byte inner box, swizzled like the frequency-major tile.
+    // (4-channel blocks take no swizzle: with a 64-byte inner box the 128-byte
+    // swizzle pads every row to 128 bytes — measured: the box overran its slot.)
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, kXBlockSwizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int sm_count() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -671,18 +716,24 @@ int sm_count() {
 }  // namespace
 
 // Host launchers (declared in btg_kernels.cuh): one persistent CTA per SM.
+bool zgemm_tma_ok(int nm) { return encode_fn() != nullptr && nm % kSpecBlock == 0; }
+
 cudaError_t launch_zgemm3m_fwd_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
-                                  int j0, int nj, bool accumulate, cudaStream_t stream) {
+                                  int j0, int nj, bool accumulate, cudaStream_t stream, bool xblocked) {
     const char* cp = std::getenv("BTG_ZGEMM_FWD_CPASYNC");  // A/B: the cp.async producer
     CUtensorMap ta, tb;
-    if (!(cp && *cp && *cp != '0') && encode_rows(&ta, F, nm, nd, nf, kTM) && encode_rows(&tb, X, nm, nrhs, nf, kTR)) {
+    if (xblocked && (j0 % kSpecBlock || !zgemm_tma_ok(nm))) return cudaErrorNotSupported;
+    if (xblocked || (!(cp && *cp && *cp != '0') && encode_rows(&tb, X, nm, nrhs, nf, kTR))) {
+        if (!encode_rows(&ta, F, nm, nd, nf, kTM)) return cudaErrorNotSupported;
+        if (xblocked && !encode_blocked(&tb, X, nm, nrhs, nf)) return cudaErrorNotSupported;
         const size_t smem = kTmaStages * kTmaStage + 1024 + 2 * kTmaStages * sizeof(uint64_t);
         cudaError_t e =
             cudaFuncSetAttribute(k_zgemm3m_fwd_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const long long tiles = (long long)nf * ((nd + kTM - 1) / kTM) * ((nrhs + kTR - 1) / kTR);
         const int grid = (int)std::min<long long>(tiles, sm_count());
-        k_zgemm3m_fwd_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, nj, accumulate);
+        k_zgemm3m_fwd_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, nj, accumulate,
+                                                              xblocked);
         return cudaGetLastError();
     }
     const size_t smem = kFwdStages * kFwdStage + 2 * kFwdStages * sizeof(uint64_t);
@@ -695,17 +746,19 @@ cudaError_t launch_zgemm3m_fwd_ws(const double2* F, const double2* X, double2* Y
 }
 
 cudaError_t launch_zgemm3m_adj_ws(const double2* F, const double2* X, double2* Y, int nf, int nd, int nm, int nrhs,
-                                  int j0, int nj, cudaStream_t stream) {
+                                  int j0, int nj, cudaStream_t stream, bool yblocked) {
     const char* bk = std::getenv("BTG_ZGEMM_ADJ_BULK");  // A/B: the 1-D bulk-copy producer
     CUtensorMap ta, tb;
-    if (!(bk && *bk && *bk != '0') && encode_rows(&ta, F, nm, nd, nf, kKC) && encode_rows(&tb, X, nd, nrhs, nf, kTR)) {
+    if (yblocked && !zgemm_tma_ok(nm)) return cudaErrorNotSupported;
+    if ((yblocked || !(bk && *bk && *bk != '0')) && encode_rows(&ta, F, nm, nd, nf, kKC) &&
+        encode_rows(&tb, X, nd, nrhs, nf, kTR)) {
         const size_t smem = kTmaStages * kTmaStage + 1024 + 2 * kTmaStages * sizeof(uint64_t);
         cudaError_t e =
             cudaFuncSetAttribute(k_zgemm3m_adj_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const long long tiles = (long long)nf * ((nj + kTM - 1) / kTM) * ((nrhs + kTR - 1) / kTR);
         const int grid = (int)std::min<long long>(tiles, sm_count());
-        k_zgemm3m_adj_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, j0 + nj);
+        k_zgemm3m_adj_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, j0 + nj, yblocked);
         return cudaGetLastError();
     }
     const size_t smem = kAdjStages * kAdjStage + 2 * kAdjStages * sizeof(uint64_t);
