@@ -822,6 +822,228 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
 }
 
 // ---------------------------------------------------------------------------
+// c2r from the channel-blocked layout (kBlockedFs) with TMA: persistent CTAs,
+// two per SM (<= 128 registers); the CTA's whole input — one contiguous
+// (N+1) x CPB block — arrives by ONE bulk copy into the channel buffers, the
+// first pass reads its (X_k, X_{N-k}) pairs from there, and the next group's
+// block is requested as soon as the last pass has read the buffers, so it lands
+// under the Gamma^-1 / alpha R v epilogue and the stores.
+// ---------------------------------------------------------------------------
+#ifndef BTG_C2R_TMA_MINB
+#define BTG_C2R_TMA_MINB 1
+#endif
+template <int N, int CPB>
+__host__ __device__ constexpr bool c2r_tma_ok() {
+    return CPB == kSpecBlock &&
+           (N / last_radix(typename FastPlan<N>::C2R{}) + FastPlan<N>::TPC - 1) / FastPlan<N>::TPC == 1 &&
+           (size_t)(N + 1) * CPB <= (size_t)CPB * chan_stride(N);
+}
+#ifndef BTG_C2R_TMA_STAGE
+#define BTG_C2R_TMA_STAGE 1
+#endif
+constexpr bool kC2RTmaStage = BTG_C2R_TMA_STAGE;
+template <int N, int CPB>
+__host__ __device__ constexpr size_t smem_bytes_c2r_tma() {
+    return smem_dir<N, CPB, false>() + 16 + (kC2RTmaStage ? sizeof(double2) * (N + 1) * CPB : 0);
+}
+template <int N, int CPB>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
+    k_c2r_tma(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
+               int channels, FastTables tabs, C2REpilogue epi) {
+    (void)in_fs;  // always channel-blocked
+    using P = FastPlan<N>;
+    using RL = typename P::C2R;
+    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int HI = tw_hi_count<N>();
+    extern __shared__ double2 sm[];
+    double2* lo = sm + CPB * CS;
+    double2* hi = lo + kTwLo;
+    double2* plo = hi + HI;
+    double2* phi = plo + kTwLo;
+    load_tables(lo, hi, HI, tabs.lo, tabs.hi);
+    load_tables(plo, phi, HI + 1, tabs.post_lo, tabs.post_hi);
+    double2* w2q = plo + kTwLo + HI + 2;  // == sm + CPB*CS + 2*kTwLo + 2*HI + 2
+    double2* ptab = w2q + w2q_entries<N, true>();
+    constexpr int LIM = TabPlan<N>::C2R;
+    load_direct_tables<N, LIM, RL, true>(w2q, ptab, tabs);
+    const double2* ptab_last = ptab + tab_entries_but_last<1, LIM>(RL{});
+    const int b = threadIdx.x % CPB;
+    const int tc = threadIdx.x / CPB;
+    double2* s = sm + b * CS;
+    // the group's channel-blocked input block lands where the channel buffers are
+    // kC2RTmaStage: a separate staging block (the next group's copy overlaps all
+    // passes) or the channel buffers themselves (copy overlaps the epilogue only)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + smem_dir<N, CPB, false>() / sizeof(double2));
+    double2* stage_buf = kC2RTmaStage ? reinterpret_cast<double2*>(bar + 2) : sm;
+    const double2* stage = stage_buf;
+    const int groups = channels / CPB;
+    constexpr uint32_t kBlockBytes = (uint32_t)((N + 1) * CPB * sizeof(double2));
+    auto issue = [&](int g) {
+        umma::mbar_expect_tx(bar, kBlockBytes);
+        umma::bulk_load(stage_buf, in + (long long)g * (N + 1) * CPB, kBlockBytes, bar, umma::policy_evict_first());
+    };
+    if (threadIdx.x == 0) {
+        umma::mbar_init(bar, 1);
+        umma::mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < groups) issue(blockIdx.x);
+    double dacc = 0.0;  // folded dot (epi.dot_out), over every group of this CTA
+    uint32_t phase = 0;
+    for (int g = blockIdx.x; g < groups; g += gridDim.x, phase ^= 1u) {
+    const int c = g * CPB + b;
+    const bool live = true;
+    umma::mbar_wait(bar, phase);
+
+    // ---- pass 1 on butterfly pairs: Z from (X_k, X_{N-k}) loaded frequency-major
+    {
+        constexpr int R = first_radix(RL{});
+        constexpr int NB = N / R;
+        constexpr int NU = NB / 2;
+        constexpr int UF = (NU + TPC - 1) / TPC;
+        constexpr double inv_len = 0.5 / N;
+        auto X = [&](int k) { return stage[k * CPB + b]; };
+        double2 va[UF][R], vb[UF][R];
+#pragma unroll
+        for (int uf = 0; uf < UF; ++uf) {
+            const int u = tc + uf * TPC;
+            if (NU % TPC != 0 && u >= NU) continue;
+            const int ja = u == 0 ? 0 : u;
+            if (u != 0) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int k = ja + q * NB;  // partner N - k = jb + (R-1-q) NB
+                    const double2 xk = X(k), xn = X(N - k);
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
+                    presplit_pair(xk, xn, w, inv_len, va[uf][q], vb[uf][R - 1 - q]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int qp = (R - q) % R;
+                    if (q > qp && q != 0) continue;
+                    const int k = q * NB;
+                    const double2 xk = X(k), xn = X(N - k);  // q = 0: X_0 and X_N
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
+                    double2 zk, zn;
+                    presplit_pair(xk, xn, w, inv_len, zk, zn);
+                    va[uf][q] = zk;
+                    if (q != qp) va[uf][qp] = zn;
+                }
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int qp = R - 1 - q;
+                    if (q > qp) continue;
+                    const int k = NB / 2 + q * NB;
+                    const double2 xk = X(k), xn = X(N - k);
+                    const double2 w = w2n_lookup<N, true>(w2q, plo, phi, k);
+                    double2 zk, zn;
+                    presplit_pair(xk, xn, w, inv_len, zk, zn);
+                    vb[uf][q] = zk;
+                    if (q != qp) vb[uf][qp] = zn;
+                }
+            }
+            dft<R, +1>(va[uf]);
+            dft<R, +1>(vb[uf]);
+        }
+        // every pair read from the staged block before any buffer write (aliased
+        // stage) / before the next block is requested (separate stage)
+        __syncthreads();
+        if (kC2RTmaStage && threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
+#pragma unroll
+        for (int uf = 0; uf < UF; ++uf) {
+            const int u = tc + uf * TPC;
+            if (NU % TPC != 0 && u >= NU) continue;
+            const int ja = u == 0 ? 0 : u;
+            const int jb = u == 0 ? NB / 2 : NB - u;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                s[pad_idx(ja * R + q)] = va[uf][q];
+                s[pad_idx(jb * R + q)] = vb[uf][q];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- middle passes
+    passes_but_last<N, TPC, first_radix(RL{}), +1, LIM>(s, tc, lo, hi, w2q, ptab, tail(RL{}));
+
+    // ---- last pass: outputs p = j + q NB; keep p < N/2 (t = 2p, 2p+1 < N)
+    constexpr int R = last_radix(RL{});
+    constexpr int NS = ns_of_last(RL{});
+    constexpr int NB = N / R;
+    constexpr int BF = (NB + TPC - 1) / TPC;
+    {
+    double* orow = out + (long long)c * out_cs;
+    const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+    const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
+#pragma unroll
+    for (int bf = 0; bf < BF; ++bf) {
+        const int j = tc + bf * TPC;
+        if (NB % TPC == 0 || j < NB) {
+            // epilogue operands first (16-byte loads), so their latency overlaps the pass
+            constexpr int NQ = (R + 1) / 2;
+            double2 er[NQ], eg[NQ];
+            double el[NQ], eh[NQ];
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int p = j + q * NB;
+                const bool ok = p < N / 2;
+                const int t0 = 2 * p;
+                er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
+                el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
+                eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
+                eg[q] = (epi.gamma_mode == 2 && ok)
+                            ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
+                            : make_double2(1.0, 1.0);
+            }
+            double2 v[R];
+            #pragma unroll
+            for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
+            static_assert(BF == 1, "one last-pass butterfly per thread: the refill follows its reads");
+            if (!kC2RTmaStage) {
+                __syncthreads();  // every channel buffer read: the next block may land
+                if (threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
+            }
+            twiddle_pass<N, R, NS, +1, LIM>(v, j, lo, hi, w2q, ptab_last);
+            dft<R, +1>(v);
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q) {  // keep p = j + q*NB < N/2 (unpad)
+                const int p = j + q * NB;
+                if ((R % 2 == 1) && q == R / 2 && p >= N / 2) break;
+                double y0 = v[q].x, y1 = v[q].y;
+                if (epi.gamma_mode == 1) {
+                    const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
+                    y0 *= g;
+                    y1 *= g;
+                } else if (epi.gamma_mode == 2) {
+                    y0 *= eg[q].x;
+                    y1 *= eg[q].y;
+                }
+                if (vrow) {
+                    double r0 = er[q].x, r1 = er[q].y;
+                    if (epi.reg_kind == 1) {
+                        const double a0 = 2.0 * r0 - el[q] - r1;  // reference order: 2x - x[t-1] - x[t+1]
+                        const double a1 = 2.0 * r1 - r0 - eh[q];
+                        r0 = a0;
+                        r1 = a1;
+                    }
+                    y0 += epi.alpha * r0;
+                    y1 += epi.alpha * r1;
+                }
+                reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
+                if (drow) {
+                    const double2 dv = __ldg(reinterpret_cast<const double2*>(drow) + p);
+                    dacc = fma(dv.x, y0, fma(dv.y, y1, dacc));
+                }
+            }
+        }
+    }
+    }
+    }
+    if (epi.dot_out) cta_dot_store(dacc, epi.dot_out);
+}
+
+// ---------------------------------------------------------------------------
 // Persistent variants (plans with PF_R2C / PF_C2R): the same passes, looping
 // over channel groups (group g = blockIdx.x + i gridDim.x); the first pass's
 // global loads for the NEXT group are issued into registers right after this

@@ -796,6 +796,20 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         return cudaErrorNotSupported;
     } else {
         constexpr size_t smem = fast::smem_dir<N, CPB, false>();
+        if constexpr (fast::c2r_tma_ok<N, CPB>()) {
+            // channel-blocked input: one bulk copy per 4-channel group (k_c2r_tma)
+            if (in_fs < 0 && !std::getenv("BTG_C2R_NO_TMA")) {
+                if (channels % CPB) return cudaErrorNotSupported;
+                constexpr size_t smem_t = fast::smem_bytes_c2r_tma<N, CPB>();
+                auto kt = fast::k_c2r_tma<N, CPB>;
+                cudaError_t e = set_smem(kt, smem_t);
+                if (e != cudaSuccess) return e;
+                const int grid = persistent_grid(kt, P::TPC * CPB, smem_t, channels / CPB);
+                if (ctas) *ctas = grid;
+                kt<<<grid, P::TPC * CPB, smem_t, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
+                return cudaGetLastError();
+            }
+        }
         auto kern = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
