@@ -68,7 +68,15 @@ BTG_PLAN(128,   16,  16, 16,  1024, 1024, false, false, BTG_R(8, 4, 4),         
 BTG_PLAN(256,   16,  16, 16,  512,  256,  true,  true,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
 BTG_PLAN(500,   64,  4,  4,   1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
 BTG_PLAN(512,   64,  4,  4,   256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
-BTG_PLAN(1000,  128, 2,  2,   1024, 1024, false, false, BTG_R(8, 5, 5, 5),      BTG_R(5, 5, 5, 8))
+#ifndef BTG_P1000_TPC
+#define BTG_P1000_TPC 128
+#define BTG_P1000_CPBR 2
+#define BTG_P1000_CPBC 2
+#define BTG_P1000_RESR 1024
+#define BTG_P1000_RESC 1024
+#endif
+BTG_PLAN(1000,  BTG_P1000_TPC, BTG_P1000_CPBR, BTG_P1000_CPBC, BTG_P1000_RESR, BTG_P1000_RESC, false, false,
+         BTG_R(8, 5, 5, 5), BTG_R(5, 5, 5, 8))
 // (BTG_P1024_* override the N_t = 1024 plan in plan sweeps)
 #ifndef BTG_P1024_TPC
 #define BTG_P1024_TPC 64
