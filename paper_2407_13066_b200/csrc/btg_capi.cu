@@ -322,6 +322,7 @@ btg_status run_c2r_vec(btg_op op, const double2* in, size_t channels, double* ou
                                           (int)channels, op->fast, epi, op->stream, dot_ctas));
     } else {
         // the generic kernels have no folded dot: the caller falls back (dot_ctas = 0)
+        if (epi.npeers) return fail(BTG_EARG, "internal: fused grid reduce needs the fast C2R");
         btg::C2REpilogue e = epi;
         e.dot_v = nullptr;
         e.dot_out = nullptr;
@@ -774,7 +775,8 @@ btg_status host_adjoint_stage_mrhs(btg_op op, double* m_host, size_t nrhs, const
 }
 
 btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, double* out,
-                     size_t out_len, size_t nrhs, const btg_epilogue* ex, unsigned flags) {
+                     size_t out_len, size_t nrhs, const btg_epilogue* ex, unsigned flags,
+                     const double* const* peers = nullptr, int npeers = 0) {
     BTG_TRY(check_ready(op));
     if (nrhs == 0) return fail(BTG_EARG, "nrhs must be >= 1");
     if (!in || !out) return fail(BTG_EARG, "null vector pointer");
@@ -847,6 +849,8 @@ btg_status apply_dir(btg_op op, bool adjoint, const double* in, size_t in_len, d
         BTG_TRY(run_r2c_vec(op, din_p, nrhs * op->nd, op->wa));
         return host_adjoint_stage_mrhs(op, out, nrhs, epi);
     }
+    epi.peers = peers;
+    epi.npeers = npeers;
     BTG_TRY(pipeline(op, adjoint, din_p, dout_p, nrhs, epi));
     return finish_host(op, out, dout_p, out_len, flags);
 }
@@ -1405,6 +1409,26 @@ btg_status btg_slice_operator(btg_op src, size_t i0, size_t i1, size_t j0, size_
 
 // Internal hooks for btg_io.cu (C++ linkage, not part of the C ABI).
 btg_status btg_internal_fail(btg_status s, const char* msg) { return fail(s, "%s", msg); }
+
+// Grid engine (btg_grid_engine.cu, P2P transport): one device-pointer, single-RHS
+// F / F* whose final C2R also tree-reduces the partials of `npeers` other group
+// members into its stores (C2REpilogue::peers). btg_internal_fused_ok says
+// whether this handle's C2R takes that path (fast plan, FP64 or FP32, 1 RHS).
+int btg_internal_fused_ok(btg_op op, int adjoint) {
+    if (!op || !op->fast_ok) return 0;
+    (void)adjoint;
+    return 1;
+}
+btg_status btg_internal_apply_fused(btg_op op, int adjoint, const double* in, size_t in_len, double* out,
+                                    size_t out_len, const btg_epilogue* ex, const double* const* peers, int npeers) {
+    if (!op) return fail(BTG_EARG, "null operator handle");
+    if (npeers < 1 || npeers > btg::kMaxFusedPeers) return fail(BTG_EARG, "fused reduce: %d peers", npeers);
+    if (!btg_internal_fused_ok(op, adjoint)) return fail(BTG_EARG, "fused reduce: no fast C2R for this horizon");
+    if (!aligned16(out) || (ex && ex->reg_v && !aligned16(ex->reg_v)))
+        return fail(BTG_EARG, "fused reduce: 16-byte aligned vectors required");
+    std::lock_guard<std::mutex> lock(op->mu);
+    return apply_dir(op, adjoint != 0, in, in_len, out, out_len, 1, ex, BTG_DEVICE_PTRS, peers, npeers);
+}
 
 btg_status btg_internal_upload_spectrum_block(btg_op op, size_t f, const double* block) {
     if (!op || !block || f > op->nt) return fail(BTG_EARG, "bad spectrum block upload");

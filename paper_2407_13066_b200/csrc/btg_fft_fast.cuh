@@ -506,6 +506,35 @@ __device__ __forceinline__ long long spec_stride(long long fs) {
     return fs < 0 ? kSpecBlock : fs;
 }
 
+// tree_reduce (distributed.cpp:36-47) of {(y0, y1), peer values at element
+// `off`} in member order, level by level: v[a] += v[a + step].
+__device__ __forceinline__ void peer_tree_reduce(const C2REpilogue& epi, long long off, double& y0, double& y1) {
+    double a0[kMaxFusedPeers + 1], a1[kMaxFusedPeers + 1];
+    a0[0] = y0;
+    a1[0] = y1;
+    const int m = epi.npeers + 1;
+#pragma unroll
+    for (int k = 1; k <= kMaxFusedPeers; ++k) {
+        if (k < m) {
+            const double2 pv = __ldg(reinterpret_cast<const double2*>(epi.peers[k - 1] + off));
+            a0[k] = pv.x;
+            a1[k] = pv.y;
+        } else {
+            a0[k] = a1[k] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int step = 1; step <= kMaxFusedPeers; step *= 2)
+#pragma unroll
+        for (int a = 0; a + step <= kMaxFusedPeers; a += 2 * step)
+            if (a + step < m) {
+                a0[a] += a0[a + step];
+                a1[a] += a1[a + step];
+            }
+    y0 = a0[0];
+    y1 = a1[0];
+}
+
 // CTA sum of the folded dot product (C2REpilogue::dot_out), one value per CTA.
 __device__ __forceinline__ void cta_dot_store(double acc, double* out) {
     __shared__ double red[32];
@@ -661,7 +690,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 // ---------------------------------------------------------------------------
 // c2r: frequency-major in[k*in_fs + c] -> SOTI rows out[c*out_cs + t], t < N
 // ---------------------------------------------------------------------------
-template <int N, int CPB>
+template <int N, int CPB, bool PEERS = false>
 __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     k_c2r_fast(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
@@ -817,6 +846,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     y0 += epi.alpha * r0;
                     y1 += epi.alpha * r1;
                 }
+                if constexpr (PEERS) peer_tree_reduce(epi, (long long)c * out_cs + 2 * p, y0, y1);
                 reinterpret_cast<double2*>(orow)[p] = make_double2(y0, y1);
                 if (drow) {
                     const double2 dv = __ldg(reinterpret_cast<const double2*>(drow) + p);

@@ -25,8 +25,13 @@
 #include <vector>
 
 #include "../../include/btg.h"
+#include "btg_kernels.cuh"
 
 extern "C" btg_status btg_internal_fail(btg_status s, const char* msg);
+extern "C" int btg_internal_fused_ok(btg_op op, int adjoint);
+extern "C" btg_status btg_internal_apply_fused(btg_op op, int adjoint, const double* in, size_t in_len, double* out,
+                                               size_t out_len, const btg_epilogue* ex, const double* const* peers,
+                                               int npeers);
 
 namespace {
 
@@ -142,8 +147,10 @@ struct btg_grid_s {
         std::vector<double> blocks;    // compact rectangle (naive backend)
         double* d_blocks = nullptr;
         ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+        const double** peer_ptrs = nullptr;  // fused reduce: device array of the group's partials
     };
     std::vector<Cell> cells;  // local cells (all for local grids, one otherwise)
+    std::vector<std::vector<char>> peer_ok;  // local grids: device a can load device b's memory
     std::vector<btg_comm_event> log;
 };
 
@@ -506,6 +513,110 @@ btg_status local_step(Grid* g, Cell& c, const btg_grid_step& s, const CallArgs& 
     return BTG_OK;
 }
 
+// ---- reduce fused into the final C2R (P2P transport) -------------------------
+// A local F (F*) followed by a row (column) reduce / all-reduce onto member 0:
+// the other members compute their partials first, then member 0's C2R loads
+// them over NVLink (peer access) and stores the reference's tree_reduce of all
+// members (C2REpilogue::peers) — no receive copies, no separate add kernels.
+// Bit-identical to the unfused P2P path (same tree, same additions).
+bool fused_enabled() {
+    const char* v = std::getenv("BTG_GRID_FUSED");
+    return !(v && *v == '0');
+}
+
+std::vector<Cell*> group_members(Grid* g, int group, size_t grp) {
+    const size_t members = group == BTG_GROUP_ROW ? g->cols : g->rows;
+    std::vector<Cell*> mem(members, nullptr);
+    for (auto& c : g->cells)
+        if (group_id(c, group) == grp) mem[member_idx(c, group)] = &c;
+    return mem;
+}
+
+bool fusable(Grid* g, const btg_grid_step& local, const btg_grid_step& red) {
+    if (!fused_enabled() || g->transport != BTG_TRANSPORT_P2P || !g->local || g->backend != 0) return false;
+    if ((red.op != BTG_STEP_REDUCE && red.op != BTG_STEP_ALLREDUCE) || red.root != 0 || red.src != local.dst)
+        return false;
+    const bool adjoint = local.op == BTG_STEP_ADJOINT;
+    const size_t ngroups = red.group == BTG_GROUP_ROW ? g->rows : g->cols;
+    for (size_t grp = 0; grp < ngroups; ++grp) {
+        auto mem = group_members(g, red.group, grp);
+        if (mem.size() > (size_t)btg::kMaxFusedPeers + 1) return false;
+        if (mem.size() < 2) continue;
+        for (Cell* c : mem)
+            if (!c) return false;
+        Cell* root = mem[0];
+        if (cell_empty(g, *root) || !root->op || !btg_internal_fused_ok(root->op, adjoint ? 1 : 0)) return false;
+        for (Cell* c : mem)
+            if (root->device >= (int)g->peer_ok.size() || c->device >= (int)g->peer_ok.size() ||
+                !g->peer_ok[root->device][c->device])
+                return false;
+    }
+    return true;
+}
+
+btg_status fused_local_reduce(Grid* g, const std::vector<std::vector<btg_grid_step>>& sch, size_t st,
+                              const CallArgs& a) {
+    const btg_grid_step& red = sch[0][st + 1];
+    const bool adjoint = sch[0][st].op == BTG_STEP_ADJOINT;
+    const size_t ngroups = red.group == BTG_GROUP_ROW ? g->rows : g->cols;
+    for (size_t grp = 0; grp < ngroups; ++grp) {
+        auto mem = group_members(g, red.group, grp);
+        Cell* root = mem[0];
+        const btg_grid_step& rs = sch[root->rank][st];
+        if (mem.size() < 2) {
+            G_TRY(local_step(g, *root, rs, a));
+            continue;
+        }
+        // the other members' partials
+        std::vector<const double*> ptrs;
+        for (size_t k = 1; k < mem.size(); ++k) {
+            Cell* c = mem[k];
+            G_TRY(local_step(g, *c, sch[c->rank][st], a));
+            DevGuard dg(c->device);
+            G_CUDA(cudaEventRecord(c->ev, c->stream));
+            DevGuard dr(root->device);
+            G_CUDA(cudaStreamWaitEvent(root->stream, c->ev, 0));
+            ptrs.push_back(c->buf[sch[c->rank][st].dst]);
+        }
+        // member 0: its own F / F* with the tree reduce in the C2R stores
+        DevGuard dg(root->device);
+        if (!root->peer_ptrs) G_CUDA(cudaMalloc(&root->peer_ptrs, btg::kMaxFusedPeers * sizeof(double*)));
+        G_CUDA(cudaMemcpyAsync(root->peer_ptrs, ptrs.data(), ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice,
+                               root->stream));
+        const size_t ld = cell_ld(g, *root), lm = cell_lm(g, *root), nt = g->nt;
+        const size_t nin = (adjoint ? ld : lm) * nt, nout = (adjoint ? lm : ld) * nt;
+        btg_epilogue epi{};
+        const bool gamma = rs.gamma && a.gamma_kind != BTG_GAMMA_NONE;
+        const bool reg = rs.reg && a.alpha != 0.0;
+        if (gamma) {
+            epi.gamma_inv = root->gam;
+            epi.gamma_kind = a.gamma_kind;
+        }
+        if (reg) {
+            epi.reg_v = root->buf[0];
+            epi.alpha = a.alpha;
+            epi.reg_kind = a.reg_kind;
+        }
+        G_TRY(btg_set_stream(root->op, root->stream));
+        G_TRY(btg_internal_apply_fused(root->op, adjoint ? 1 : 0, root->buf[rs.src], nin, root->buf[rs.dst], nout,
+                                       (gamma || reg) ? &epi : nullptr, root->peer_ptrs, (int)ptrs.size()));
+        // the partials are read: their buffers may be reused
+        G_CUDA(cudaEventRecord(root->ev, root->stream));
+        for (size_t k = 1; k < mem.size(); ++k) {
+            DevGuard dm(mem[k]->device);
+            G_CUDA(cudaStreamWaitEvent(mem[k]->stream, root->ev, 0));
+        }
+    }
+    if (red.op == BTG_STEP_ALLREDUCE) {  // member 0 holds the sum: broadcast it over the group
+        btg_grid_step b = red;
+        b.op = BTG_STEP_BROADCAST;
+        b.root = 0;
+        G_TRY(p2p_collective(g, b));
+    }
+    return BTG_OK;
+}
+
+
 // Gamma^-1 rows of the cell on its device (the C2R epilogue reads them there):
 // a one-rank grid with a 16-byte aligned device pointer borrows them in place.
 btg_status stage_gamma(Grid* g, Cell& c, const CallArgs& a) {
@@ -607,6 +718,16 @@ btg_status run(Grid* g, int kind, const CallArgs& a) {
             }
             case BTG_STEP_FORWARD:
             case BTG_STEP_ADJOINT: {
+                if (st + 1 < nsteps && fusable(g, s, sch[0][st + 1])) {
+                    G_TRY(fused_local_reduce(g, sch, st, a));
+                    ++st;  // the reduce ran inside member 0's C2R
+                    break;
+                }
+                // BTG_GRID_FUSED_REQUIRE=1 (tests): a P2P reduce that could not be fused is an error
+                if (st + 1 < nsteps && g->transport == BTG_TRANSPORT_P2P && fused_enabled() &&
+                    (sch[0][st + 1].op == BTG_STEP_REDUCE || sch[0][st + 1].op == BTG_STEP_ALLREDUCE) &&
+                    std::getenv("BTG_GRID_FUSED_REQUIRE"))
+                    return gfail(BTG_EARG, "fused reduce required but not applicable");
                 if (g->parallel && g->cells.size() > 1) {
                     std::vector<btg_status> rs(g->cells.size(), BTG_OK);
                     std::vector<std::string> msg(g->cells.size());
@@ -650,6 +771,7 @@ void destroy_cell(Cell& c) {
     if (c.world) ncclCommDestroy(c.world);
     if (c.ev) cudaEventDestroy(c.ev);
     if (c.own_stream) cudaStreamDestroy(c.own_stream);
+    cudaFree(c.peer_ptrs);
 }
 
 btg_status bind_op(Cell& c, btg_op op, bool own) {
@@ -785,6 +907,22 @@ btg_status btg_grid_create_local(size_t rows, size_t cols, const int* devices, s
     for (size_t k = 0; k < n; ++k) rd.emplace_back(k, devs[k % devs.size()]);
     btg_status s = create_cells(g, rd);
     if (s != BTG_OK) return bail(s);
+    // P2P: direct loads between the grid's devices (NVLink) where the hardware allows
+    g->peer_ok.assign(ndev, std::vector<char>(ndev, 0));
+    for (int a : devs)
+        for (int b : devs) {
+            if (a == b) {
+                g->peer_ok[a][b] = 1;
+                continue;
+            }
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
+                DevGuard dg(a);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) g->peer_ok[a][b] = 1;
+                cudaGetLastError();
+            }
+        }
     if (transport == BTG_TRANSPORT_NCCL) {
         std::vector<int> list;
         for (auto& c : g->cells) list.push_back(c.device);

@@ -798,7 +798,7 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         constexpr size_t smem = fast::smem_dir<N, CPB, false>();
         if constexpr (fast::c2r_tma_ok<N, CPB>()) {
             // channel-blocked input: one bulk copy per 4-channel group (k_c2r_tma)
-            if (in_fs < 0 && !std::getenv("BTG_C2R_NO_TMA")) {
+            if (in_fs < 0 && !std::getenv("BTG_C2R_NO_TMA") && !epi.npeers) {
                 if (channels % CPB) return cudaErrorNotSupported;
                 constexpr size_t smem_t = fast::smem_bytes_c2r_tma<N, CPB>();
                 auto kt = fast::k_c2r_tma<N, CPB>;
@@ -810,11 +810,14 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
                 return cudaGetLastError();
             }
         }
-        auto kern = P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>;
+        // the grid reduce fused into the stores (epi.npeers): its own instantiation,
+        // so the other C2Rs carry no peer-load code (it cost them 10-17 %)
+        auto kern = epi.npeers ? fast::k_c2r_fast<N, CPB, true>
+                               : (P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>);
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         const int groups = (channels + CPB - 1) / CPB;
-        const int grid = P::PF_C2R ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
+        const int grid = (P::PF_C2R && !epi.npeers) ? persistent_grid(kern, P::TPC * CPB, smem, groups) : groups;
         if (ctas) *ctas = grid;
         kern<<<grid, P::TPC * CPB, smem, stream>>>(in, in_fs, out, out_cs, channels, tabs, epi);
         return cudaGetLastError();

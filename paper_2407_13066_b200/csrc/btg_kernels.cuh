@@ -23,7 +23,15 @@ struct C2REpilogue {
     // kernels only; the launcher reports the CTA count).
     const double* dot_v = nullptr;  // SOTI vector sharing the output layout
     double* dot_out = nullptr;
+    // Grid reduce fused into the stores (btg_grid_engine.cu, P2P transport): the
+    // partials of the other npeers members of this cell's row / column group,
+    // same layout as the output, possibly on other GPUs (NVLink peer loads);
+    // device array of pointers. The stored value is the reference's tree_reduce
+    // (distributed.cpp:36-47) of {own, peers[0], ..} in member order.
+    const double* const* peers = nullptr;
+    int npeers = 0;
 };
+constexpr int kMaxFusedPeers = 7;  // groups of up to 8 members
 
 // Split twiddle tables of the compile-time-N vector FFTs (btg_fft_fast.cuh):
 // lo[i] = W_N^i (i < 32), hi[h] = W_N^{32h}; post_* the same for W_{2N}.

@@ -205,3 +205,34 @@ def test_partition_forward_is_reference_tree_of_the_partials():
                                                    s.source_begin:s.source_end])) as op:
             parts.append(op.apply_forward(np.ascontiguousarray(m[s.source_begin:s.source_end])))
     assert np.array_equal(got, R.tree_reduce(parts))
+
+
+@pytest.mark.parametrize("grid,nt", [((2, 3), 64), ((1, 5), 64), ((3, 2), 1024), ((4, 2), 256)])
+def test_p2p_reduce_fused_into_c2r_matches_unfused(monkeypatch, grid, nt):
+    """P2P transport: a local F / F* followed by a group reduce runs as the
+    other members' partials + member 0's C2R loading them (peer access) and
+    storing their tree_reduce (C2REpilogue::peers). Same tree, same additions:
+    identical bits to the unfused path (BTG_GRID_FUSED=0: receive copies + add
+    kernels), for F, F* and the Hessian (row all-reduce) with Gamma^-1 and
+    alpha R v."""
+    from paper_2407_13066_b200.distributed import Partition
+
+    nd, nm = 7, 29
+    blocks, m, d = R.random_problem(41, nd, nm, nt)
+    gs = np.linspace(0.5, 2.0, nd)
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("BTG_GRID_FUSED", fused)
+        if fused == "1":  # every reduce of these schedules must take the fused path
+            monkeypatch.setenv("BTG_GRID_FUSED_REQUIRE", "1")
+        with Partition(blocks, grid) as p:
+            out[fused] = (p.forward(m), p.adjoint(d), p.hessian(m, alpha=0.3, reg="temporal-laplacian", gamma_inv=gs))
+        monkeypatch.delenv("BTG_GRID_FUSED_REQUIRE", raising=False)
+    monkeypatch.delenv("BTG_GRID_FUSED", raising=False)
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    spec = R.setup_full(blocks)
+    f, a, h = out["1"]
+    assert R.rel_l2(f, R.apply_forward(spec, m)) <= 1e-12
+    assert R.rel_l2(a, R.apply_adjoint(spec, d)) <= 1e-12
+    assert R.rel_l2(h, R.gauss_newton_apply(spec, m, gs, 0.3, 1)) <= 1e-12
