@@ -413,6 +413,38 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 struct TileA {  // adjoint tile: frequency, first output column j, first rhs
     int f, j0, r0;
 };
+// (f, j tile, r tile) of tile t = blockIdx.x + i gridDim.x, rhs tiles fastest:
+// one division at the start, then carries (the stride's own decomposition is
+// smaller than each radix, so each digit wraps at most once per step)
+struct TileWalk {
+    int r, j, f, sr, sj, sf, jt, rt;
+    __device__ TileWalk(int t, int stride, int jt_, int rt_) : jt(jt_), rt(rt_) {
+        r = t % rt;
+        t /= rt;
+        j = t % jt;
+        f = t / jt;
+        sr = stride % rt;
+        stride /= rt;
+        sj = stride % jt;
+        sf = stride / jt;
+    }
+    __device__ __forceinline__ void next() {
+        r += sr;
+        int c = 0;
+        if (r >= rt) {
+            r -= rt;
+            c = 1;
+        }
+        j += sj + c;
+        c = 0;
+        if (j >= jt) {
+            j -= jt;
+            c = 1;
+        }
+        f += sf + c;
+    }
+};
+
 __device__ __forceinline__ TileA adj_tile(int t, int jt, int rt, int jbase) {
     TileA d;
     d.r0 = (t % rt) * kTR;
@@ -587,8 +619,15 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int g = lane >> 2, tig = lane & 3;
     const int wm = warp % kWarpsM, wn = warp / kWarpsM;
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileA d = adj_tile(t, jtiles, rtiles, jbase);
+    // tiles walked incrementally (no integer division per tile: the epilogue and
+    // tile setup were ~9 % of the MMA warps' samples)
+    TileWalk tw(blockIdx.x, gridDim.x, jtiles, rtiles);
+    const size_t rstride = yblocked ? (size_t)nm * nf : (size_t)nm;  // Y offset per right-hand side
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tw.next()) {
+        TileA d;
+        d.r0 = tw.r * kTR;
+        d.j0 = jbase + tw.j * kTM;
+        d.f = tw.f;
         double p1[kMT][2][4], p2[kMT][2][4], p3[kMT][2][4];
 #pragma unroll
         for (int a = 0; a < kMT; ++a)
@@ -627,31 +666,30 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             __syncwarp();
             if (lane == 0) umma::mbar_arrive(empty + st);
         }
+        // per-lane output offsets: Y[f][r][j] (or channel-blocked [c/4][f][c%4],
+        // c = r N_m + j, N_m and j0 multiples of 4): base + r * rstride + col(j)
+        const size_t ftile = yblocked ? (size_t)kSpecBlock * d.f : (size_t)d.f * nrhs * nm;
 #pragma unroll
         for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
+            for (int h = 0; h < 2; ++h) {
+                const int jj = d.j0 + wm * (16 * kMT) + mt * 16 + h * 8 + g;
+                if (jj >= jend) continue;
+                const size_t col = yblocked ? (size_t)(jj / kSpecBlock) * kSpecBlock * nf + (jj % kSpecBlock)
+                                            : (size_t)jj;
+                double2* yc = Y + ftile + col;
+                const int cc0 = 2 * h;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int r = d.r0 + wn * 16 + nt * 8 + 2 * tig + q;
-                    if (r >= nrhs) continue;
-                    double2* yr = Y + ((size_t)d.f * nrhs + r) * nm;
+                for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int jj = d.j0 + wm * (16 * kMT) + mt * 16 + h * 8 + g;
-                        const int cc = 2 * h + q;
-                        if (jj < jend) {
-                            const double2 v = make_double2(p1[mt][nt][cc] + p2[mt][nt][cc],
-                                                           p3[mt][nt][cc] - p1[mt][nt][cc] + p2[mt][nt][cc]);
-                            if (yblocked) {  // channel c = r nm + j, blocks of kSpecBlock channels
-                                const size_t ch = (size_t)r * nm + jj;
-                                Y[((ch / kSpecBlock) * nf + d.f) * kSpecBlock + ch % kSpecBlock] = v;
-                            } else {
-                                yr[jj] = v;
-                            }
-                        }
+                    for (int q = 0; q < 2; ++q) {
+                        const int r = d.r0 + wn * 16 + nt * 8 + 2 * tig + q;
+                        if (r >= nrhs) continue;
+                        const int cc = cc0 + q;
+                        yc[(size_t)r * rstride] = make_double2(p1[mt][nt][cc] + p2[mt][nt][cc],
+                                                               p3[mt][nt][cc] - p1[mt][nt][cc] + p2[mt][nt][cc]);
                     }
-                }
+            }
     }
 }
 
