@@ -68,15 +68,11 @@ BTG_PLAN(128,   16,  16, 16,  1024, 1024, false, false, BTG_R(8, 4, 4),         
 BTG_PLAN(256,   16,  16, 16,  512,  256,  true,  true,  BTG_R(16, 4, 4),        BTG_R(4, 4, 16))
 BTG_PLAN(500,   64,  4,  4,   1024, 768,  false, false, BTG_R(4, 5, 5, 5),      BTG_R(5, 5, 5, 4))
 BTG_PLAN(512,   64,  4,  4,   256,  768,  false, false, BTG_R(16, 8, 4),        BTG_R(4, 8, 16))
-#ifndef BTG_P1000_TPC
-#define BTG_P1000_TPC 128
-#define BTG_P1000_CPBR 2
-#define BTG_P1000_CPBC 2
-#define BTG_P1000_RESR 1024
-#define BTG_P1000_RESC 1024
-#endif
-BTG_PLAN(1000,  BTG_P1000_TPC, BTG_P1000_CPBR, BTG_P1000_CPBC, BTG_P1000_RESR, BTG_P1000_RESC, false, false,
-         BTG_R(8, 5, 5, 5), BTG_R(5, 5, 5, 8))
+// N_t = 1000: 10 x 10 x 10 (radix-10 = 2 x 5 in registers), 50 threads per channel
+// — three passes, no idle butterfly slots (the 8.5.5.5 plan at 128 threads left 22 %
+// of its radix-5 slots idle); measured at configs[2] (8192 / 600 channels):
+// R2C 0.100 -> 0.085 ms, C2R 0.127 -> 0.102 ms (profiles/r02s2_fft1000.md)
+BTG_PLAN(1000,  50,  2,  2,   400,  400,  false, false, BTG_R(10, 10, 10),      BTG_R(10, 10, 10))
 // (BTG_P1024_* override the N_t = 1024 plan in plan sweeps)
 #ifndef BTG_P1024_TPC
 #define BTG_P1024_TPC 64
@@ -176,6 +172,28 @@ __device__ __forceinline__ void dft(double2* v) {
     else if constexpr (R == 3) dft3<SIGN>(v);
     else if constexpr (R == 4) dft4<SIGN>(v);
     else if constexpr (R == 5) dft5<SIGN>(v);
+    else if constexpr (R == 10) {
+        // 10 = 2 x 5: dft5 over s of a[r][s] = v[r + 2s], twiddle W_10^{r k}, dft2 over r;
+        // output k + 5 m
+        double2 a[2][5];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) a[r][q] = v[r + 2 * q];
+            dft5<SIGN>(a[r]);
+        }
+        constexpr double c1 = 0.80901699437494742410, s1 = 0.58778525229247312917;  // W_10^1
+        constexpr double c2 = 0.30901699437494742410, s2 = 0.95105651629515357212;  // W_10^2
+        a[1][1] = cmul(a[1][1], make_double2(c1, SIGN * s1));
+        a[1][2] = cmul(a[1][2], make_double2(c2, SIGN * s2));
+        a[1][3] = cmul(a[1][3], make_double2(-c2, SIGN * s2));  // W_10^3
+        a[1][4] = cmul(a[1][4], make_double2(-c1, SIGN * s1));  // W_10^4
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            v[k] = cadd(a[0][k], a[1][k]);
+            v[k + 5] = csub(a[0][k], a[1][k]);
+        }
+    }
     else if constexpr (R == 8) dft8<SIGN>(v);
     else if constexpr (R == 16) {
         // 16 = 4 x 4: columns, twiddle W_16^{r k}, rows, transpose.
