@@ -643,7 +643,21 @@ cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int
                 continue;
             }
         }
-        k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+        // 4 rows x 4 unrolled column steps per thread (16 loads of 16 B in flight): measured
+        // against 8 x 2 (round 1), 16 x 1, 12 x 1, 2 x 8, 4 x 6, 4 x 3 — configs[1] 7.47 ->
+        // 7.36 ms, configs[2] 11.40 -> 10.81 ms, configs[4] shard 19.8 -> 19.0 ms. The
+        // per-thread j order (ascending) and the block reduction are unchanged, so the
+        // results are bit-identical. BTG_FWD_SHAPE=1: the 8 x 2 kernel.
+        static const bool rows8 = [] {
+            const char* e = std::getenv("BTG_FWD_SHAPE");
+            return e && *e == '1';
+        }();
+        if (rows8) {
+            k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+        } else {
+            dim3 g4((nd + 3) / 4, nb);
+            k_gemv_fwd<TF, 1, 4, 4><<<g4, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+        }
     }
     return cudaGetLastError();
 }
