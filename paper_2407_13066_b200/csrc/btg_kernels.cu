@@ -61,6 +61,30 @@ struct FLoad<double2, 1> {
     __device__ __forceinline__ static double2 scalar(const double2* p) { return __ldg(p); }
 };
 
+// Two adjacent FP64 complex in ONE 32-byte load (LDG.E.256 on sm_100a)
+struct Dbl4 {
+    double a, b, c, d;
+};
+template <>
+struct FLoad<double2, 2> {
+    using Raw = Dbl4;
+    __device__ __forceinline__ static void load_raw(const double2* p, uint64_t pol, Raw& r) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+            : "=d"(r.a), "=d"(r.b), "=d"(r.c), "=d"(r.d)
+            : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double2 get(const Raw& r, int v) {
+        return v == 0 ? make_double2(r.a, r.b) : make_double2(r.c, r.d);
+    }
+    __device__ __forceinline__ static void load(const double2* p, uint64_t pol, double2* out) {
+        Raw r;
+        load_raw(p, pol, r);
+        out[0] = make_double2(r.a, r.b);
+        out[1] = make_double2(r.c, r.d);
+    }
+    __device__ __forceinline__ static double2 scalar(const double2* p) { return __ldg(p); }
+};
+
 template <>
 struct FLoad<float2, 1> {
     using Raw = float2;
@@ -652,6 +676,16 @@ cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int
             const char* e = std::getenv("BTG_FWD_SHAPE");
             return e && *e == '1';
         }();
+        if constexpr (sizeof(TF) == 16) {
+            // FP64: two adjacent complex per 32-byte load (LDG.E.256), 2 rows x 4 steps
+            // in flight — configs[1] 7.36 -> 7.32 ms, configs[2] 10.81 -> 10.69 ms over
+            // the 16-byte 4 x 4 kernel (which odd column offsets still take)
+            if (!rows8 && (nm & 1) == 0 && (j0 & 1) == 0) {
+                dim3 g2((nd + 1) / 2, nb);
+                k_gemv_fwd<TF, 2, 2, 4><<<g2, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+                continue;
+            }
+        }
         if (rows8) {
             k_gemv_fwd<TF, 1, kRows, 2><<<grid, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
         } else {
@@ -671,7 +705,7 @@ cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, i
 template <typename TF, int VEC>
 cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0, int nj,
                            cudaStream_t stream) {
-    constexpr int kJpt = 2;
+    constexpr int kJpt = (sizeof(TF) == 16 && VEC == 2) ? 1 : 2;
     constexpr int kUnr = 8;
     const size_t smem = (size_t)nd * sizeof(double2);
     // Default: read d-hat_f through the read-only path (a warp-uniform broadcast
@@ -700,6 +734,11 @@ template <typename TF>
 cudaError_t launch_gemv_adj_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
                                   int nj, cudaStream_t stream) {
     if constexpr (sizeof(TF) == 8) {
+        if ((nm & 1) == 0 && (j0 & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, j0, nj, stream);
+    } else {
+        // FP64: a thread's two columns adjacent and read by ONE 32-byte load (LDG.E.256);
+        // same i-ascending accumulation per column, so bit-identical to the 16-byte
+        // kernel (configs[1] 7.67 -> 7.62 ms, configs[2] 10.83 -> 10.75 ms)
         if ((nm & 1) == 0 && (j0 & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, j0, nj, stream);
     }
     return launch_adj_vec<TF, 1>(F, x, y, nf, nd, nm, j0, nj, stream);
