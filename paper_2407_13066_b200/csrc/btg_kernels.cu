@@ -132,6 +132,34 @@ struct FLoad<float2, 2> {
     }
 };
 
+// Four adjacent FP32 complex in ONE 32-byte load (LDG.E.256 on sm_100a)
+struct Flt8 {
+    float v[8];
+};
+template <>
+struct FLoad<float2, 4> {
+    using Raw = Flt8;
+    __device__ __forceinline__ static void load_raw(const float2* p, uint64_t pol, Raw& r) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+            : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+              "=f"(r.v[7])
+            : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double2 get(const Raw& r, int v) {
+        return make_double2(r.v[2 * v], r.v[2 * v + 1]);
+    }
+    __device__ __forceinline__ static void load(const float2* p, uint64_t pol, double2* out) {
+        Raw r;
+        load_raw(p, pol, r);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) out[v] = make_double2(r.v[2 * v], r.v[2 * v + 1]);
+    }
+    __device__ __forceinline__ static double2 scalar(const float2* p) {
+        const float2 v = __ldg(p);
+        return make_double2(v.x, v.y);
+    }
+};
+
 // acc += a * b
 __device__ __forceinline__ void cmac(double& re, double& im, double2 a, double2 b) {
     re = fma(a.x, b.x, re);
@@ -662,6 +690,14 @@ cudaError_t launch_gemv_fwd_range(const TF* F, const double2* x, double2* y, int
             if ((nm & 1) == 0 && (j0 & 1) == 0) {
                 // FP32 pairs: 16-byte loads of two complex, 4 rows x 2 unrolled steps per
                 // thread (8 rows x 2 spills; measured 3.99 vs 9.98 ms at configs[1])
+                if ((nm & 3) == 0 && (j0 & 3) == 0) {
+                    // four adjacent complex per 32-byte load, 4 rows in flight: FP32
+                    // configs[1] forward 4.05 -> 3.92 ms (4 x 2 / 2 x 4 / 2 x 2 of these
+                    // spill or lose)
+                    dim3 g((nd + 3) / 4, nb);
+                    k_gemv_fwd<TF, 4, 4, 1><<<g, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
+                    continue;
+                }
                 dim3 g4((nd + 3) / 4, nb);
                 k_gemv_fwd<TF, 2, 4, 2><<<g4, kThreads, 0, stream>>>(Fb, xb, yb, nd, nm, j0, nj, accumulate);
                 continue;
@@ -705,7 +741,7 @@ cudaError_t launch_gemv_fwd(const TF* F, const double2* x, double2* y, int nf, i
 template <typename TF, int VEC>
 cudaError_t launch_adj_vec(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0, int nj,
                            cudaStream_t stream) {
-    constexpr int kJpt = (sizeof(TF) == 16 && VEC == 2) ? 1 : 2;
+    constexpr int kJpt = ((sizeof(TF) == 16 && VEC == 2) || VEC == 4) ? 1 : 2;
     constexpr int kUnr = 8;
     const size_t smem = (size_t)nd * sizeof(double2);
     // Default: read d-hat_f through the read-only path (a warp-uniform broadcast
@@ -734,6 +770,9 @@ template <typename TF>
 cudaError_t launch_gemv_adj_range(const TF* F, const double2* x, double2* y, int nf, int nd, int nm, int j0,
                                   int nj, cudaStream_t stream) {
     if constexpr (sizeof(TF) == 8) {
+        // four adjacent columns per thread in one 32-byte load (bit-identical: i-ascending
+        // per column): FP32 configs[1] adjoint 3.98 -> 3.93 ms
+        if ((nm & 3) == 0 && (j0 & 3) == 0) return launch_adj_vec<TF, 4>(F, x, y, nf, nd, nm, j0, nj, stream);
         if ((nm & 1) == 0 && (j0 & 1) == 0) return launch_adj_vec<TF, 2>(F, x, y, nf, nd, nm, j0, nj, stream);
     } else {
         // FP64: a thread's two columns adjacent and read by ONE 32-byte load (LDG.E.256);
