@@ -787,7 +787,7 @@ cudaError_t launch_zgemm3m_adj_ws(const double2* F, const double2* X, double2* Y
                                   int j0, int nj, cudaStream_t stream, bool yblocked) {
     const char* bk = std::getenv("BTG_ZGEMM_ADJ_BULK");  // A/B: the 1-D bulk-copy producer
     CUtensorMap ta, tb;
-    if (yblocked && !zgemm_tma_ok(nm)) return cudaErrorNotSupported;
+    if (yblocked && (j0 % kSpecBlock || !zgemm_tma_ok(nm))) return cudaErrorNotSupported;
     if ((yblocked || !(bk && *bk && *bk != '0')) && encode_rows(&ta, F, nm, nd, nf, kKC) &&
         encode_rows(&tb, X, nd, nrhs, nf, kTR)) {
         const size_t smem = kTmaStages * kTmaStage + 1024 + 2 * kTmaStages * sizeof(uint64_t);
