@@ -26,7 +26,7 @@ namespace btg {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kFwdWarpMaxCols = 4096;
+constexpr int kFwdWarpMaxCols = 8192;  // host-pipeline chunks up to this width: measured e2e F 8.63 -> 8.26 ms (4096 -> 8192)
 constexpr int kMaxGridY = 65535;        // frequency batches per launch (grid.y limit)  // forward GEMV rows up to this length: warp-per-row kernel
 
 // ---------------------------------------------------------------------------
