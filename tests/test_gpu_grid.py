@@ -236,3 +236,25 @@ def test_p2p_reduce_fused_into_c2r_matches_unfused(monkeypatch, grid, nt):
     assert R.rel_l2(f, R.apply_forward(spec, m)) <= 1e-12
     assert R.rel_l2(a, R.apply_adjoint(spec, d)) <= 1e-12
     assert R.rel_l2(h, R.gauss_newton_apply(spec, m, gs, 0.3, 1)) <= 1e-12
+
+
+def test_p2p_fused_reduce_with_empty_cells(monkeypatch):
+    """A grid with more rows than the ceiling partition fills (N_d = 5 on 4 rows:
+    the last row is empty): column groups fuse with an all-zero member, row
+    groups whose member 0 is empty fall back to copies + adds; the results
+    equal the unfused path bit for bit and the oracle."""
+    from paper_2407_13066_b200.distributed import Partition
+
+    nd, nm, nt = 5, 12, 64
+    blocks, m, d = R.random_problem(43, nd, nm, nt)
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("BTG_GRID_FUSED", fused)
+        with Partition(blocks, (4, 2)) as p:
+            out[fused] = (p.forward(m), p.adjoint(d), p.hessian(m, alpha=0.2))
+    monkeypatch.delenv("BTG_GRID_FUSED", raising=False)
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+    spec = R.setup_full(blocks)
+    assert R.rel_l2(out["1"][0], R.apply_forward(spec, m)) <= 1e-12
+    assert R.rel_l2(out["1"][1], R.apply_adjoint(spec, d)) <= 1e-12
