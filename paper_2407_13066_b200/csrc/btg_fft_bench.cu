@@ -81,9 +81,29 @@ struct Run {
         constexpr bool tma_r = fast::UseTmaR2C<N>::value;
 #endif
         auto r2c = tma_r ? fast::k_r2c_tma<N, CPBR> : pf_r ? fast::k_r2c_pf<N, CPBR> : fast::k_r2c_fast<N, CPBR>;
-        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
         constexpr size_t smem_r = tma_r ? fast::smem_bytes_tma<N, CPBR>() : fast::smem_dir<N, CPBR, true>();
+#ifdef BENCH_BLOCKED
+        // the multi-RHS pipeline's channel-blocked spectrum: TMA R2C -> k_c2r_tma
+        static_assert(fast::c2r_tma_ok<N, CPBC>(), "blocked C2R needs the TMA plan");
+        constexpr bool c2r_persist = true;
+        const long long fs = kBlockedFs;
+#ifdef BENCH_LIGHT
+        constexpr bool light = true;
+#else
+        constexpr bool light = false;
+#endif
+        auto c2r = fast::k_c2r_tma<N, CPBC, light>;
+        constexpr size_t smem_c = fast::smem_bytes_c2r_tma<N, CPBC, light>();
+#else
+        constexpr bool c2r_persist = pf_c;
+        const long long fs = C;
+#ifdef BENCH_LIGHT
+        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC, true> : fast::k_c2r_fast<N, CPBC>;
+#else
+        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
+#endif
         constexpr size_t smem_c = fast::smem_dir<N, CPBC, false>();
+#endif
         CK(cudaFuncSetAttribute(r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
         CK(cudaFuncSetAttribute(c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
         int occ_r = 1, occ_c = 1, sms = 148;
@@ -92,7 +112,7 @@ struct Run {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, c2r, P::TPC * CPBC, smem_c);
         const int groups_r = (C + CPBR - 1) / CPBR, groups_c = (C + CPBC - 1) / CPBC;
         const int grid_r = (pf_r || tma_r) ? std::min(groups_r, occ_r * sms) : groups_r;
-        const int grid_c = pf_c ? std::min(groups_c, occ_c * sms) : groups_c;
+        const int grid_c = c2r_persist ? std::min(groups_c, occ_c * sms) : groups_c;
         C2REpilogue epi{};
         cudaEvent_t e0, e1, e2;
         cudaEventCreate(&e0);
@@ -101,9 +121,9 @@ struct Run {
         float tr = 0, tc = 0;
         for (int r = -2; r < reps; ++r) {
             cudaEventRecord(e0);
-            r2c<<<grid_r, P::TPC * CPBR, smem_r>>>(x, N, X, C, C, tabs, R2CBlockMax{});
+            r2c<<<grid_r, P::TPC * CPBR, smem_r>>>(x, N, X, fs, C, tabs, R2CBlockMax{});
             cudaEventRecord(e1);
-            c2r<<<grid_c, P::TPC * CPBC, smem_c>>>(X, C, y, N, C, tabs, epi);
+            c2r<<<grid_c, P::TPC * CPBC, smem_c>>>(X, fs, y, N, C, tabs, epi);
             cudaEventRecord(e2);
             CK(cudaEventSynchronize(e2));
             float a, b;
@@ -127,8 +147,8 @@ struct Run {
         const double bytes = 8.0 * nx + 16.0 * nf;
         std::printf(
             "{\"N_t\": %d, \"channels\": %d, \"cpb\": %d, \"r2c_ms\": %.4f, \"r2c_tbs\": %.3f, \"c2r_ms\": %.4f, "
-            "\"c2r_tbs\": %.3f, \"roundtrip_rel_l2\": %.3e}\n",
-            N, C, CPBR * 100 + CPBC, tr, bytes / tr / 1e9, tc, bytes / tc / 1e9, std::sqrt(num / den));
+            "\"c2r_tbs\": %.3f, \"roundtrip_rel_l2\": %.3e, \"occ\": [%d, %d], \"blocked\": %d}\n",
+            N, C, CPBR * 100 + CPBC, tr, bytes / tr / 1e9, tc, bytes / tc / 1e9, std::sqrt(num / den), occ_r, occ_c, (int)(fs < 0));
         cudaFree(x);
         cudaFree(y);
         cudaFree(X);
@@ -140,6 +160,13 @@ int main(int argc, char** argv) {
     const int n = argc > 1 ? std::atoi(argv[1]) : 1024;
     const int C = argc > 2 ? std::atoi(argv[2]) : 524288;
     const int reps = argc > 3 ? std::atoi(argv[3]) : 10;
+#ifdef BENCH_BLOCKED
+    if (n != 1024) {
+        std::printf("{\"error\": \"blocked mode: N_t = 1024 only\"}\n");
+        return 1;
+    }
+    Run<1024>::go(C, reps);
+#else
     switch (n) {
         case 64: Run<64>::go(C, reps); break;
         case 128: Run<128>::go(C, reps); break;
@@ -153,5 +180,6 @@ int main(int argc, char** argv) {
         case 4096: Run<4096>::go(C, reps); break;
         default: std::printf("{\"error\": \"unsupported N_t %d\"}\n", n); return 1;
     }
+#endif
     return 0;
 }

@@ -112,7 +112,17 @@ constexpr int kMinBlocksC2R = min_blocks(FastPlan<N>::RES_C2R, FastPlan<N>::TPC 
 #endif
 
 __host__ __device__ constexpr int pad_idx(int p) { return p + (p >> 4); }
-__host__ __device__ constexpr int chan_stride(int n) { return pad_idx(n) + 2; }
+// Channel-buffer stride (double2): the CPB channel buffers a quarter-warp touches
+// start in distinct bank groups — stride = 8 / CPB (mod 8) for CPB <= 8, 1 for
+// wider groups (8 channels of one butterfly per quarter-warp). N_t = 1000 at 2
+// channels per CTA had both channels on the same banks (1064 = 0 mod 8).
+template <int CPB>
+__host__ __device__ constexpr int chan_stride(int n) {
+    const int base = pad_idx(n) + 2;
+    const int want = CPB >= 8 ? 1 : (8 / CPB) % 8;
+    return CPB == 1 ? base : base + ((want - base) % 8 + 8) % 8;
+}
+static_assert(chan_stride<4>(1024) == 1090, "the N_t = 1024 layout is unchanged");
 constexpr int kTwLo = 32;
 
 template <int N>
@@ -120,7 +130,7 @@ __host__ __device__ constexpr int tw_hi_count() { return (N + kTwLo - 1) / kTwLo
 
 template <int N, int CPB>
 __host__ __device__ constexpr size_t smem_bytes() {
-    return sizeof(double2) * ((size_t)CPB * chan_stride(N) + 2 * kTwLo + 2 * tw_hi_count<N>() + 2);
+    return sizeof(double2) * ((size_t)CPB * chan_stride<CPB>(N) + 2 * kTwLo + 2 * tw_hi_count<N>() + 2);
 }
 
 // W^e for W = exp(SIGN * 2 pi i / n_tw) from the split table (lo[e % 32] * hi[e / 32]).
@@ -577,7 +587,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                int channels, FastTables tabs, R2CBlockMax bm) {
     using P = FastPlan<N>;
     using RL = typename P::R2C;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
@@ -714,7 +724,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                int channels, FastTables tabs, C2REpilogue epi) {
     using P = FastPlan<N>;
     using RL = typename P::C2R;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
@@ -892,24 +902,35 @@ template <int N, int CPB>
 __host__ __device__ constexpr bool c2r_tma_ok() {
     return CPB == kSpecBlock &&
            (N / last_radix(typename FastPlan<N>::C2R{}) + FastPlan<N>::TPC - 1) / FastPlan<N>::TPC == 1 &&
-           (size_t)(N + 1) * CPB <= (size_t)CPB * chan_stride(N);
+           (size_t)(N + 1) * CPB <= (size_t)CPB * chan_stride<CPB>(N);
 }
 #ifndef BTG_C2R_TMA_STAGE
 #define BTG_C2R_TMA_STAGE 1
 #endif
 constexpr bool kC2RTmaStage = BTG_C2R_TMA_STAGE;
-template <int N, int CPB>
+// The LIGHT instantiation (no prefetched per-sample epilogue operands: <= 128
+// registers) runs two CTAs per SM with the block landing in the channel buffers
+// (the copy overlaps the other CTA's passes); the full-epilogue one (176
+// registers, one CTA per SM) keeps the separate staging block. Measured at
+// 524288 channels (profiles/r02s4_fft_c2r_light.md): 3.03 ms (full, staged) ->
+// 2.79 (light, staged, one CTA) -> 2.73 (light, aliased, two CTAs).
+template <bool LIGHT>
+constexpr bool c2r_tma_stage() { return LIGHT ? false : kC2RTmaStage; }
+template <int N, int CPB, bool LIGHT = false>
 __host__ __device__ constexpr size_t smem_bytes_c2r_tma() {
-    return smem_dir<N, CPB, false>() + 16 + (kC2RTmaStage ? sizeof(double2) * (N + 1) * CPB : 0);
+    return smem_dir<N, CPB, false>() + 16 + (c2r_tma_stage<LIGHT>() ? sizeof(double2) * (N + 1) * CPB : 0);
 }
-template <int N, int CPB>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
+// LIGHT: no per-sample epilogue operands (epi.v == nullptr, gamma_mode != 2) —
+// the instantiation without the prefetched operand registers.
+template <int N, int CPB, bool LIGHT = false>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, LIGHT ? 2 : BTG_C2R_TMA_MINB)
     k_c2r_tma(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
     (void)in_fs;  // always channel-blocked
+    constexpr bool kStage = c2r_tma_stage<LIGHT>();
     using P = FastPlan<N>;
     using RL = typename P::C2R;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     extern __shared__ double2 sm[];
     double2* lo = sm + CPB * CS;
@@ -927,10 +948,10 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
     const int tc = threadIdx.x / CPB;
     double2* s = sm + b * CS;
     // the group's channel-blocked input block lands where the channel buffers are
-    // kC2RTmaStage: a separate staging block (the next group's copy overlaps all
+    // kStage: a separate staging block (the next group's copy overlaps all
     // passes) or the channel buffers themselves (copy overlaps the epilogue only)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + smem_dir<N, CPB, false>() / sizeof(double2));
-    double2* stage_buf = kC2RTmaStage ? reinterpret_cast<double2*>(bar + 2) : sm;
+    double2* stage_buf = kStage ? reinterpret_cast<double2*>(bar + 2) : sm;
     const double2* stage = stage_buf;
     const int groups = channels / CPB;
     constexpr uint32_t kBlockBytes = (uint32_t)((N + 1) * CPB * sizeof(double2));
@@ -1005,7 +1026,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
         // every pair read from the staged block before any buffer write (aliased
         // stage) / before the next block is requested (separate stage)
         __syncthreads();
-        if (kC2RTmaStage && threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
+        if (kStage && threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
 #pragma unroll
         for (int uf = 0; uf < UF; ++uf) {
             const int u = tc + uf * TPC;
@@ -1030,7 +1051,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
     constexpr int BF = (NB + TPC - 1) / TPC;
     {
     double* orow = out + (long long)c * out_cs;
-    const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+    const double* vrow = (!LIGHT && epi.v) ? epi.v + (long long)c * out_cs : nullptr;
     const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
 #pragma unroll
     for (int bf = 0; bf < BF; ++bf) {
@@ -1048,7 +1069,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
                 er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
                 el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
                 eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
-                eg[q] = (epi.gamma_mode == 2 && ok)
+                eg[q] = (!LIGHT && epi.gamma_mode == 2 && ok)
                             ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
                             : make_double2(1.0, 1.0);
             }
@@ -1056,7 +1077,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
             #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = s[pad_idx(j + q * NB)];
             static_assert(BF == 1, "one last-pass butterfly per thread: the refill follows its reads");
-            if (!kC2RTmaStage) {
+            if (!kStage) {
                 __syncthreads();  // every channel buffer read: the next block may land
                 if (threadIdx.x == 0 && g + (int)gridDim.x < groups) issue(g + gridDim.x);
             }
@@ -1071,7 +1092,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, BTG_C2R_TMA_MINB)
                     const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
                     y0 *= g;
                     y1 *= g;
-                } else if (epi.gamma_mode == 2) {
+                } else if (!LIGHT && epi.gamma_mode == 2) {
                     y0 *= eg[q].x;
                     y1 *= eg[q].y;
                 }
@@ -1112,7 +1133,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
                int channels, FastTables tabs, R2CBlockMax bm) {
     using P = FastPlan<N>;
     using RL = typename P::R2C;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     constexpr int R1 = first_radix(RL{});
     constexpr int NB1 = N / R1;
@@ -1259,13 +1280,23 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 
 // c2r, persistent: the (X_k, X_{N-k}) pairs of the next group's first pass are
 // loaded into registers while this group finishes.
-template <int N, int CPB>
-__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
+// LIGHT as k_c2r_tma: no prefetched per-sample epilogue operands. N_t = 1024 at
+// 32768 channels (profiles/r02s4_fft_c2r_light.md): 255 -> 220 registers, C2R
+// 0.247 -> 0.222 ms at one CTA per SM; forcing two CTAs (128 registers) spills
+// and is slower (0.282 ms), three (80) much slower (0.588).
+#ifndef BTG_C2R_PF_LIGHT_MINB
+#define BTG_C2R_PF_LIGHT_MINB 1
+#endif
+template <int N, int CPB, bool LIGHT>
+constexpr int kMinBlocksC2RPf =
+    (LIGHT && kMinBlocksC2R<N, CPB> < BTG_C2R_PF_LIGHT_MINB) ? BTG_C2R_PF_LIGHT_MINB : kMinBlocksC2R<N, CPB>;
+template <int N, int CPB, bool LIGHT = false>
+__global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, (kMinBlocksC2RPf<N, CPB, LIGHT>))
     k_c2r_pf(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
     using P = FastPlan<N>;
     using RL = typename P::C2R;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     constexpr int R1 = first_radix(RL{});
     constexpr int NB1 = N / R1;
@@ -1393,7 +1424,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
         constexpr int BF = (NB + TPC - 1) / TPC;
         if (live) {
             double* orow = out + (long long)c * out_cs;
-            const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+            const double* vrow = (!LIGHT && epi.v) ? epi.v + (long long)c * out_cs : nullptr;
             const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
 #pragma unroll
             for (int bf = 0; bf < BF; ++bf) {
@@ -1411,7 +1442,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                         er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
                         el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
                         eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
-                        eg[q] = (epi.gamma_mode == 2 && ok)
+                        eg[q] = (!LIGHT && epi.gamma_mode == 2 && ok)
                                     ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
                                     : make_double2(1.0, 1.0);
                     }
@@ -1429,7 +1460,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                             const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
                             y0 *= g;
                             y1 *= g;
-                        } else if (epi.gamma_mode == 2) {
+                        } else if (!LIGHT && epi.gamma_mode == 2) {
                             y0 *= eg[q].x;
                             y1 *= eg[q].y;
                         }
@@ -1511,7 +1542,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, 2)
               int channels, FastTables tabs, R2CBlockMax bm) {
     using P = FastPlan<N>;
     using RL = typename P::R2C;
-    constexpr int TPC = P::TPC, CS = chan_stride(N);
+    constexpr int TPC = P::TPC, CS = chan_stride<CPB>(N);
     constexpr int HI = tw_hi_count<N>();
     constexpr int R1 = first_radix(RL{});
     constexpr int NB1 = N / R1;

@@ -892,8 +892,10 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
             // channel-blocked input: one bulk copy per 4-channel group (k_c2r_tma)
             if (in_fs < 0 && !std::getenv("BTG_C2R_NO_TMA") && !epi.npeers) {
                 if (channels % CPB) return cudaErrorNotSupported;
-                constexpr size_t smem_t = fast::smem_bytes_c2r_tma<N, CPB>();
-                auto kt = fast::k_c2r_tma<N, CPB>;
+                const bool light = !epi.v && epi.gamma_mode != 2;  // no per-sample operands
+                const size_t smem_t =
+                    light ? fast::smem_bytes_c2r_tma<N, CPB, true>() : fast::smem_bytes_c2r_tma<N, CPB, false>();
+                auto kt = light ? fast::k_c2r_tma<N, CPB, true> : fast::k_c2r_tma<N, CPB, false>;
                 cudaError_t e = set_smem(kt, smem_t);
                 if (e != cudaSuccess) return e;
                 const int grid = persistent_grid(kt, P::TPC * CPB, smem_t, channels / CPB);
@@ -904,8 +906,10 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         }
         // the grid reduce fused into the stores (epi.npeers): its own instantiation,
         // so the other C2Rs carry no peer-load code (it cost them 10-17 %)
+        const bool light = !epi.v && epi.gamma_mode != 2;  // no per-sample operands
         auto kern = epi.npeers ? fast::k_c2r_fast<N, CPB, true>
-                               : (P::PF_C2R ? fast::k_c2r_pf<N, CPB> : fast::k_c2r_fast<N, CPB>);
+                               : (P::PF_C2R ? (light ? fast::k_c2r_pf<N, CPB, true> : fast::k_c2r_pf<N, CPB, false>)
+                                            : fast::k_c2r_fast<N, CPB>);
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         const int groups = (channels + CPB - 1) / CPB;

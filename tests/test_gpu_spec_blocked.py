@@ -29,6 +29,7 @@ def test_blocked_equals_frequency_major(btg, monkeypatch, nd, nm, nrhs):
     M = rng.uniform(-1, 1, size=(nrhs, nm, nt))
     D = rng.uniform(-1, 1, size=(nrhs, nd, nt))
     gam = torch.from_numpy(rng.uniform(0.5, 2.0, nd)).cuda()
+    gam_s = torch.from_numpy(rng.uniform(0.5, 2.0, (nd, nt))).cuda()
     out = {}
     with btg.setup(blocks) as op:
         for mode in ("1", "0"):
@@ -37,13 +38,18 @@ def test_blocked_equals_frequency_major(btg, monkeypatch, nd, nm, nrhs):
             a = op.apply_adjoint(torch.from_numpy(D).cuda()).cpu().numpy()
             h = op.hessian_apply(torch.from_numpy(M).cuda(), alpha=0.2, reg="temporal-laplacian",
                                  gamma_inv=gam).cpu().numpy()
-            out[mode] = (f, a, h)
+            # per-sample Gamma^-1 without a regulariser: the C2R's full-epilogue
+            # instantiation with no alpha R v operand (the others take the light one)
+            hs = op.hessian_apply(torch.from_numpy(M).cuda(), alpha=0.0, gamma_inv=gam_s).cpu().numpy()
+            out[mode] = (f, a, h, hs)
         monkeypatch.delenv("BTG_SPEC_BLOCKED", raising=False)
     for x, y in zip(out["1"], out["0"]):
         assert np.array_equal(x, y)
     spec = R.setup_full(blocks)
-    f, a, h = out["1"]
+    f, a, h, hs = out["1"]
     for r in (0, nrhs - 1):
+        want_s = R.gauss_newton_apply(spec, M[r], gam_s.cpu().numpy(), 0.0, 0)
+        assert R.rel_l2(hs[r], want_s) <= 1e-12
         assert R.rel_l2(f[r], R.apply_forward(spec, M[r])) <= 1e-12
         assert R.rel_l2(a[r], R.apply_adjoint(spec, D[r])) <= 1e-12
         want = R.gauss_newton_apply(spec, M[r], gam.cpu().numpy(), 0.2, 1)
