@@ -98,7 +98,7 @@ struct Run {
         constexpr bool c2r_persist = pf_c;
         const long long fs = C;
 #ifdef BENCH_LIGHT
-        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC, true> : fast::k_c2r_fast<N, CPBC>;
+        auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC, true> : fast::k_c2r_fast<N, CPBC, false, true>;
 #else
         auto c2r = pf_c ? fast::k_c2r_pf<N, CPBC> : fast::k_c2r_fast<N, CPBC>;
 #endif

@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksR2C<N, CPB>)
 // ---------------------------------------------------------------------------
 // c2r: frequency-major in[k*in_fs + c] -> SOTI rows out[c*out_cs + t], t < N
 // ---------------------------------------------------------------------------
-template <int N, int CPB, bool PEERS = false>
+template <int N, int CPB, bool PEERS = false, bool LIGHT = false>
 __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     k_c2r_fast(const double2* __restrict__ in, long long in_fs, double* __restrict__ out, long long out_cs,
                int channels, FastTables tabs, C2REpilogue epi) {
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
     double dacc = 0.0;  // folded dot (epi.dot_out)
     if (live) {
     double* orow = out + (long long)c * out_cs;
-    const double* vrow = epi.v ? epi.v + (long long)c * out_cs : nullptr;
+    const double* vrow = (!LIGHT && epi.v) ? epi.v + (long long)c * out_cs : nullptr;
     const double* drow = epi.dot_out ? epi.dot_v + (long long)c * out_cs : nullptr;
 #pragma unroll
     for (int bf = 0; bf < BF; ++bf) {
@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                 er[q] = (vrow && ok) ? __ldg(reinterpret_cast<const double2*>(vrow) + p) : make_double2(0.0, 0.0);
                 el[q] = (vrow && ok && epi.reg_kind == 1 && t0 > 0) ? __ldg(vrow + t0 - 1) : 0.0;
                 eh[q] = (vrow && ok && epi.reg_kind == 1 && t0 + 2 < N) ? __ldg(vrow + t0 + 2) : 0.0;
-                eg[q] = (epi.gamma_mode == 2 && ok)
+                eg[q] = (!LIGHT && epi.gamma_mode == 2 && ok)
                             ? __ldg(reinterpret_cast<const double2*>(epi.gamma + (long long)(c % epi.gamma_dim) * N) + p)
                             : make_double2(1.0, 1.0);
             }
@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(FastPlan<N>::TPC * CPB, kMinBlocksC2R<N, CPB>)
                     const double g = __ldg(epi.gamma + (c % epi.gamma_dim));
                     y0 *= g;
                     y1 *= g;
-                } else if (epi.gamma_mode == 2) {
+                } else if (!LIGHT && epi.gamma_mode == 2) {
                     y0 *= eg[q].x;
                     y1 *= eg[q].y;
                 }

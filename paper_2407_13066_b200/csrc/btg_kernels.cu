@@ -909,7 +909,8 @@ cudaError_t c2r_fast_nc(const double2* in, long long in_fs, double* out, long lo
         const bool light = !epi.v && epi.gamma_mode != 2;  // no per-sample operands
         auto kern = epi.npeers ? fast::k_c2r_fast<N, CPB, true>
                                : (P::PF_C2R ? (light ? fast::k_c2r_pf<N, CPB, true> : fast::k_c2r_pf<N, CPB, false>)
-                                            : fast::k_c2r_fast<N, CPB>);
+                                            : (light ? fast::k_c2r_fast<N, CPB, false, true>
+                                                     : fast::k_c2r_fast<N, CPB, false, false>));
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         const int groups = (channels + CPB - 1) / CPB;
