@@ -669,6 +669,32 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         // per-lane output offsets: Y[f][r][j] (or channel-blocked [c/4][f][c%4],
         // c = r N_m + j, N_m and j0 multiples of 4): base + r * rstride + col(j)
         const size_t ftile = yblocked ? (size_t)kSpecBlock * d.f : (size_t)d.f * nrhs * nm;
+        if (d.r0 + kTR <= nrhs && d.j0 + kTM <= jend) {
+            // full tile: one base address per lane, every store at a constant
+            // offset from it — (mt, h) steps 8 columns (two spectral blocks when
+            // blocked), (nt, q) steps right-hand sides; no per-store index math
+            // or bounds branches (they were ~400 instructions per tile per lane)
+            const int jj0 = d.j0 + wm * (16 * kMT) + g;
+            const size_t col0 = yblocked ? (size_t)(jj0 / kSpecBlock) * kSpecBlock * nf + (jj0 % kSpecBlock)
+                                         : (size_t)jj0;
+            const size_t j8 = yblocked ? (size_t)(8 / kSpecBlock) * kSpecBlock * nf : (size_t)8;
+            double2* yb = Y + ftile + col0 + (size_t)(d.r0 + wn * 16 + 2 * tig) * rstride;
+#pragma unroll
+            for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double2* yc = yb + (size_t)(2 * mt + h) * j8;
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int cc = 2 * h + q;
+                            yc[(size_t)(8 * nt + q) * rstride] =
+                                make_double2(p1[mt][nt][cc] + p2[mt][nt][cc], p3[mt][nt][cc] - p1[mt][nt][cc] + p2[mt][nt][cc]);
+                        }
+                }
+            continue;
+        }
 #pragma unroll
         for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
