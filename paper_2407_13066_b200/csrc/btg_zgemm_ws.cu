@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_zgemm3m_adj_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       double2* __restrict__ Y, int nf, int nd, int nm, int nrhs, int jbase, int jend,
-                      bool yblocked) {
+                      bool yblocked, bool chunked) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     const uint32_t base_u = (umma::smem_u32(smraw) + 1023u) & ~1023u;
     unsigned char* base = smraw + (base_u - umma::smem_u32(smraw));
@@ -604,6 +604,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     umma::mbar_expect_tx(full + st, kTmaStage);
                     const uint32_t sa = base_u + st * kTmaStage;
                     const int kc = kt * kKC;
+                    if (chunked) {
+                        // one box each: A = 16 chunks of 8 complex x 16 rows, B = 2 chunks x 32 rows
+                        tma_load4(sa, &tmA, 0, kc, d.j0 / 8, d.f, full + st, pol_a);
+                        tma_load4(sa + kTmaA, &tmB, 0, d.r0, kc / 8, d.f, full + st, pol_b);
+                        continue;
+                    }
 #pragma unroll
                     for (int b = 0; b < kTM / 8; ++b)
                         tma_load3(sa + b * 2048, &tmA, 2 * (d.j0 + 8 * b), kc, d.f, full + st, pol_a);
@@ -748,6 +754,23 @@ bool encode_rows(CUtensorMap* m, const void* ptr, int cols, int rows, int planes
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [planes][rows][cols complex] as (16 doubles, rows, cols / 8 chunks, planes): ONE
+// box of box_rows rows x box_chunks 8-complex chunks lands chunk-major,
+// [chunk][row][128 B], 128-byte swizzled — the layout of box_chunks separate
+// encode_rows boxes side by side (the adjoint's A stage in one copy, not 16)
+bool encode_chunks(CUtensorMap* m, const void* ptr, int cols, int rows, int planes, int box_rows,
+                   int box_chunks) {
+    const EncodeTiled fn = encode_fn();
+    if (!fn || cols % 8) return false;
+    const cuuint64_t dims[4] = {16, (cuuint64_t)rows, (cuuint64_t)cols / 8, (cuuint64_t)planes};
+    const cuuint64_t strides[3] = {(cuuint64_t)cols * 16, 128, (cuuint64_t)cols * 16 * rows};
+    const cuuint32_t box[4] = {16, (cuuint32_t)box_rows, (cuuint32_t)box_chunks, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // X channel-blocked ([r nm + j] / 4, f, (r nm + j) % 4): dims (8 doubles, nf, nm / 4, nrhs), box (8, 1, 2, 32)
 bool encode_blocked(CUtensorMap* m, const void* ptr, int nm, int nrhs, int nf) {
     const EncodeTiled fn = encode_fn();
@@ -814,15 +837,20 @@ cudaError_t launch_zgemm3m_adj_ws(const double2* F, const double2* X, double2* Y
     const char* bk = std::getenv("BTG_ZGEMM_ADJ_BULK");  // A/B: the 1-D bulk-copy producer
     CUtensorMap ta, tb;
     if (yblocked && (j0 % kSpecBlock || !zgemm_tma_ok(nm))) return cudaErrorNotSupported;
-    if ((yblocked || !(bk && *bk && *bk != '0')) && encode_rows(&ta, F, nm, nd, nf, kKC) &&
-        encode_rows(&tb, X, nd, nrhs, nf, kTR)) {
+    // one TMA box per operand and stage when N_m, N_d and the column origin allow it
+    const char* sb = std::getenv("BTG_ZGEMM_ADJ_BOXES");  // A/B: 16 + 2 boxes per stage
+    const bool chunked = !(sb && *sb && *sb != '0') && nm % 8 == 0 && nd % 8 == 0 && j0 % 8 == 0 &&
+                         encode_chunks(&ta, F, nm, nd, nf, kKC, kTM / 8) && encode_chunks(&tb, X, nd, nrhs, nf, kTR, 2);
+    if ((yblocked || !(bk && *bk && *bk != '0')) &&
+        (chunked || (encode_rows(&ta, F, nm, nd, nf, kKC) && encode_rows(&tb, X, nd, nrhs, nf, kTR)))) {
         const size_t smem = kTmaStages * kTmaStage + 1024 + 2 * kTmaStages * sizeof(uint64_t);
         cudaError_t e =
             cudaFuncSetAttribute(k_zgemm3m_adj_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const long long tiles = (long long)nf * ((nj + kTM - 1) / kTM) * ((nrhs + kTR - 1) / kTR);
         const int grid = (int)std::min<long long>(tiles, sm_count());
-        k_zgemm3m_adj_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, j0 + nj, yblocked);
+        k_zgemm3m_adj_tma<<<grid, kWsThreads, smem, stream>>>(ta, tb, Y, nf, nd, nm, nrhs, j0, j0 + nj, yblocked,
+                                                              chunked);
         return cudaGetLastError();
     }
     const size_t smem = kAdjStages * kAdjStage + 2 * kAdjStages * sizeof(uint64_t);
