@@ -77,6 +77,7 @@ constexpr size_t kFftSmemBudget = 200 * 1024;      // per CTA
 constexpr size_t kFftSmemTarget = 100 * 1024;      // aim for 2 CTAs / SM
 constexpr size_t kHostStageBytes = 512ull << 20;   // host->device setup staging
 constexpr size_t kScratchCapBytes = 1ull << 30;    // global FFT scratch bound
+constexpr size_t kSetupSotiBytes = 1ull << 30;     // setup: transposed (SOTI) slab buffer
 
 }  // namespace
 
@@ -1043,10 +1044,41 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
     const size_t rows = i1 - i0;
     const size_t slab_channels = rows * op->nm;
     const long long out_fs = (long long)(op->nd * op->nm);
+    // FP64 with a compile-time FFT plan: transpose the TOSI slab to SOTI rows in a
+    // bounded device buffer, then the vector R2C (frequency-major stores into F-hat);
+    // otherwise (FP32 F-hat, lengths without a plan, BTG_SETUP_GENERIC, or no room
+    // for the buffer) the generic strided R2C. Each channel's transform is the
+    // vector R2C's, wherever the channel lands.
+    double* soti = nullptr;
+    size_t soti_channels = 0;
+    if (op->fast_ok && op->precision == BTG_F64 && !std::getenv("BTG_SETUP_GENERIC")) {
+        soti_channels = std::min(slab_channels, std::max<size_t>(1, kSetupSotiBytes / (op->nt * sizeof(double))));
+        if (cudaMalloc(&soti, soti_channels * op->nt * sizeof(double)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            soti = nullptr;
+        }
+    }
+    struct SotiFree {
+        double* p;
+        ~SotiFree() {
+            if (p) cudaFree(p);
+        }
+    } soti_free{soti};
     auto launch = [&](const double* src, long long in_ts, size_t c_begin, size_t count) -> btg_status {
         StageClock clk(op, &op->counters.forward_fft);
         cudaError_t e;
         const size_t off = i0 * op->nm + c_begin;
+        if (soti) {
+            for (size_t c = 0; c < count; c += soti_channels) {
+                const size_t cnt = std::min(soti_channels, count - c);
+                BTG_CUDA(btg::launch_tosi_to_soti(src + c, in_ts, soti, (int)op->nt, (long long)cnt, op->stream));
+                BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, soti, (long long)op->nt,
+                                                  static_cast<double2*>(op->F) + off + c, out_fs, (int)cnt, op->fast,
+                                                  op->stream));
+                op->counters.launches += 2;
+            }
+            return BTG_OK;
+        }
         if (op->precision == BTG_F64)
             e = btg::launch_r2c<double2>(src, 1, in_ts, static_cast<double2*>(op->F) + off, out_fs, 1,
                                          (int)count, (int)op->nt, op->plan, op->fft_batch_setup, op->stream,

@@ -214,6 +214,10 @@ cudaError_t launch_reg_apply(double* y, const double* v, size_t rows, int nt, in
 cudaError_t launch_reg_apply_inverse(double* x, const double* b, const double* pivot, const double* scratch,
                                      size_t rows, int nt, cudaStream_t stream);
 
+// SOTI rows out[c * nt + t] from a TOSI slab in[t * ts + c], c < cnt, t < nt
+cudaError_t launch_tosi_to_soti(const double* in, long long ts, double* out, int nt, long long cnt,
+                                cudaStream_t stream);
+
 // out[(a*nb + b)*nc + c] = uniform(seed ^ (offset + a*sa + b*sb + c))
 cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                 uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream);
