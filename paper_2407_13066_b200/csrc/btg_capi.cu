@@ -1049,13 +1049,20 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
     // otherwise (FP32 F-hat, lengths without a plan, BTG_SETUP_GENERIC, or no room
     // for the buffer) the generic strided R2C. Each channel's transform is the
     // vector R2C's, wherever the channel lands.
+    // FP32 F-hat: the vector R2C writes a complex128 block (frequency-major, stride
+    // = the chunk's channels) after the SOTI rows, rounded into F-hat by
+    // k_spec_to_f32 — the same per-element rounding as the strided kernel.
     double* soti = nullptr;
+    double2* spec64 = nullptr;
     size_t soti_channels = 0;
-    if (op->fast_ok && op->precision == BTG_F64 && !std::getenv("BTG_SETUP_GENERIC")) {
+    if (op->fast_ok && !std::getenv("BTG_SETUP_GENERIC")) {
         soti_channels = std::min(slab_channels, std::max<size_t>(1, kSetupSotiBytes / (op->nt * sizeof(double))));
-        if (cudaMalloc(&soti, soti_channels * op->nt * sizeof(double)) != cudaSuccess) {
+        const size_t spec_bytes = op->precision == BTG_F64 ? 0 : soti_channels * op->nf * sizeof(double2);
+        if (cudaMalloc(&soti, soti_channels * op->nt * sizeof(double) + spec_bytes) != cudaSuccess) {
             (void)cudaGetLastError();
             soti = nullptr;
+        } else if (spec_bytes) {
+            spec64 = reinterpret_cast<double2*>(soti + soti_channels * op->nt);
         }
     }
     struct SotiFree {
@@ -1072,10 +1079,18 @@ btg_status btg_setup_rows(btg_op op, const double* blocks, size_t i0, size_t i1,
             for (size_t c = 0; c < count; c += soti_channels) {
                 const size_t cnt = std::min(soti_channels, count - c);
                 BTG_CUDA(btg::launch_tosi_to_soti(src + c, in_ts, soti, (int)op->nt, (long long)cnt, op->stream));
-                BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, soti, (long long)op->nt,
-                                                  static_cast<double2*>(op->F) + off + c, out_fs, (int)cnt, op->fast,
-                                                  op->stream));
-                op->counters.launches += 2;
+                if (spec64) {
+                    BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, soti, (long long)op->nt, spec64, (long long)cnt,
+                                                      (int)cnt, op->fast, op->stream));
+                    BTG_CUDA(btg::launch_spec_to_f32(spec64, (long long)cnt, (int)op->nf,
+                                                     static_cast<float2*>(op->F) + off + c, out_fs, op->stream));
+                    op->counters.launches += 3;
+                } else {
+                    BTG_CUDA(btg::launch_r2c_vec_fast((int)op->nt, soti, (long long)op->nt,
+                                                      static_cast<double2*>(op->F) + off + c, out_fs, (int)cnt,
+                                                      op->fast, op->stream));
+                    op->counters.launches += 2;
+                }
             }
             return BTG_OK;
         }

@@ -825,6 +825,27 @@ __global__ void __launch_bounds__(256) k_tosi_to_soti(const double* __restrict__
     }
 }
 
+// FP32 F-hat setup: rows k of a frequency-major complex128 block (in[k * cnt + c])
+// rounded to complex64 at out[k * out_fs + c] (the same rounding as k_r2c<float2>'s
+// to_out)
+__global__ void k_spec_to_f32(const double2* __restrict__ in, long long cnt, float2* __restrict__ out,
+                              long long out_fs, long long total) {
+    for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
+         u += (long long)gridDim.x * blockDim.x) {
+        const long long k = u / cnt, c = u - k * cnt;
+        out[k * out_fs + c] = to_out<float2>(__ldcs(in + u));
+    }
+}
+
+cudaError_t launch_spec_to_f32(const double2* in, long long cnt, int nf, float2* out, long long out_fs,
+                               cudaStream_t stream) {
+    const long long total = cnt * (long long)nf;
+    if (total <= 0) return cudaSuccess;
+    const int grid = (int)std::min<long long>((total + 255) / 256, (long long)sm_count() * 16);
+    k_spec_to_f32<<<grid, 256, 0, stream>>>(in, cnt, out, out_fs, total);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tosi_to_soti(const double* in, long long ts, double* out, int nt, long long cnt,
                                 cudaStream_t stream) {
     if (cnt <= 0 || nt <= 0) return cudaSuccess;

@@ -218,6 +218,10 @@ cudaError_t launch_reg_apply_inverse(double* x, const double* b, const double* p
 cudaError_t launch_tosi_to_soti(const double* in, long long ts, double* out, int nt, long long cnt,
                                 cudaStream_t stream);
 
+// out[k * out_fs + c] = (complex64) in[k * cnt + c], k < nf, c < cnt
+cudaError_t launch_spec_to_f32(const double2* in, long long cnt, int nf, float2* out, long long out_fs,
+                               cudaStream_t stream);
+
 // out[(a*nb + b)*nc + c] = uniform(seed ^ (offset + a*sa + b*sb + c))
 cudaError_t launch_fill_uniform(double* out, size_t na, size_t nb, size_t nc, uint64_t seed, uint64_t offset,
                                 uint64_t sa, uint64_t sb, double lo, double hi, cudaStream_t stream);

@@ -63,3 +63,22 @@ def test_transposed_setup_placement_independent_at_scale(btg):
     spec = R.setup_full(b0)
     with btg.setup(np.ascontiguousarray(b0)) as small:
         assert R.rel_l2(small.spectrum(), spec[: nt + 1]) <= 1e-14
+
+
+@pytest.mark.parametrize("nt,nd,nm", [(1024, 3, 301), (4096, 2, 33)])
+def test_transposed_setup_fp32_fhat(btg, monkeypatch, nt, nd, nm):
+    """FP32 F-hat: the complex128 vector-R2C block rounded to complex64
+    (k_spec_to_f32) — within FP32 rounding of the oracle and of the generic
+    strided path (whose FP64 sums differ from the vector R2C's in the last bits,
+    so an element may round to the neighbouring float)."""
+    blocks, _, _ = R.random_problem(nt + 3 * nd, nd, nm, nt)
+    want = R.setup_full(blocks)[: nt + 1]
+    got = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BTG_SETUP_GENERIC", mode)
+        with btg.setup(blocks, precision=32) as op:
+            got[mode] = op.spectrum()
+    monkeypatch.delenv("BTG_SETUP_GENERIC", raising=False)
+    for mode in ("0", "1"):
+        assert R.rel_l2(got[mode], want) <= 1e-7
+    assert R.rel_l2(got["0"], got["1"]) <= 1e-7
